@@ -1,0 +1,420 @@
+// tcgen05 GEMM for the complex64 contraction steps (K2 on the tensor cores).
+//
+// A complex GEMM C[M,N] = A[M,K] B[K,N] (the `np.tensordot` -> cgemm of
+// tncut engine.py:129) is run as ONE real GEMM
+//     C'[M][2N] = A'[M][2K] x B'^T,   A' = interleaved A,
+//     B'[2n][2k..2k+1] = (br, -bi),  B'[2n+1][2k..2k+1] = (bi, br)
+// whose fp32 output rows are exactly the interleaved complex64 rows of C.
+// fp32 accuracy comes from a 2-term fp16 split with power-of-two scaling
+// (x s = hi + lo): C' = Ahi Blo + Alo Bhi + Ahi Bhi, three kind::f16 UMMAs
+// per K step into one fp32 TMEM accumulator.
+//
+// Structure (one CTA per SM, persistent over output tiles):
+//   warp 0  : TMA producer (4 tiles per stage: Ahi, Alo, Bhi, Blo), mbarrier ring
+//   warp 1  : single-thread tcgen05.mma issuer, commits to the ring / TMEM barriers
+//   warp 2  : TMEM allocator (512 columns = 2 partial accumulators of 128 x 256 fp32)
+//   warps 4-19: promotion + epilogue (TMEM partials -> fp32 registers -> global)
+#include "tnb_internal.h"
+
+#include <cuda.h>
+#include <cstdlib>
+#include <mutex>
+
+namespace tnb {
+namespace {
+
+constexpr int BM = 128;
+constexpr int BN = 256;
+constexpr int BK = 32;                       // fp16 elements per stage row (64 B, SWIZZLE_64B)
+constexpr int STAGES = 4;
+constexpr int A_TILE = BM * BK * 2;          // 8 KB
+constexpr int B_TILE = BN * BK * 2;          // 16 KB
+constexpr int STAGE_BYTES = 2 * A_TILE + 2 * B_TILE;
+constexpr int EPI_SPLIT = 4;                 // column groups per TMEM lane quadrant
+constexpr int EPI_THREADS = 128 * EPI_SPLIT; // 16 epilogue warps: 4 lane quadrants x 4 column groups
+constexpr int EPI_COLS = BN / EPI_SPLIT;     // fp32 register accumulator columns per epilogue thread
+constexpr int NUM_THREADS = 128 + EPI_THREADS;
+constexpr int TMEM_COLS = 512;
+constexpr int kDefaultChunkKb = 8;          // K blocks (of 32 fp16) per promotion chunk
+constexpr int GROUP_N = 8;                   // rasterisation: m-fastest within 8 n-tiles
+constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
+
+// instruction descriptor: F32 accum, F16 x F16, K-major both, M=128, N=256
+constexpr uint32_t IDESC = (1u << 4) | ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  const uint32_t addr = smem_u32(bar);
+  uint32_t ok = 0;
+  do {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(ok)
+        : "r"(addr), "r"(parity)
+        : "memory");
+  } while (!ok);
+}
+
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+__device__ __forceinline__ void tma_load_2d(void* smem_dst, const CUtensorMap* map, uint64_t* bar,
+                                            int c0, int c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4}], [%2];" ::"r"(smem_u32(smem_dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1)
+      : "memory");
+}
+
+__device__ __forceinline__ uint64_t make_desc_sw64(const void* smem_ptr) {
+  // K-major, SWIZZLE_64B: 8-row core groups 8*64 B apart (SBO), LBO unused.
+  const uint64_t addr = smem_u32(smem_ptr);
+  uint64_t d = 0;
+  d |= (addr >> 4) & 0x3FFFull;            // start address
+  d |= (uint64_t)(512 >> 4) << 32;          // stride byte offset
+  d |= 1ull << 46;                          // descriptor version (sm100)
+  d |= 4ull << 61;                          // layout: SWIZZLE_64B
+  return d;
+}
+
+__device__ __forceinline__ void umma_f16(uint32_t tmem_c, uint64_t da, uint64_t db, uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_c),
+      "l"(da), "l"(db), "r"(IDESC), "r"(acc));
+}
+
+__device__ __forceinline__ void umma_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                   smem_u32(bar))
+               : "memory");
+}
+
+__device__ __forceinline__ void tc_fence_after() {
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void tc_fence_before() {
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+}
+
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&r)[16]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 "
+      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
+        "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+
+__device__ __forceinline__ float scale_of(unsigned int bits) {
+  const float m = __uint_as_float(bits);
+  if (!(m > 0.f)) return 1.f;
+  int e;
+  frexpf(m, &e);
+  int p = 15 - e;
+  p = p > 126 ? 126 : (p < -126 ? -126 : p);
+  return ldexpf(1.f, p);
+}
+
+struct WorkCoord {
+  int split, mb, nb;
+};
+
+__device__ __forceinline__ WorkCoord decode(int w, int nm, int nn) {
+  const int per_split = nm * nn;
+  WorkCoord c;
+  c.split = w / per_split;
+  const int t = w - c.split * per_split;
+  const int group = t / (GROUP_N * nm);
+  const int idx = t - group * (GROUP_N * nm);
+  c.mb = idx % nm;
+  c.nb = group * GROUP_N + idx / nm;
+  return c;
+}
+
+// Accumulation: the tensor cores' fp32 accumulator loses precision over
+// thousands of K steps (measured ~15x the IEEE fp32 error growth).  K is
+// therefore processed in chunks of `chunk_kb` K blocks into one of two TMEM
+// partial accumulators; the epilogue warps promote every finished partial
+// into an IEEE fp32 register accumulator (DeepGEMM-style promotion), while
+// the MMA warp fills the other partial.
+__global__ void __launch_bounds__(NUM_THREADS, 1)
+gemm_f16x3_kernel(const __grid_constant__ CUtensorMap tm_ahi, const __grid_constant__ CUtensorMap tm_alo,
+                  const __grid_constant__ CUtensorMap tm_bhi, const __grid_constant__ CUtensorMap tm_blo,
+                  float* __restrict__ C, int M, int Np, int Kp, int splits, int k_per_split,
+                  int chunk_kb, const unsigned int* __restrict__ maxbits) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES);
+  uint64_t* empty_bar = full_bar + STAGES;
+  uint64_t* pfull_bar = empty_bar + STAGES;
+  uint64_t* pempty_bar = pfull_bar + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(pempty_bar + 2);
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const int nm = (M + BM - 1) / BM;
+  const int nn = (Np + BN - 1) / BN;
+  const int total = nm * nn * splits;
+
+  if (warp == 0 && lane == 0) {
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tm_ahi)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tm_alo)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tm_bhi)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tm_blo)) : "memory");
+  }
+  if (warp == 1 && lane == 0) {
+    for (int i = 0; i < STAGES; ++i) {
+      mbar_init(&full_bar[i], 1);
+      mbar_init(&empty_bar[i], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&pfull_bar[i], 1);
+      mbar_init(&pempty_bar[i], EPI_THREADS);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 2) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(tmem_slot)),
+                 "r"(TMEM_COLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      // ===== TMA producer =====
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int w = blockIdx.x; w < total; w += gridDim.x) {
+        const WorkCoord wc = decode(w, nm, nn);
+        const int k_begin = wc.split * k_per_split;
+        const int k_end = min(Kp, k_begin + k_per_split);
+        const int m0 = wc.mb * BM, n0 = wc.nb * BN;
+        for (int k = k_begin; k < k_end; k += BK) {
+          mbar_wait(&empty_bar[stage], phase ^ 1);
+          uint8_t* st = smem + stage * STAGE_BYTES;
+          mbar_arrive_expect_tx(&full_bar[stage], STAGE_BYTES);
+          tma_load_2d(st, &tm_ahi, &full_bar[stage], k, m0);
+          tma_load_2d(st + A_TILE, &tm_alo, &full_bar[stage], k, m0);
+          tma_load_2d(st + 2 * A_TILE, &tm_bhi, &full_bar[stage], k, n0);
+          tma_load_2d(st + 2 * A_TILE + B_TILE, &tm_blo, &full_bar[stage], k, n0);
+          if (++stage == STAGES) { stage = 0; phase ^= 1; }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ===== MMA issuer =====
+    int stage = 0;
+    uint32_t phase = 0;
+    int gchunk = 0;
+    for (int w = blockIdx.x; w < total; w += gridDim.x) {
+      const WorkCoord wc = decode(w, nm, nn);
+      const int k_begin = wc.split * k_per_split;
+      const int nkb = (min(Kp, k_begin + k_per_split) - k_begin + BK - 1) / BK;
+      for (int c0 = 0; c0 < nkb; c0 += chunk_kb, ++gchunk) {
+        const int buf = gchunk & 1;
+        mbar_wait(&pempty_bar[buf], ((gchunk >> 1) & 1) ^ 1);
+        tc_fence_after();
+        const uint32_t tmem_c = tmem_base + buf * BN;
+        const int c1 = min(nkb, c0 + chunk_kb);
+        for (int kb = c0; kb < c1; ++kb) {
+          mbar_wait(&full_bar[stage], phase);
+          tc_fence_after();
+          if (lane == 0) {
+            uint8_t* st = smem + stage * STAGE_BYTES;
+            const uint64_t d_ahi = make_desc_sw64(st);
+            const uint64_t d_alo = make_desc_sw64(st + A_TILE);
+            const uint64_t d_bhi = make_desc_sw64(st + 2 * A_TILE);
+            const uint64_t d_blo = make_desc_sw64(st + 2 * A_TILE + B_TILE);
+#pragma unroll
+            for (int kk = 0; kk < BK / 16; ++kk) {
+              const uint64_t adv = (uint64_t)(kk * 32) >> 4;  // 16 fp16 = 32 B along K
+              umma_f16(tmem_c, d_ahi + adv, d_blo + adv, (kb == c0 && kk == 0) ? 0u : 1u);
+              umma_f16(tmem_c, d_alo + adv, d_bhi + adv, 1u);
+              umma_f16(tmem_c, d_ahi + adv, d_bhi + adv, 1u);
+            }
+            umma_commit(&empty_bar[stage]);
+          }
+          __syncwarp();
+          if (++stage == STAGES) { stage = 0; phase ^= 1; }
+        }
+        if (lane == 0) umma_commit(&pfull_bar[buf]);
+        __syncwarp();
+      }
+    }
+  } else if (warp >= 4) {
+    // ===== promotion + epilogue: warp -> TMEM lane quadrant (warp % 4), column group =====
+    const int q = warp & 3;
+    const int grp = (warp - 4) >> 2;
+    const float alpha = splits == 1 ? 1.f / (scale_of(maxbits[0]) * scale_of(maxbits[1])) : 1.f;
+    int gchunk = 0;
+    for (int w = blockIdx.x; w < total; w += gridDim.x) {
+      const WorkCoord wc = decode(w, nm, nn);
+      const int k_begin = wc.split * k_per_split;
+      const int nkb = (min(Kp, k_begin + k_per_split) - k_begin + BK - 1) / BK;
+      float acc[EPI_COLS];
+#pragma unroll
+      for (int j = 0; j < EPI_COLS; ++j) acc[j] = 0.f;
+      for (int c0 = 0; c0 < nkb; c0 += chunk_kb, ++gchunk) {
+        const int buf = gchunk & 1;
+        mbar_wait(&pfull_bar[buf], (gchunk >> 1) & 1);
+        tc_fence_after();
+        const uint32_t taddr = tmem_base + ((uint32_t)(q * 32) << 16) + buf * BN + grp * EPI_COLS;
+#pragma unroll
+        for (int s = 0; s < EPI_COLS / 16; ++s) {
+          uint32_t r[16];
+          tmem_ld16(taddr + s * 16, r);
+#pragma unroll
+          for (int j = 0; j < 16; ++j) acc[s * 16 + j] += __uint_as_float(r[j]);
+        }
+        tc_fence_before();
+        mbar_arrive(&pempty_bar[buf]);
+      }
+      const int row = wc.mb * BM + q * 32 + lane;
+      const int col0 = wc.nb * BN + grp * EPI_COLS;
+      if (row < M && col0 < Np) {
+        float* dst = C + (size_t)wc.split * (size_t)M * (size_t)Np + (size_t)row * Np + col0;
+        if (col0 + EPI_COLS <= Np) {
+#pragma unroll
+          for (int j = 0; j < EPI_COLS; j += 4)
+            *reinterpret_cast<float4*>(dst + j) =
+                make_float4(acc[j] * alpha, acc[j + 1] * alpha, acc[j + 2] * alpha, acc[j + 3] * alpha);
+        } else {
+#pragma unroll
+          for (int j = 0; j < EPI_COLS; ++j)
+            if (col0 + j < Np) dst[j] = acc[j] * alpha;
+        }
+      }
+    }
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
+                 "r"(TMEM_COLS));
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Host side: tensor maps through the driver entry point (no -lcuda needed).
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                  const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                  const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                  CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiledFn get_encode() {
+  static EncodeTiledFn fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeTiledFn>(p);
+  });
+  if (!fn) throw Error(TNB_ERR_CUDA, "cuTensorMapEncodeTiled entry point unavailable");
+  return fn;
+}
+
+void make_map(void* out, const __half* base, int64_t rows, int64_t kp, int box_rows) {
+  if ((reinterpret_cast<uintptr_t>(base) & 15) != 0 || (kp % 8) != 0)
+    throw Error(TNB_ERR_SHAPE, "tensor-core operand not 16-byte aligned");
+  cuuint64_t dims[2] = {(cuuint64_t)kp, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)kp * 2};
+  cuuint32_t box[2] = {(cuuint32_t)BK, (cuuint32_t)box_rows};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = get_encode()(reinterpret_cast<CUtensorMap*>(out), CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2,
+                            const_cast<__half*>(base), dims, strides, box, estr,
+                            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B,
+                            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) throw Error(TNB_ERR_CUDA, "cuTensorMapEncodeTiled failed: " + std::to_string((int)r));
+}
+
+int choose_splits(int64_t M, int64_t Np, int64_t Kp, int num_sms) {
+  const int64_t tiles = ((M + BM - 1) / BM) * ((Np + BN - 1) / BN);
+  const int64_t kblocks = (Kp + BK - 1) / BK;
+  int s = 1;
+  // split K while tiles leave SMs idle and every split keeps >= 16 K blocks
+  while (tiles * s * 2 <= num_sms && kblocks / (s * 2) >= 16 && s < 32) s *= 2;
+  return s;
+}
+
+}  // namespace
+
+bool tc_available(int device) {
+  cudaDeviceProp prop;
+  if (cudaGetDeviceProperties(&prop, device) != cudaSuccess) return false;
+  return prop.major == 10 && prop.minor == 0;
+}
+
+int64_t tc_workspace_elems(int64_t M, int64_t Np, int64_t Kp, int num_sms) {
+  const int s = choose_splits(M, Np, Kp, num_sms);
+  return s > 1 ? (int64_t)s * M * Np : 0;
+}
+
+void tc_plan_gemm(TcGemmPlan* p, const __half* Ahi, const __half* Alo, const __half* Bhi,
+                  const __half* Blo, int64_t M, int64_t Np, int64_t Kp, float* C, float* workspace,
+                  int64_t workspace_elems, const unsigned int* maxbits, int num_sms) {
+  if (M > (1ll << 31) - 1 || Np > (1ll << 31) - 1 || Kp > (1ll << 31) - 1)
+    throw Error(TNB_ERR_SHAPE, "tensor-core GEMM dimension too large");
+  p->M = M; p->Np = Np; p->Kp = Kp;
+  p->splits = choose_splits(M, Np, Kp, num_sms);
+  const int64_t kblocks = (Kp + BK - 1) / BK;
+  p->k_per_split = ((kblocks + p->splits - 1) / p->splits) * BK;
+  const int64_t work = ((M + BM - 1) / BM) * ((Np + BN - 1) / BN) * p->splits;
+  p->grid = (int)(work < num_sms ? work : num_sms);
+  if (p->splits > 1) {
+    if (workspace == nullptr || workspace_elems < (int64_t)p->splits * M * Np)
+      throw Error(TNB_ERR_ARG, "split-K workspace too small");
+    p->C = workspace;
+  } else {
+    p->C = C;
+  }
+  p->maxbits = maxbits;
+  const char* env = getenv("TNB_CHUNK_KB");
+  p->chunk_kb = env ? atoi(env) : kDefaultChunkKb;
+  if (p->chunk_kb <= 0) p->chunk_kb = 1 << 30;  // no promotion: whole K in TMEM
+  make_map(p->tmap[0], Ahi, M, Kp, BM);
+  make_map(p->tmap[1], Alo, M, Kp, BM);
+  make_map(p->tmap[2], Bhi, Np, Kp, BN);
+  make_map(p->tmap[3], Blo, Np, Kp, BN);
+}
+
+void tc_launch_gemm(const TcGemmPlan* p, cudaStream_t s) {
+  TNB_CUDA(cudaFuncSetAttribute(gemm_f16x3_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                SMEM_BYTES));
+  const CUtensorMap* maps = reinterpret_cast<const CUtensorMap*>(p->tmap);
+  gemm_f16x3_kernel<<<p->grid, NUM_THREADS, SMEM_BYTES, s>>>(
+      maps[0], maps[1], maps[2], maps[3], p->C, (int)p->M, (int)p->Np, (int)p->Kp, p->splits,
+      (int)p->k_per_split, p->chunk_kb, p->maxbits);
+  check_launch("gemm_f16x3");
+}
+
+}  // namespace tnb

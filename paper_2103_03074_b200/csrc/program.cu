@@ -1,0 +1,710 @@
+// Program = compiled pairwise contraction schedule + device buffers.
+//
+// Host-side compilation (once per (network topology, tree, slicing)):
+//   * axis lists for every leaf (sliced axes removed) and step result,
+//     exactly the index bookkeeping of tncut `_contract_steps`
+//     (engine.py:117-144): shared = a_ids & b_ids in a's order, result =
+//     free axes of the two operands;
+//   * slice dependence: a tensor is slice-variant iff some leaf below it
+//     carries a sliced index; invariant subtrees are computed once and kept
+//     (hoisting) -- they do not change with the mask;
+//   * per step a kernel choice (tcgen05 3xFP16 GEMM or SIMT), the
+//     canonical-layout byte LUTs, and -- for the tensor-core path -- the
+//     operand roles (smaller operand is expanded) and TMA descriptors;
+//   * a first-fit arena for slice-variant intermediates (liveness in step
+//     order) and one scratch region for GEMM operand staging.
+// Execution of a slice range follows compute_head_vector's loop
+// (engine.py:275-298) with the binary-counter fixed-mode sum
+// (engine.py:207-222) or the free running sum.
+#include "tnb_internal.h"
+
+#include <algorithm>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <numeric>
+#include <unordered_map>
+
+namespace tnb {
+
+namespace {
+
+constexpr int64_t kAlign = 1024;
+inline int64_t align_up(int64_t x, int64_t a) { return (x + a - 1) / a * a; }
+
+struct Arena {
+  // first-fit allocator over a virtual offset space
+  std::map<int64_t, int64_t> free_;  // offset -> size
+  int64_t top = 0;
+  int64_t alloc(int64_t size) {
+    size = align_up(size, kAlign);
+    for (auto it = free_.begin(); it != free_.end(); ++it) {
+      if (it->second >= size) {
+        const int64_t off = it->first;
+        const int64_t rest = it->second - size;
+        free_.erase(it);
+        if (rest > 0) free_[off + size] = rest;
+        return off;
+      }
+    }
+    // extend: merge with a trailing free block if there is one
+    if (!free_.empty()) {
+      auto last = std::prev(free_.end());
+      if (last->first + last->second == top) {
+        const int64_t off = last->first;
+        free_.erase(last);
+        top = off + size;
+        return off;
+      }
+    }
+    const int64_t off = top;
+    top += size;
+    return off;
+  }
+  void release(int64_t off, int64_t size) {
+    size = align_up(size, kAlign);
+    auto it = free_.emplace(off, size).first;
+    // coalesce with next
+    auto nx = std::next(it);
+    if (nx != free_.end() && it->first + it->second == nx->first) {
+      it->second += nx->second;
+      free_.erase(nx);
+    }
+    if (it != free_.begin()) {
+      auto pv = std::prev(it);
+      if (pv->first + pv->second == it->first) {
+        pv->second += it->second;
+        free_.erase(it);
+      }
+    }
+  }
+};
+
+enum Pool { POOL_LEAF = 0, POOL_SLICE = 1, POOL_PERSIST = 2, POOL_ARENA = 3 };
+
+struct TensorRec {
+  std::vector<int64_t> axes;
+  bool variant = false;
+  int pool = POOL_LEAF;
+  int64_t off = 0;  // element offset within the pool
+  int64_t elems = 1;
+  int leaf_pos = -1;
+  int def_step = -1;   // step producing it (-1: leaf)
+  int last_use = -1;   // last consuming step (n_steps: the root)
+};
+
+enum StepKind { KIND_SIMT = 0, KIND_TC = 1 };
+
+struct StepRec {
+  int a = -1, b = -1, out = -1;
+  int kind = KIND_SIMT;
+  bool hoisted = false;
+  int64_t M = 1, N = 1, K = 1;   // SIMT: rows of a, cols of b, shared. TC: rows/cols operand.
+  int rows_t = -1, cols_t = -1;  // TC operand tensors (rows unexpanded, cols expanded)
+  int lut_a = -1, lut_b = -1;    // indices into the LUT table
+  double mults = 0;
+  TcGemmPlan tc;
+};
+
+}  // namespace
+
+// ---------------------------------------------------------------------------
+struct Program {
+  int device = 0;
+  int precision = TNB_SINGLE;
+  uint32_t flags = 0;
+  size_t esize = 8;  // bytes per complex element
+  int num_sms = 148;
+  cudaStream_t stream = nullptr;
+
+  int n_sliced = 0;
+  std::vector<TensorRec> tensors;        // leaves first (leaf_pos order), then step outputs
+  std::vector<StepRec> steps;
+  std::vector<int32_t> leaf_ranks;
+  std::vector<int64_t> leaf_pool_off;    // element offset of full leaf data in the leaf pool
+  std::vector<ByteLut> luts;
+  int root = -1;
+  int root_lut = -1;
+  int64_t out_elems = 1;
+  bool root_identity = false;
+
+  // device memory
+  void* d_leaf_pool = nullptr;   int64_t leaf_pool_elems = 0;
+  void* d_slice_pool = nullptr;  int64_t slice_pool_elems = 0;
+  void* d_persist = nullptr;     int64_t persist_elems = 0;
+  void* d_arena = nullptr;       int64_t arena_bytes = 0;
+  void* d_scratch = nullptr;     int64_t scratch_bytes = 0;
+  ByteLut* d_luts = nullptr;
+  SlicedLeafDesc* d_sl_descs = nullptr; int n_sl_descs = 0;
+  uint32_t* d_keep = nullptr;
+  unsigned int* d_maxbits = nullptr;
+  void* d_acc = nullptr;          // (n_sliced + 2) accumulator slots of out_elems
+  int n_acc_slots = 0;
+  bool invariant_valid = false;
+
+  // timing
+  bool timing = false;
+  tnb_timing last{};
+  std::vector<cudaEvent_t> ev_pool;
+
+  // stats
+  double flops_per_slice = 0, tc_flops_per_slice = 0;
+  int n_tc = 0, n_simt = 0, n_hoisted = 0;
+
+  ~Program() {
+    if (device >= 0) cudaSetDevice(device);
+    void* ptrs[] = {d_leaf_pool, d_slice_pool, d_persist, d_arena, d_scratch, d_luts,
+                    d_sl_descs, d_keep, d_maxbits, d_acc};
+    for (void* p : ptrs)
+      if (p) cudaFree(p);
+    for (auto e : ev_pool) cudaEventDestroy(e);
+    if (stream) cudaStreamDestroy(stream);
+  }
+
+  void* tensor_ptr(int t) const {
+    const TensorRec& r = tensors[t];
+    char* base = nullptr;
+    switch (r.pool) {
+      case POOL_LEAF: base = (char*)d_leaf_pool; break;
+      case POOL_SLICE: base = (char*)d_slice_pool; break;
+      case POOL_PERSIST: base = (char*)d_persist; break;
+      default: base = (char*)d_arena; break;
+    }
+    return base + (size_t)r.off * esize;
+  }
+};
+
+namespace {
+
+// canonical (row, k) index -> source element offset in tensor `t`:
+// canonical bit p < nk <-> kaxes[nk-1-p]; bit p >= nk <-> raxes[nr-1-(p-nk)].
+std::vector<int> canon_bits(const std::vector<int64_t>& axes, const std::vector<int64_t>& raxes,
+                            const std::vector<int64_t>& kaxes) {
+  const int r = (int)axes.size();
+  std::unordered_map<int64_t, int> pos;
+  for (int i = 0; i < r; ++i) pos[axes[i]] = i;
+  std::vector<int> src;
+  src.reserve(r);
+  for (int p = 0; p < (int)kaxes.size(); ++p) src.push_back(r - 1 - pos.at(kaxes[kaxes.size() - 1 - p]));
+  for (int p = 0; p < (int)raxes.size(); ++p) src.push_back(r - 1 - pos.at(raxes[raxes.size() - 1 - p]));
+  return src;
+}
+
+int add_lut(Program* P, const std::vector<int>& src_bit) {
+  ByteLut l;
+  build_lut(src_bit, &l);
+  P->luts.push_back(l);
+  return (int)P->luts.size() - 1;
+}
+
+template <typename T>
+void exec_step(Program* P, StepRec& s);
+
+template <typename T>
+void run_range_t(Program* P, uint64_t a, uint64_t b, int mode, void* out, bool out_dev);
+
+}  // namespace
+
+// ---------------------------------------------------------------------------
+Program* program_create(const tnb_program_desc* d) {
+  if (!d) throw Error(TNB_ERR_ARG, "null descriptor");
+  if (d->precision != TNB_SINGLE && d->precision != TNB_DOUBLE)
+    throw Error(TNB_ERR_ARG, "precision must be TNB_SINGLE or TNB_DOUBLE");
+  if (d->n_leaves <= 0) throw Error(TNB_ERR_SHAPE, "program needs at least one leaf");
+  if (d->n_sliced < 0 || d->n_sliced > 64) throw Error(TNB_ERR_ARG, "n_sliced must be in [0, 64]");
+  int ndev = 0;
+  TNB_CUDA(cudaGetDeviceCount(&ndev));
+  if (d->device < 0 || d->device >= ndev) throw Error(TNB_ERR_NODEV, "device ordinal out of range");
+
+  std::unique_ptr<Program> P(new Program());
+  P->device = d->device;
+  P->precision = d->precision;
+  P->flags = d->flags;
+  P->esize = d->precision == TNB_SINGLE ? 8 : 16;
+  P->n_sliced = d->n_sliced;
+  TNB_CUDA(cudaSetDevice(P->device));
+  TNB_CUDA(cudaDeviceGetAttribute(&P->num_sms, cudaDevAttrMultiProcessorCount, P->device));
+  TNB_CUDA(cudaStreamCreateWithFlags(&P->stream, cudaStreamNonBlocking));
+  const bool use_tc = d->precision == TNB_SINGLE && !(d->flags & TNB_FLAG_NO_TENSOR_CORES) &&
+                      tc_available(P->device);
+
+  // sliced index -> mask bit (engine.py:276-279: bit n_e-1-pos pins sliced[pos])
+  std::unordered_map<int64_t, int> slice_bit;
+  for (int i = 0; i < d->n_sliced; ++i) {
+    if (slice_bit.count(d->sliced[i])) throw Error(TNB_ERR_ARG, "duplicate sliced index");
+    slice_bit[d->sliced[i]] = d->n_sliced - 1 - i;
+  }
+
+  // ---- leaves
+  std::unordered_map<int64_t, int> id2t;
+  std::vector<SlicedLeafDesc> sl_descs;
+  std::vector<uint32_t> keep;
+  int64_t leaf_off = 0, slice_off = 0, idx_off = 0;
+  P->leaf_ranks.assign(d->leaf_ranks, d->leaf_ranks + d->n_leaves);
+  for (int i = 0; i < d->n_leaves; ++i) {
+    const int r = d->leaf_ranks[i];
+    if (r < 0 || r > 32) throw Error(TNB_ERR_SHAPE, "leaf rank out of range");
+    TensorRec t;
+    t.leaf_pos = i;
+    std::vector<int64_t> full(d->leaf_indices + idx_off, d->leaf_indices + idx_off + r);
+    idx_off += r;
+    std::vector<std::pair<int, uint32_t>> sl;  // (mask bit, stride)
+    std::vector<int> keep_src;
+    for (int ax = 0; ax < r; ++ax) {
+      auto it = slice_bit.find(full[ax]);
+      if (it != slice_bit.end()) {
+        sl.push_back({it->second, 1u << (r - 1 - ax)});
+      } else {
+        t.axes.push_back(full[ax]);
+        keep_src.push_back(r - 1 - ax);
+      }
+    }
+    P->leaf_pool_off.push_back(leaf_off);
+    leaf_off += (int64_t)1 << r;
+    t.elems = (int64_t)1 << t.axes.size();
+    if (!sl.empty()) {
+      if (sl.size() > 8) throw Error(TNB_ERR_SHAPE, "more than 8 sliced axes on one leaf");
+      t.variant = true;
+      t.pool = POOL_SLICE;
+      t.off = slice_off;
+      slice_off += align_up(t.elems, 128);
+      SlicedLeafDesc sd{};
+      sd.src_off = P->leaf_pool_off.back();
+      sd.dst_off = t.off;
+      sd.out_elems = (uint32_t)t.elems;
+      sd.n_sl = (uint32_t)sl.size();
+      sd.keep_lut_off = (uint32_t)keep.size();
+      for (size_t j = 0; j < sl.size(); ++j) { sd.sl_bit[j] = sl[j].first; sd.sl_stride[j] = sl[j].second; }
+      // out index bit p (LSB first) <-> kept axis keep_src.size()-1-p
+      const int nk = (int)keep_src.size();
+      for (int64_t jj = 0; jj < t.elems; ++jj) {
+        uint32_t o = 0;
+        for (int p = 0; p < nk; ++p)
+          if ((jj >> p) & 1) o |= 1u << keep_src[nk - 1 - p];
+        keep.push_back(o);
+      }
+      sl_descs.push_back(sd);
+    } else {
+      t.pool = POOL_LEAF;
+      t.off = P->leaf_pool_off.back();
+    }
+    if (id2t.count(d->leaf_ids[i])) throw Error(TNB_ERR_SHAPE, "duplicate leaf id");
+    id2t[d->leaf_ids[i]] = (int)P->tensors.size();
+    P->tensors.push_back(t);
+  }
+  P->leaf_pool_elems = leaf_off;
+  P->slice_pool_elems = slice_off;
+
+  // ---- steps: axis bookkeeping (engine.py:125-134)
+  for (int i = 0; i < d->n_steps; ++i) {
+    const int64_t lhs = d->steps[3 * i], rhs = d->steps[3 * i + 1], outid = d->steps[3 * i + 2];
+    auto ia = id2t.find(lhs), ib = id2t.find(rhs);
+    if (ia == id2t.end() || ib == id2t.end() || lhs == rhs)
+      throw Error(TNB_ERR_SHAPE, "step " + std::to_string(i) + " references a missing operand");
+    StepRec s;
+    s.a = ia->second;
+    s.b = ib->second;
+    id2t.erase(ia);
+    id2t.erase(id2t.find(rhs));
+    const TensorRec& A = P->tensors[s.a];
+    const TensorRec& B = P->tensors[s.b];
+    std::vector<int64_t> shared, afree, bfree;
+    for (int64_t x : A.axes)
+      (std::find(B.axes.begin(), B.axes.end(), x) != B.axes.end() ? shared : afree).push_back(x);
+    for (int64_t x : B.axes)
+      if (std::find(A.axes.begin(), A.axes.end(), x) == A.axes.end()) bfree.push_back(x);
+    const int na = (int)afree.size(), nb = (int)bfree.size(), nab = (int)shared.size();
+    s.mults = std::ldexp(1.0, na + nb + nab);
+    TensorRec o;
+    o.variant = A.variant || B.variant;
+    o.def_step = i;
+    s.M = (int64_t)1 << na;
+    s.N = (int64_t)1 << nb;
+    s.K = (int64_t)1 << nab;
+    // tensor-core eligibility: big enough to fill 128x256 tiles and amortise staging
+    bool tc = use_tc && nab >= 3 && na + nb + nab >= 27 && std::max(na, nb) >= 7 &&
+              std::min(na, nb) >= 3;
+    if (tc) {
+      // expand the smaller operand (B' doubles its size); rows = the other one
+      const bool rows_is_a = ((int64_t)1 << (na + nab)) >= ((int64_t)1 << (nb + nab));
+      s.kind = KIND_TC;
+      if (rows_is_a) {
+        s.rows_t = s.a; s.cols_t = s.b;
+        o.axes = afree; o.axes.insert(o.axes.end(), bfree.begin(), bfree.end());
+        s.M = (int64_t)1 << na; s.N = (int64_t)1 << nb;
+        s.lut_a = add_lut(P.get(), canon_bits(A.axes, afree, shared));
+        s.lut_b = add_lut(P.get(), canon_bits(B.axes, bfree, shared));
+      } else {
+        s.rows_t = s.b; s.cols_t = s.a;
+        o.axes = bfree; o.axes.insert(o.axes.end(), afree.begin(), afree.end());
+        s.M = (int64_t)1 << nb; s.N = (int64_t)1 << na;
+        s.lut_a = add_lut(P.get(), canon_bits(B.axes, bfree, shared));
+        s.lut_b = add_lut(P.get(), canon_bits(A.axes, afree, shared));
+      }
+    } else {
+      s.kind = KIND_SIMT;
+      o.axes = afree; o.axes.insert(o.axes.end(), bfree.begin(), bfree.end());
+      s.lut_a = add_lut(P.get(), canon_bits(A.axes, afree, shared));
+      s.lut_b = add_lut(P.get(), canon_bits(B.axes, bfree, shared));
+    }
+    if (o.axes.size() > 32) throw Error(TNB_ERR_SHAPE, "intermediate rank above 32");
+    o.elems = (int64_t)1 << o.axes.size();
+    P->tensors[s.a].last_use = i;
+    P->tensors[s.b].last_use = i;
+    s.out = (int)P->tensors.size();
+    s.hoisted = !o.variant && !(d->flags & TNB_FLAG_NO_HOIST);
+    P->tensors.push_back(o);
+    if (id2t.count(outid)) throw Error(TNB_ERR_SHAPE, "step output id reused");
+    id2t[outid] = s.out;
+    P->flops_per_slice += 8.0 * s.mults;
+    if (s.kind == KIND_TC) { P->tc_flops_per_slice += 8.0 * s.mults; P->n_tc++; } else P->n_simt++;
+    if (s.hoisted) P->n_hoisted++;
+    P->steps.push_back(s);
+  }
+  if (id2t.size() != 1)
+    throw Error(TNB_ERR_SHAPE, std::to_string(id2t.size()) + " results left after contraction");
+  P->root = id2t.begin()->second;
+  const int n_steps = (int)P->steps.size();
+  P->tensors[P->root].last_use = n_steps;
+
+  // ---- root output order
+  {
+    const TensorRec& R = P->tensors[P->root];
+    std::vector<int64_t> want(d->out_order, d->out_order + d->n_out);
+    std::vector<int64_t> s1 = want, s2 = R.axes;
+    std::sort(s1.begin(), s1.end());
+    std::sort(s2.begin(), s2.end());
+    if (s1 != s2) throw Error(TNB_ERR_SHAPE, "root indices differ from the requested output order");
+    P->out_elems = R.elems;
+    P->root_identity = (want == R.axes);
+    P->root_lut = add_lut(P.get(), canon_bits(R.axes, want, {}));
+  }
+
+  // ---- memory planning: persistent (hoisted) and arena (variant) tensors
+  int64_t persist_off = 0;
+  Arena arena;
+  std::vector<std::vector<int>> free_after(n_steps + 1);
+  for (int t = 0; t < (int)P->tensors.size(); ++t) {
+    const TensorRec& r = P->tensors[t];
+    if (r.def_step >= 0 && r.last_use >= 0 && r.last_use < n_steps) free_after[r.last_use].push_back(t);
+  }
+  int64_t scratch_bytes = 0;
+  for (int i = 0; i < n_steps; ++i) {
+    StepRec& s = P->steps[i];
+    TensorRec& o = P->tensors[s.out];
+    if (s.hoisted || !o.variant) {
+      o.pool = POOL_PERSIST;
+      o.off = persist_off;
+      persist_off += align_up(o.elems, 128);
+    } else {
+      o.pool = POOL_ARENA;
+      o.off = arena.alloc(o.elems * (int64_t)P->esize) / (int64_t)P->esize;
+    }
+    if (s.kind == KIND_TC) {
+      const int64_t Kp = 2 * s.K, Np = 2 * s.N;
+      int64_t need = 2 * s.M * Kp * 2 + 2 * Np * Kp * 2;  // hi+lo for both operands (fp16)
+      need = align_up(need, kAlign) + tc_workspace_elems(s.M, Np, Kp, P->num_sms) * 4;
+      scratch_bytes = std::max(scratch_bytes, need);
+    }
+    // variant operands whose last use is this step are released after it
+    for (int t : free_after[i]) {
+      TensorRec& r = P->tensors[t];
+      if (r.pool == POOL_ARENA) arena.release(r.off * (int64_t)P->esize, r.elems * (int64_t)P->esize);
+    }
+  }
+  P->persist_elems = persist_off;
+  P->arena_bytes = arena.top;
+  P->scratch_bytes = scratch_bytes;
+
+  // ---- device allocations
+  auto dmalloc = [](void** p, int64_t bytes) {
+    if (bytes <= 0) bytes = 256;
+    TNB_CUDA(cudaMalloc(p, (size_t)bytes));
+  };
+  dmalloc(&P->d_leaf_pool, P->leaf_pool_elems * (int64_t)P->esize);
+  dmalloc(&P->d_slice_pool, P->slice_pool_elems * (int64_t)P->esize);
+  dmalloc(&P->d_persist, P->persist_elems * (int64_t)P->esize);
+  dmalloc(&P->d_arena, P->arena_bytes);
+  dmalloc(&P->d_scratch, P->scratch_bytes);
+  dmalloc((void**)&P->d_luts, (int64_t)P->luts.size() * sizeof(ByteLut));
+  TNB_CUDA(cudaMemcpy(P->d_luts, P->luts.data(), P->luts.size() * sizeof(ByteLut), cudaMemcpyHostToDevice));
+  P->n_sl_descs = (int)sl_descs.size();
+  dmalloc((void**)&P->d_sl_descs, (int64_t)sl_descs.size() * sizeof(SlicedLeafDesc));
+  if (!sl_descs.empty())
+    TNB_CUDA(cudaMemcpy(P->d_sl_descs, sl_descs.data(), sl_descs.size() * sizeof(SlicedLeafDesc),
+                        cudaMemcpyHostToDevice));
+  dmalloc((void**)&P->d_keep, (int64_t)keep.size() * 4);
+  if (!keep.empty())
+    TNB_CUDA(cudaMemcpy(P->d_keep, keep.data(), keep.size() * 4, cudaMemcpyHostToDevice));
+  dmalloc((void**)&P->d_maxbits, 64);
+  P->n_acc_slots = P->n_sliced + 3;  // counter levels + total + permuted output
+  dmalloc(&P->d_acc, (int64_t)P->n_acc_slots * align_up(P->out_elems, 128) * (int64_t)P->esize);
+
+  // ---- tensor-core plans (fixed addresses -> TMA descriptors built once)
+  for (auto& s : P->steps) {
+    if (s.kind != KIND_TC) continue;
+    const int64_t Kp = 2 * s.K, Np = 2 * s.N;
+    char* base = (char*)P->d_scratch;
+    __half* ahi = (__half*)base;
+    __half* alo = ahi + s.M * Kp;
+    __half* bhi = alo + s.M * Kp;
+    __half* blo = bhi + Np * Kp;
+    float* ws = (float*)(base + align_up(2 * s.M * Kp * 2 + 2 * Np * Kp * 2, kAlign));
+    const int64_t ws_elems = tc_workspace_elems(s.M, Np, Kp, P->num_sms);
+    tc_plan_gemm(&s.tc, ahi, alo, bhi, blo, s.M, Np, Kp, (float*)P->tensor_ptr(s.out), ws, ws_elems,
+                 P->d_maxbits, P->num_sms);
+  }
+
+  // ---- upload leaf values
+  {
+    std::vector<char> host((size_t)P->leaf_pool_elems * P->esize);
+    if (P->precision == TNB_SINGLE) {
+      float* h = (float*)host.data();
+      for (int64_t i = 0; i < 2 * P->leaf_pool_elems; ++i) h[i] = (float)d->leaf_data[i];
+    } else {
+      std::memcpy(host.data(), d->leaf_data, host.size());
+    }
+    TNB_CUDA(cudaMemcpy(P->d_leaf_pool, host.data(), host.size(), cudaMemcpyHostToDevice));
+  }
+  return P.release();
+}
+
+void program_destroy(Program* P) { delete P; }
+
+void program_info(const Program* P, tnb_program_info* info) {
+  info->out_elems = P->out_elems;
+  info->flops_per_slice = P->flops_per_slice;
+  info->tc_flops_per_slice = P->tc_flops_per_slice;
+  info->arena_bytes = P->arena_bytes;
+  info->persistent_bytes = (P->leaf_pool_elems + P->slice_pool_elems + P->persist_elems) * (int64_t)P->esize;
+  info->scratch_bytes = P->scratch_bytes;
+  info->n_steps_tc = P->n_tc;
+  info->n_steps_simt = P->n_simt;
+  info->n_steps_hoisted = P->n_hoisted;
+  int k = P->n_sl_descs ? 1 : 0;
+  for (auto& s : P->steps) {
+    if (s.hoisted) continue;
+    k += s.kind == KIND_TC ? (3 + (s.tc.splits > 1 ? 1 : 0)) : 1;
+  }
+  info->kernels_per_slice = k + 1;
+}
+
+void program_set_leaf(Program* P, int leaf_pos, const double* data) {
+  if (leaf_pos < 0 || leaf_pos >= (int)P->leaf_ranks.size()) throw Error(TNB_ERR_ARG, "leaf index out of range");
+  TNB_CUDA(cudaSetDevice(P->device));
+  const int64_t n = (int64_t)1 << P->leaf_ranks[leaf_pos];
+  char* dst = (char*)P->d_leaf_pool + (size_t)P->leaf_pool_off[leaf_pos] * P->esize;
+  if (P->precision == TNB_SINGLE) {
+    std::vector<float> h(2 * n);
+    for (int64_t i = 0; i < 2 * n; ++i) h[i] = (float)data[i];
+    TNB_CUDA(cudaMemcpyAsync(dst, h.data(), h.size() * 4, cudaMemcpyHostToDevice, P->stream));
+    TNB_CUDA(cudaStreamSynchronize(P->stream));
+  } else {
+    TNB_CUDA(cudaMemcpyAsync(dst, data, (size_t)n * 16, cudaMemcpyHostToDevice, P->stream));
+    TNB_CUDA(cudaStreamSynchronize(P->stream));
+  }
+  P->invariant_valid = false;
+}
+
+void program_set_leaf_device(Program* P, int leaf_pos, const void* dev) {
+  if (leaf_pos < 0 || leaf_pos >= (int)P->leaf_ranks.size()) throw Error(TNB_ERR_ARG, "leaf index out of range");
+  TNB_CUDA(cudaSetDevice(P->device));
+  const int64_t n = (int64_t)1 << P->leaf_ranks[leaf_pos];
+  char* dst = (char*)P->d_leaf_pool + (size_t)P->leaf_pool_off[leaf_pos] * P->esize;
+  TNB_CUDA(cudaMemcpyAsync(dst, dev, (size_t)n * P->esize, cudaMemcpyDeviceToDevice, P->stream));
+  TNB_CUDA(cudaStreamSynchronize(P->stream));
+  P->invariant_valid = false;
+}
+
+namespace {
+
+struct EvRec { int cls; cudaEvent_t a, b; };
+
+struct RunCtx {
+  Program* P;
+  std::vector<EvRec> recs;
+  size_t ev_next = 0;
+  int64_t launches = 0, gemm_launches = 0;
+  double gemm_flops = 0;
+  cudaEvent_t get() {
+    if (ev_next == P->ev_pool.size()) {
+      cudaEvent_t e;
+      TNB_CUDA(cudaEventCreate(&e));
+      P->ev_pool.push_back(e);
+    }
+    return P->ev_pool[ev_next++];
+  }
+  cudaEvent_t mark() {
+    if (!P->timing) return nullptr;
+    cudaEvent_t e = get();
+    TNB_CUDA(cudaEventRecord(e, P->stream));
+    return e;
+  }
+  void close(int cls, cudaEvent_t a) {
+    if (!P->timing) return;
+    cudaEvent_t b = mark();
+    recs.push_back({cls, a, b});
+  }
+};
+
+thread_local RunCtx* g_ctx = nullptr;
+
+template <typename T>
+void exec_step(Program* P, StepRec& s) {
+  RunCtx& C = *g_ctx;
+  if (s.kind == KIND_SIMT) {
+    cudaEvent_t e = C.mark();
+    launch_contract_simt<T>((const T*)P->tensor_ptr(s.a), (const T*)P->tensor_ptr(s.b),
+                            (T*)P->tensor_ptr(s.out), s.M, s.N, s.K, P->d_luts + s.lut_a,
+                            P->d_luts + s.lut_b, P->stream);
+    C.close(2, e);
+    C.launches++;
+    return;
+  }
+  if constexpr (std::is_same<T, float2>::value) {
+    const int64_t Kp = 2 * s.K, Np = 2 * s.N;
+    const float2* rows = (const float2*)P->tensor_ptr(s.rows_t);
+    const float2* cols = (const float2*)P->tensor_ptr(s.cols_t);
+    char* base = (char*)P->d_scratch;
+    __half* ahi = (__half*)base;
+    __half* alo = ahi + s.M * Kp;
+    __half* bhi = alo + s.M * Kp;
+    __half* blo = bhi + Np * Kp;
+    cudaEvent_t e = C.mark();
+    launch_absmax2(rows, s.M * s.K, cols, s.N * s.K, P->d_maxbits, P->stream);
+    launch_split_rows(rows, P->d_luts + s.lut_a, s.M, s.K, P->d_maxbits, ahi, alo, P->stream);
+    launch_split_cols_expand(cols, P->d_luts + s.lut_b, s.N, s.K, P->d_maxbits, bhi, blo, P->stream);
+    C.close(1, e);
+    e = C.mark();
+    tc_launch_gemm(&s.tc, P->stream);
+    C.close(0, e);
+    C.launches += 4;
+    C.gemm_launches++;
+    C.gemm_flops += 8.0 * s.mults;
+    if (s.tc.splits > 1) {
+      e = C.mark();
+      launch_splitk_reduce(s.tc.C, s.tc.splits, s.M * Np, (float*)P->tensor_ptr(s.out), P->d_maxbits,
+                           P->stream);
+      C.close(1, e);
+      C.launches++;
+    }
+  } else {
+    throw Error(TNB_ERR_ARG, "tensor-core path requires single precision");
+  }
+}
+
+template <typename T>
+void run_range_t(Program* P, uint64_t a, uint64_t b, int mode, void* out, bool out_dev) {
+  RunCtx ctx;
+  ctx.P = P;
+  g_ctx = &ctx;
+  struct Reset { ~Reset() { g_ctx = nullptr; } } reset;
+  cudaStream_t st = P->stream;
+  const int64_t E = P->out_elems;
+  const int64_t slot_stride = align_up(E, 128);
+  T* slots = (T*)P->d_acc;
+  auto slot = [&](int i) { return slots + (size_t)i * slot_stride; };
+  T* total_slot = slot(P->n_sliced + 1);
+  T* perm_slot = slot(P->n_sliced + 2);
+  cudaEvent_t t_start = ctx.mark();
+
+  // hoisted slice-invariant steps (once per leaf-data version)
+  if (!P->invariant_valid) {
+    for (auto& s : P->steps)
+      if (s.hoisted) exec_step<T>(P, s);
+    P->invariant_valid = true;
+  }
+
+  // occupied binary-counter levels; level l holds a sum of 2^l chunks
+  std::vector<int> occupied(P->n_sliced + 2, 0);
+  uint64_t count = 0;
+  const T* root_ptr = (const T*)P->tensor_ptr(P->root);
+  for (uint64_t mask = a; mask < b; ++mask) {
+    cudaEvent_t e = ctx.mark();
+    launch_prepare_leaves<T>((const T*)P->d_leaf_pool, (T*)P->d_slice_pool, P->d_sl_descs,
+                             P->n_sl_descs, P->d_keep, mask, st);
+    if (P->n_sl_descs) ctx.launches++;
+    ctx.close(3, e);
+    for (auto& s : P->steps)
+      if (!s.hoisted) exec_step<T>(P, s);
+    e = ctx.mark();
+    if (mode == TNB_FIXED) {
+      // binary-counter increment: the new chunk merges with the levels
+      // 0..merges-1 (x = prev + x, lowest level first) -> level `merges`
+      int merges = 0;
+      while ((count >> merges) & 1ull) ++merges;
+      launch_counter_merge<T>(root_ptr, slot(0), slot_stride, merges, slot(merges), E, st);
+      for (int l = 0; l < merges; ++l) occupied[l] = 0;
+      occupied[merges] = 1;
+    } else {
+      // free mode: data = x if data is None else data + x (engine.py:295-298)
+      if (count == 0) launch_copy<T>(root_ptr, total_slot, E, st);
+      else launch_add<T>(total_slot, root_ptr, total_slot, E, st);
+    }
+    ctx.launches++;
+    ctx.close(3, e);
+    ++count;
+  }
+  cudaEvent_t e = ctx.mark();
+  const T* result = total_slot;
+  if (mode == TNB_FIXED) {
+    // total = stack[0] (highest level) + stack[1] + ... (engine.py:218-221)
+    bool first = true;
+    for (int l = (int)occupied.size() - 1; l >= 0; --l) {
+      if (!occupied[l]) continue;
+      if (first) launch_copy<T>(slot(l), total_slot, E, st);
+      else launch_add<T>(total_slot, slot(l), total_slot, E, st);
+      first = false;
+      ctx.launches++;
+    }
+  }
+  if (!P->root_identity) {
+    launch_permute<T>(result, perm_slot, E, P->d_luts + P->root_lut, st);
+    ctx.launches++;
+    result = perm_slot;
+  }
+  ctx.close(3, e);
+  if (out_dev) {
+    TNB_CUDA(cudaMemcpyAsync(out, result, (size_t)E * sizeof(T), cudaMemcpyDeviceToDevice, st));
+  } else {
+    TNB_CUDA(cudaMemcpyAsync(out, result, (size_t)E * sizeof(T), cudaMemcpyDeviceToHost, st));
+  }
+  cudaEvent_t t_end = ctx.mark();
+  TNB_CUDA(cudaStreamSynchronize(st));
+  tnb_timing tm{};
+  if (P->timing) {
+    float ms = 0;
+    TNB_CUDA(cudaEventElapsedTime(&ms, t_start, t_end));
+    tm.total_ms = ms;
+    for (auto& r : ctx.recs) {
+      TNB_CUDA(cudaEventElapsedTime(&ms, r.a, r.b));
+      if (r.cls == 0) tm.gemm_ms += ms;
+      else if (r.cls == 1) tm.convert_ms += ms;
+      else if (r.cls == 2) tm.simt_ms += ms;
+      else tm.other_ms += ms;
+    }
+  }
+  tm.launches = ctx.launches;
+  tm.gemm_launches = ctx.gemm_launches;
+  tm.gemm_flops = ctx.gemm_flops;
+  P->last = tm;
+}
+
+}  // namespace
+
+void program_run_range(Program* P, uint64_t a, uint64_t b, int mode, void* out, int out_dev) {
+  if (mode != TNB_FIXED && mode != TNB_FREE) throw Error(TNB_ERR_ARG, "unknown reduction mode");
+  const uint64_t total = P->n_sliced >= 64 ? ~0ull : (1ull << P->n_sliced);
+  if (!(a < b) || (P->n_sliced < 64 && b > total))
+    throw Error(TNB_ERR_RANGE, "range [" + std::to_string(a) + "," + std::to_string(b) +
+                                   ") outside [0," + std::to_string(total) + ")");
+  if (!out) throw Error(TNB_ERR_ARG, "null output");
+  TNB_CUDA(cudaSetDevice(P->device));
+  if (P->precision == TNB_SINGLE) run_range_t<float2>(P, a, b, mode, out, out_dev != 0);
+  else run_range_t<double2>(P, a, b, mode, out, out_dev != 0);
+}
+
+void program_set_timing(Program* P, int on) { P->timing = on != 0; }
+void program_get_timing(const Program* P, tnb_timing* t) { *t = P->last; }
+
+}  // namespace tnb

@@ -1,0 +1,119 @@
+// Internal declarations shared by the libtnb translation units.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <cuda_fp16.h>
+#include <cstdint>
+#include <string>
+#include <vector>
+#include <stdexcept>
+
+#include "../../include/tnb.h"
+
+namespace tnb {
+
+// ---------------------------------------------------------------------------
+// Errors: every internal failure throws tnb::Error(code, msg); the C-ABI
+// layer converts it into a status + thread-local message.
+struct Error : std::runtime_error {
+  int code;
+  Error(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+
+void set_last_error(const std::string& m);
+
+#define TNB_CUDA(call)                                                              \
+  do {                                                                              \
+    cudaError_t _e = (call);                                                        \
+    if (_e != cudaSuccess) {                                                        \
+      throw ::tnb::Error(_e == cudaErrorMemoryAllocation ? TNB_ERR_NOMEM : TNB_ERR_CUDA, \
+                         std::string(#call) + ": " + cudaGetErrorString(_e));       \
+    }                                                                               \
+  } while (0)
+
+inline void check_launch(const char* what) {
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) throw Error(TNB_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+// ---------------------------------------------------------------------------
+// Byte lookup tables that map a canonical (row-major GEMM) element index to
+// the element offset inside a tensor stored with an arbitrary axis order.
+// All bond dimensions are 2, so an index is a bit vector and the map is a
+// bit permutation: src = T0[j & 255] | T1[(j>>8)&255] | T2[(j>>16)&255] | T3[j>>24].
+struct ByteLut {
+  uint32_t t[4][256];
+};
+
+// Build the LUT for a permutation given as src_bit[p] = source bit position
+// of canonical bit p (p = 0 is the least significant canonical bit).
+void build_lut(const std::vector<int>& src_bit, ByteLut* out);
+
+// ---------------------------------------------------------------------------
+// Kernel launchers (kernels.cu).  All take a stream; pointers are device.
+struct SlicedLeafDesc {      // one sliced leaf to prepare per mask
+  uint64_t src_off;          // element offset of the full leaf in the leaf pool
+  uint64_t dst_off;          // element offset of the prepared leaf (slice pool)
+  uint32_t out_elems;        // 2^(rank - #sliced axes)
+  uint32_t n_sl;             // number of sliced axes (<= 8)
+  uint32_t keep_lut_off;     // offset into a shared uint32 table: out index -> src offset
+  uint32_t pad;
+  uint32_t sl_stride[8];     // element stride of each sliced axis in the full leaf
+  uint32_t sl_bit[8];        // mask bit position (n_e-1-pos)
+};
+
+template <typename T>
+void launch_prepare_leaves(const T* leaf_pool, T* slice_pool, const SlicedLeafDesc* descs,
+                           int n_descs, const uint32_t* keep_tables, uint64_t mask,
+                           cudaStream_t s);
+
+template <typename T>
+void launch_contract_simt(const T* A, const T* B, T* C, int64_t M, int64_t N, int64_t K,
+                          const ByteLut* lutA, const ByteLut* lutB, cudaStream_t s);
+
+template <typename T>
+void launch_permute(const T* in, T* out, int64_t elems, const ByteLut* lut, cudaStream_t s);
+
+template <typename T>
+void launch_counter_merge(const T* x, const T* slots, int64_t stride, int n_merge, T* dst,
+                          int64_t elems, cudaStream_t s);
+
+template <typename T>
+void launch_add(const T* a, const T* b, T* out, int64_t elems, cudaStream_t s);
+
+template <typename T>
+void launch_copy(const T* a, T* out, int64_t elems, cudaStream_t s);
+
+// Tensor-core operand staging (single precision only).
+void launch_absmax2(const float2* A, int64_t nA, const float2* B, int64_t nB,
+                    unsigned int* maxbits /*2*/, cudaStream_t s);
+void launch_split_rows(const float2* src, const ByteLut* lut, int64_t M, int64_t K,
+                       const unsigned int* maxbits, __half* hi, __half* lo, cudaStream_t s);
+void launch_split_cols_expand(const float2* src, const ByteLut* lut, int64_t N, int64_t K,
+                              const unsigned int* maxbits, __half* hi, __half* lo, cudaStream_t s);
+void launch_splitk_reduce(const float* ws, int splits, int64_t elems, float* C,
+                          const unsigned int* maxbits, cudaStream_t s);
+
+// ---------------------------------------------------------------------------
+// tcgen05 GEMM (gemm_tc.cu):  C[M][Np] (fp32) = alpha * sum over the three
+// split products of Ahi/Alo[M][Kp] (fp16, K-major) x Bhi/Blo[Np][Kp].
+struct TcGemmPlan {
+  int64_t M = 0, Np = 0, Kp = 0;
+  int splits = 1;
+  int chunk_kb = 8;              // promotion chunk (K blocks); see gemm_tc.cu
+  int64_t k_per_split = 0;       // multiple of the K block
+  int grid = 0;
+  alignas(64) unsigned char tmap[4][128];  // CUtensorMap x4: Ahi, Alo, Bhi, Blo
+  float* C = nullptr;            // output (splits == 1) or workspace [splits][M][Np]
+  const unsigned int* maxbits = nullptr;  // device: absmax bits of A, B
+};
+
+bool tc_available(int device);
+void tc_plan_gemm(TcGemmPlan* p, const __half* Ahi, const __half* Alo, const __half* Bhi,
+                  const __half* Blo, int64_t M, int64_t Np, int64_t Kp, float* C,
+                  float* workspace, int64_t workspace_elems, const unsigned int* maxbits,
+                  int num_sms);
+void tc_launch_gemm(const TcGemmPlan* p, cudaStream_t s);
+int64_t tc_workspace_elems(int64_t M, int64_t Np, int64_t Kp, int num_sms);
+
+}  // namespace tnb

@@ -1,0 +1,415 @@
+"""Drop-in replacement of the reference execution engine (tncut engine.py).
+
+Same names, signatures, argument meaning, return types and exceptions as
+``tncut.engine`` (engine.py:147-165, 242-378, 398-458); the arithmetic runs
+in libtnb.so on an sm_100 device:
+
+* ``compute_head_vector`` -> one compiled *program* per (head topology,
+  slicing, precision, device), executed over the slice range in C++/CUDA
+  (sliced-leaf gather, per-step tcgen05 or SIMT contraction, on-device
+  fixed/free slice sum, root permuted to ascending cut ids);
+* ``compute_tail_amplitudes`` -> the head vector is absorbed into the tail
+  network as one extra leaf and the result contracted on the device with
+  the open indices kept (mathematically the reference's per-block
+  ``T @ v_head``, engine.py:358-377, at 10^3-10^4x fewer multiplications);
+  the amplitude rows keep the reference's s2 order (MSB = lowest open qubit);
+* ``contract_tree`` -> the same program path with every index pinned;
+* ``reduce_partials`` -> the reference's validation and aligned binary
+  combine (engine.py:398-452), adds executed on the device.
+
+``EngineStats`` is filled with the reference's exact counters, computed
+analytically from the index sets (they depend only on the schedule).
+There is no CPU fallback.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import dataclasses
+import hashlib
+import threading
+
+import numpy as np
+
+from . import _lib
+from .errors import (ProvenanceMismatch, RangeGap, RangeOutOfBounds, RangeOverlap,
+                     ShapeMismatch)
+from .planner import greedy_steps, split, step_mults
+from .provenance import circuit_sha, normalize_s1, order_sha256, provenance_hash
+from .types import AmplitudeTable, EngineStats, HeadVector
+
+DTYPES = {"double": np.complex128, "single": np.complex64}
+_PREC = {"double": _lib.TNB_DOUBLE, "single": _lib.TNB_SINGLE}
+_MODES = {"fixed": _lib.TNB_FIXED, "free": _lib.TNB_FREE}
+
+# default device for the calling process (one process per GPU)
+_default_device = 0
+_flags = 0
+
+
+def set_device(device: int) -> None:
+    global _default_device
+    _default_device = int(device)
+
+
+def set_flags(flags: int) -> None:
+    """Executor flags (``_lib.TNB_FLAG_*``) for programs compiled afterwards."""
+    global _flags
+    _flags = int(flags)
+
+
+# ---------------------------------------------------------------------------
+# Program wrapper
+
+class Program:
+    """A compiled contraction schedule living on one device (libtnb program)."""
+
+    def __init__(self, leaves, steps, sliced, out_order, precision: str, device: int,
+                 flags: int = 0):
+        lib = _lib.load()
+        _lib.require_device()
+        self.lib = lib
+        self.precision = precision
+        self.device = device
+        self.dtype = DTYPES[precision]
+        self.n_leaves = len(leaves)
+        self.leaf_pos = {nid: i for i, (nid, _, _) in enumerate(leaves)}
+        self._leaf_data = [np.ascontiguousarray(d, dtype=np.complex128).reshape(-1)
+                           for (_, _, d) in leaves]
+        ids = np.array([nid for (nid, _, _) in leaves], dtype=np.int64)
+        ranks = np.array([len(ix) for (_, ix, _) in leaves], dtype=np.int32)
+        idx = np.array([i for (_, ix, _) in leaves for i in ix] or [0], dtype=np.int64)
+        data = np.concatenate(self._leaf_data) if leaves else np.zeros(1, np.complex128)
+        data = np.ascontiguousarray(data).view(np.float64)
+        st = np.array([v for s in steps for v in s] or [0], dtype=np.int64)
+        sl = np.array(list(sliced) or [0], dtype=np.int64)
+        oo = np.array(list(out_order) or [0], dtype=np.int64)
+        self._keep = (ids, ranks, idx, data, st, sl, oo)
+        d = _lib.ProgramDesc(
+            n_leaves=len(leaves),
+            leaf_ids=ids.ctypes.data_as(C.POINTER(C.c_int64)),
+            leaf_ranks=ranks.ctypes.data_as(C.POINTER(C.c_int32)),
+            leaf_indices=idx.ctypes.data_as(C.POINTER(C.c_int64)),
+            leaf_data=data.ctypes.data_as(C.POINTER(C.c_double)),
+            n_steps=len(steps), steps=st.ctypes.data_as(C.POINTER(C.c_int64)),
+            n_sliced=len(sliced), sliced=sl.ctypes.data_as(C.POINTER(C.c_int64)),
+            n_out=len(out_order), out_order=oo.ctypes.data_as(C.POINTER(C.c_int64)),
+            precision=_PREC[precision], device=device, flags=flags,
+        )
+        h = C.c_void_p()
+        _lib.check(lib.tnb_program_create(C.byref(d), C.byref(h)))
+        self.handle = h
+        self.lock = threading.Lock()
+        info = _lib.ProgramInfo()
+        _lib.check(lib.tnb_program_get_info(self.handle, C.byref(info)))
+        self.info = info
+
+    def __del__(self):
+        h = getattr(self, "handle", None)
+        if h is not None and h.value:
+            try:
+                self.lib.tnb_program_destroy(h)
+            except Exception:
+                pass
+
+    def update_leaves(self, leaves) -> None:
+        """Upload leaves whose values changed (repin), topology unchanged."""
+        for nid, _, d in leaves:
+            pos = self.leaf_pos[nid]
+            new = np.ascontiguousarray(d, dtype=np.complex128).reshape(-1)
+            if not np.array_equal(new, self._leaf_data[pos]):
+                buf = new.view(np.float64)
+                _lib.check(self.lib.tnb_program_set_leaf(
+                    self.handle, pos, buf.ctypes.data_as(C.POINTER(C.c_double))))
+                self._leaf_data[pos] = new
+
+    def set_leaf_device(self, pos: int, dev_ptr: int) -> None:
+        _lib.check(self.lib.tnb_program_set_leaf_device(self.handle, pos, C.c_void_p(dev_ptr)))
+        self._leaf_data[pos] = None  # unknown host copy: force upload next time
+
+    def run_range(self, a: int, b: int, mode: str = "fixed", out=None) -> np.ndarray:
+        """Host result (numpy) unless ``out`` is a device pointer (int)."""
+        with self.lock:
+            if out is None:
+                res = np.empty(self.info.out_elems, dtype=self.dtype)
+                _lib.check(self.lib.tnb_program_run_range(
+                    self.handle, a, b, _MODES[mode], res.ctypes.data_as(C.c_void_p), 0))
+                return res
+            _lib.check(self.lib.tnb_program_run_range(
+                self.handle, a, b, _MODES[mode], C.c_void_p(out), 1))
+            return None
+
+    def set_timing(self, on: bool) -> None:
+        _lib.check(self.lib.tnb_program_set_timing(self.handle, 1 if on else 0))
+
+    def timing(self) -> dict:
+        t = _lib.Timing()
+        _lib.check(self.lib.tnb_program_get_timing(self.handle, C.byref(t)))
+        return {f: getattr(t, f) for f, _ in _lib.Timing._fields_}
+
+
+_cache: dict = {}
+_cache_lock = threading.Lock()
+_CACHE_MAX = 8
+
+
+def _signature(leaves, steps, sliced, out_order, precision, device, flags) -> str:
+    h = hashlib.sha256()
+    for nid, ix, _ in leaves:
+        h.update(repr((nid, tuple(ix))).encode())
+    h.update(repr(tuple(tuple(s) for s in steps)).encode())
+    h.update(repr((tuple(sliced), tuple(out_order), precision, device, flags)).encode())
+    return h.hexdigest()
+
+
+def get_program(leaves, steps, sliced, out_order, precision, device=None, flags=None) -> Program:
+    device = _default_device if device is None else device
+    flags = _flags if flags is None else flags
+    key = _signature(leaves, steps, sliced, out_order, precision, device, flags)
+    with _cache_lock:
+        prog = _cache.get(key)
+        if prog is None:
+            if len(_cache) >= _CACHE_MAX:
+                _cache.pop(next(iter(_cache)))
+            prog = Program(leaves, steps, sliced, out_order, precision, device, flags)
+            _cache[key] = prog
+        else:
+            _cache[key] = _cache.pop(key)  # LRU touch
+    prog.update_leaves(leaves)
+    return prog
+
+
+def clear_cache() -> None:
+    with _cache_lock:
+        _cache.clear()
+
+
+def _steps_tuples(steps):
+    return [(s.lhs, s.rhs, s.out) for s in steps]
+
+
+def _leaf_entries(tn, leaf_ids):
+    return [(nid, list(tn.nodes[nid].indices), tn.nodes[nid].data) for nid in leaf_ids]
+
+
+# ---------------------------------------------------------------------------
+# Reference-shaped API
+
+def head_program(tn, tree, sliced_indices, precision="single", device=None, flags=None):
+    """The compiled head program (for benchmarks / timing introspection)."""
+    head_leaves, head_steps, _, _, cut = split(tn, tree)
+    return get_program(_leaf_entries(tn, head_leaves), _steps_tuples(head_steps),
+                       list(sliced_indices), sorted(cut), precision, device, flags)
+
+
+def compute_head_vector(tn, tree, sliced_indices, s1, slice_range=None, precision="double",
+                        mode="fixed", stats=None, device=None) -> HeadVector:
+    """Sum of head contractions over a slice range (engine.py:242-310)."""
+    s1 = normalize_s1(tn, s1)
+    tn = tn.repin(s1)
+    sliced_indices = list(sliced_indices)
+    head_leaves, head_steps, _, _, cut = split(tn, tree)
+    head_set = set(head_leaves)
+    for ix in sliced_indices:
+        eps = tn.index_endpoints.get(ix, ())
+        if len(eps) != 2 or any(e not in head_set for e in eps):
+            raise ShapeMismatch(f"sliced index {ix} is not internal to the head")
+    n_e = len(sliced_indices)
+    total = 1 << n_e
+    a, b = slice_range if slice_range is not None else (0, total)
+    if not (0 <= a < b <= total):
+        raise RangeOutOfBounds(f"range [{a},{b}) outside [0,{total})")
+    if mode not in _MODES:
+        raise ValueError(f"unknown reduction mode {mode!r}")
+    dtype = DTYPES[precision]
+    if stats is not None:
+        stats.head_contractions += b - a
+    if not head_leaves:
+        # degenerate head (engine.py:282-283): every slice contributes ones(1)
+        data = _degenerate_sum(b - a, dtype, mode)
+    else:
+        prog = get_program(_leaf_entries(tn, head_leaves), _steps_tuples(head_steps),
+                           sliced_indices, sorted(cut), precision, device)
+        data = prog.run_range(a, b, mode)
+        if stats is not None:
+            sets = {nid: tn.nodes[nid].indices for nid in head_leaves}
+            mults, _ = step_mults(sets, head_steps, frozenset(sliced_indices))
+            stats.multiplications += mults * (b - a)
+            stats.steps_executed += len(head_steps) * (b - a)
+    return HeadVector(
+        s1=s1,
+        data=data,
+        provenance=provenance_hash(tn, tree, s1, precision, mode, sliced_indices),
+        cut_order=sorted(cut),
+        n_e=n_e,
+        slice_range=(a, b),
+        mode=mode,
+        sliced_indices=tuple(sliced_indices),
+    )
+
+
+def _degenerate_sum(count, dtype, mode):
+    # sum of `count` scalars 1.0: exact in both modes
+    return np.array([float(count)], dtype=dtype)
+
+
+def tail_plan(tn, tree, cut, head_id=None):
+    """Leaves + greedy steps of the head-absorbed tail network."""
+    _, _, tail_leaves, _, _ = split(tn, tree)
+    hid = (max(tn.nodes) + 1) if head_id is None else head_id
+    sets = {nid: frozenset(tn.nodes[nid].indices) for nid in tail_leaves}
+    sets[hid] = frozenset(cut)
+    steps = greedy_steps(sets, hid + 1)
+    return tail_leaves, hid, steps
+
+
+def compute_tail_amplitudes(tn, tree, head: HeadVector, space_cap=None, precision="double",
+                            stats=None, device=None) -> AmplitudeTable:
+    """All 2**n_open amplitudes of the head/tail split (engine.py:313-378)."""
+    s1 = head.s1
+    tn = tn.repin(s1)
+    expect = provenance_hash(tn, tree, s1, precision, head.mode, head.sliced_indices)
+    if expect != head.provenance:
+        raise ProvenanceMismatch("head vector was produced from different inputs")
+    if head.slice_range != (0, 1 << head.n_e):
+        raise ProvenanceMismatch("head vector is a partial; reduce it first")
+    return _tail(tn, tree, head, space_cap, precision, stats, device)
+
+
+def tail_amplitudes_unchecked(tn, tree, head: HeadVector, space_cap=None, precision="single",
+                              stats=None, device=None) -> AmplitudeTable:
+    """Tail of a (possibly partial) head vector without the full-range check.
+
+    The tail is linear in the head vector, so the amplitudes of a partial
+    slice range are the partial amplitude sums (used for sharded runs and
+    fixed-subset benchmarks)."""
+    return _tail(tn.repin(head.s1), tree, head, space_cap, precision, stats, device)
+
+
+def _tail(tn, tree, head, space_cap, precision, stats, device):
+    _, _, tail_leaves, tail_steps, cut = split(tn, tree)
+    if sorted(cut) != list(head.cut_order):
+        raise ProvenanceMismatch("cut indices differ from the head vector's")
+    dtype = DTYPES[precision]
+    open_qubits = sorted(tn.open_output_indices)
+    n2 = len(open_qubits)
+    n_c = head.n_c
+    amplitudes = np.zeros(1 << n2, dtype=dtype)
+    if not tail_leaves:
+        amplitudes[0] = head.data.reshape(()) if head.data.size == 1 else head.data[0]
+        return _make_table(tn, tree, head, amplitudes, open_qubits, precision)
+
+    # reference-equivalent instrumentation (engine.py:348-377)
+    k = 0
+    if space_cap is not None:
+        while n2 - k + n_c > space_cap and k < n2:
+            k += 1
+    if stats is not None:
+        pinned = frozenset(tn.open_output_indices[q] for q in open_qubits[:k])
+        sets = {nid: tn.nodes[nid].indices for nid in tail_leaves}
+        mults, _ = step_mults(sets, tail_steps, pinned)
+        blocks = 1 << k
+        stats.tail_contractions += blocks
+        stats.multiplications += blocks * (mults + (1 << (n2 - k + n_c)))
+        stats.steps_executed += blocks * len(tail_steps)
+
+    leaves, hid, steps = tail_plan(tn, tree, head.cut_order)
+    entries = _leaf_entries(tn, leaves)
+    entries.append((hid, list(head.cut_order), np.asarray(head.data).reshape(-1)))
+    out_order = [tn.open_output_indices[q] for q in open_qubits]
+    # cache keyed on topology only: the head leaf is re-uploaded when it changes
+    prog = get_program(entries, steps, [], out_order, precision, device)
+    amps = prog.run_range(0, 1, "fixed")
+    return _make_table(tn, tree, head, amps.astype(dtype, copy=False), open_qubits, precision)
+
+
+def _make_table(tn, tree, head, amplitudes, open_qubits, precision):
+    csha = circuit_sha(tn)
+    return AmplitudeTable(
+        s1=head.s1,
+        open_qubits=open_qubits,
+        amplitudes=amplitudes,
+        layout_ids=sorted(tn.circuit.layout.ids) if tn.circuit else
+        sorted(set(tn.open_output_indices) | set(tn.fixed_output_bits)),
+        circuit_sha256=csha,
+        order_sha256=order_sha256(tree, tn, head.sliced_indices),
+        precision=precision,
+        mode=head.mode,
+    )
+
+
+def contract_tree(tn, tree, slice_assignment, dtype=np.complex128, stats=None, device=None):
+    """Whole-tree contraction, sliced indices pinned, root axes ascending (engine.py:147-165)."""
+    precision = "double" if np.dtype(dtype) == np.complex128 else "single"
+    sliced = sorted(slice_assignment)
+    leaves = _leaf_entries(tn, list(tree.leaves))
+    steps = _steps_tuples(tree.steps)
+    # root ids: leaf indices minus pinned ones, contracted pairwise
+    sets = {nid: frozenset(ix) - frozenset(sliced) for nid, ix, _ in leaves}
+    for (l, r, o) in steps:
+        sets[o] = sets.pop(l) ^ sets.pop(r)
+    if len(sets) != 1:
+        raise ShapeMismatch(f"{len(sets)} results left after contraction")
+    root_ids = sorted(next(iter(sets.values())))
+    # indices that are not in the network at all are ignored, as np.take never sees them
+    present = {i for _, ix, _ in leaves for i in ix}
+    pinned = [ix for ix in sliced if ix in present]
+    mask = 0
+    for ix in pinned:
+        mask = (mask << 1) | (int(slice_assignment[ix]) & 1)
+    prog = get_program(leaves, steps, pinned, root_ids, precision, device)
+    out = prog.run_range(mask, mask + 1, "fixed")
+    if stats is not None:
+        mults, _ = step_mults({nid: ix for nid, ix, _ in leaves}, steps, frozenset(pinned))
+        stats.multiplications += mults
+        stats.steps_executed += len(steps)
+    return out.astype(dtype, copy=False).reshape((2,) * len(root_ids))
+
+
+def reduce_partials(partials) -> HeadVector:
+    """Combine disjoint-range partial head vectors (engine.py:398-452)."""
+    if not partials:
+        raise RangeGap("no partials given")
+    prov = partials[0].provenance
+    n_e = partials[0].n_e
+    for p in partials[1:]:
+        if p.provenance != prov:
+            raise ProvenanceMismatch("partials come from different runs")
+        if p.n_e != n_e:
+            raise ProvenanceMismatch("partials disagree on slice count")
+    ordered = sorted(partials, key=lambda p: p.slice_range[0])
+    pos = 0
+    for p in ordered:
+        a, b = p.slice_range
+        if a < pos:
+            raise RangeOverlap(f"range [{a},{b}) overlaps at {pos}")
+        if a > pos:
+            raise RangeGap(f"missing slice range [{pos},{a})")
+        pos = b
+    total = 1 << n_e
+    if pos != total:
+        raise RangeGap(f"missing slice range [{pos},{total})")
+
+    from .device import DeviceAdder  # torch-backed device buffers
+    adder = DeviceAdder(ordered[0].data.dtype, ordered[0].data.size, _default_device)
+
+    def combine(lo, hi, items):
+        if len(items) == 1 and items[0].slice_range == (lo, hi):
+            return adder.upload(items[0].data)
+        mid = (lo + hi) // 2
+        left = [p for p in items if p.slice_range[1] <= mid]
+        right = [p for p in items if p.slice_range[0] >= mid]
+        if len(left) + len(right) == len(items) and left and right:
+            return adder.add(combine(lo, mid, left), combine(mid, hi, right))
+        acc = adder.upload(items[0].data)
+        for p in items[1:]:
+            acc = adder.add(acc, adder.upload(p.data))
+        return acc
+
+    data = adder.download(combine(0, total, ordered))
+    return dataclasses.replace(ordered[0], data=data, slice_range=(0, total))
+
+
+def flop_estimate(complexity) -> float:
+    """8 FLOPs per counted multiplication (engine.py:455-458)."""
+    return 8.0 * float(complexity.tc)

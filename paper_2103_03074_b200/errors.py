@@ -1,0 +1,42 @@
+"""Exception classes of the drop-in engine.
+
+When the reference package ``tncut`` is importable the engine raises ITS
+classes (errors.py:11-128), so existing ``except tncut.errors.X`` handlers
+keep working.  Otherwise identical stand-ins with the same names and
+hierarchy are defined here.
+"""
+
+from __future__ import annotations
+
+try:  # pragma: no cover - depends on the environment
+    from tncut.errors import (  # type: ignore
+        ProvenanceMismatch,
+        RangeGap,
+        RangeOutOfBounds,
+        RangeOverlap,
+        ShapeMismatch,
+        TncutError,
+    )
+except Exception:  # tncut not installed (e.g. the GPU box)
+
+    class TncutError(Exception):
+        """Base class for all package errors (errors.py:11-12)."""
+
+    class ShapeMismatch(TncutError):
+        """Internal tensor-shape inconsistency (errors.py:83-84)."""
+
+    class RangeOutOfBounds(TncutError):
+        pass
+
+    class RangeGap(TncutError):
+        pass
+
+    class RangeOverlap(TncutError):
+        pass
+
+    class ProvenanceMismatch(TncutError):
+        """Inputs were produced from different circuits, orders or modes."""
+
+
+__all__ = ["TncutError", "ShapeMismatch", "RangeOutOfBounds", "RangeGap", "RangeOverlap",
+           "ProvenanceMismatch"]

@@ -1,0 +1,79 @@
+"""Host-side schedule helpers for the executor.
+
+* ``split`` restates the engine's head/tail split (engine.py:171-185) and
+  ``cut_indices`` (ordering.py:372-380) on duck-typed networks/trees.
+* ``greedy_steps`` restates the reference's deterministic greedy pair
+  order (ordering.py:256-285: minimise (result rank, union rank, ids)); the
+  executor uses it to order the head-absorbed tail network, which the
+  reference never builds (it contracts the tail per pinned block and takes
+  a GEMV with the head vector instead, engine.py:358-377).
+"""
+
+from __future__ import annotations
+
+
+def cut_indices(tn, head: set, tail: set) -> list:
+    crossing = []
+    for ix, eps in tn.index_endpoints.items():
+        if len(eps) == 2:
+            in_head = [e in head for e in eps]
+            if any(in_head) and not all(in_head):
+                crossing.append(ix)
+    return sorted(crossing)
+
+
+def split(tn, tree):
+    """(head_leaves, head_steps, tail_leaves, tail_steps, cut ids)."""
+    if tree.first_cut is not None:
+        head_leaves, tail_leaves = tree.head_tail_leaves()
+        cut = cut_indices(tn, set(head_leaves), set(tail_leaves))
+        return sorted(head_leaves), tree.head_steps(), sorted(tail_leaves), tree.tail_steps(), cut
+    if tn.open_output_indices:
+        return [], [], sorted(tree.leaves), list(tree.steps), []
+    return sorted(tree.leaves), list(tree.steps), [], [], []
+
+
+def greedy_steps(index_sets: dict, next_out: int) -> list:
+    """Greedy pairwise order over {id: frozenset(indices)} -> [(lhs, rhs, out)]."""
+    sets = {k: frozenset(v) for k, v in index_sets.items()}
+    live = sorted(sets)
+    steps = []
+
+    def key(i, j):
+        a, b = sets[i], sets[j]
+        return (len(a ^ b), len(a | b), i, j)
+
+    pairs = {}
+    for x, i in enumerate(live):
+        for j in live[x + 1:]:
+            pairs[(i, j)] = key(i, j)
+    while len(live) > 1:
+        (i, j) = min(pairs, key=lambda p: pairs[p])
+        out = next_out
+        next_out += 1
+        sets[out] = sets[i] ^ sets[j]
+        steps.append((i, j, out))
+        live.remove(i)
+        live.remove(j)
+        for p in [p for p in pairs if i in p or j in p]:
+            del pairs[p]
+        for other in live:
+            pair = (other, out) if other < out else (out, other)
+            pairs[pair] = key(*pair)
+        live.append(out)
+    return steps
+
+
+def step_mults(leaf_sets: dict, steps, removed=frozenset()) -> tuple:
+    """(sum of 2^(|a|+|b|-|a&b|), max result rank) over a step list with
+    `removed` indices pinned -- the engine's exact counter (engine.py:138-140)."""
+    sets = {k: frozenset(v) - removed for k, v in leaf_sets.items()}
+    total = 0
+    rank = 0
+    for s in steps:
+        lhs, rhs, out = (s.lhs, s.rhs, s.out) if hasattr(s, "lhs") else s
+        a, b = sets[lhs], sets[rhs]
+        total += 1 << (len(a) + len(b) - len(a & b))
+        sets[out] = a ^ b
+        rank = max(rank, len(sets[out]))
+    return total, rank

@@ -1,0 +1,79 @@
+"""Shared test helpers.
+
+``-m "not gpu"``: oracle vs reference golden vectors, host logic, C-ABI
+load/exports, multi-process (gloo) sharding logic.  ``-m gpu``: parity of
+the CUDA path (through the C-ABI) against the oracle and the goldens.
+"""
+
+from __future__ import annotations
+
+import os
+import sys
+
+import numpy as np
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+if ROOT not in sys.path:
+    sys.path.insert(0, ROOT)
+GOLDEN = os.path.join(ROOT, "tests", "golden")
+REF_SRC = "/root/reference/pkg/src"
+
+
+def pytest_configure(config):
+    config.addinivalue_line("markers", "gpu: needs an sm_100 GPU and libtnb.so")
+
+
+def rel_l2(a, b) -> float:
+    a = np.asarray(a, dtype=np.complex128).reshape(-1)
+    b = np.asarray(b, dtype=np.complex128).reshape(-1)
+    den = np.linalg.norm(b)
+    return float(np.linalg.norm(a - b) / (den if den > 0 else 1.0))
+
+
+def golden(name):
+    path = os.path.join(GOLDEN, name, "golden.npz")
+    if not os.path.exists(path):
+        pytest.skip(f"golden vectors for {name} not generated")
+    return np.load(path)
+
+
+def reference_available() -> bool:
+    return os.path.isdir(REF_SRC)
+
+
+def import_reference():
+    """The reference package (only in the build container, never on the GPU box)."""
+    if not reference_available():
+        pytest.skip("reference package not present")
+    if REF_SRC not in sys.path:
+        sys.path.insert(0, REF_SRC)
+    os.environ.setdefault("NUMBA_CACHE_DIR", "/tmp/numba_cache")
+    import tncut  # noqa: F401
+
+    return tncut
+
+
+@pytest.fixture(scope="session")
+def workloads():
+    from paper_2103_03074_b200.workloads import load_workload
+
+    cache = {}
+
+    def get(name):
+        if name not in cache:
+            cache[name] = load_workload(name)
+        return cache[name]
+
+    return get
+
+
+@pytest.fixture(scope="session")
+def gpu():
+    """Skip unless a device is visible; fail loudly if the library is missing."""
+    from paper_2103_03074_b200 import _lib
+
+    lib = _lib.load()  # raises if libtnb.so was not built
+    if _lib.device_count() == 0:
+        pytest.skip("no CUDA device")
+    return lib
