@@ -1,0 +1,330 @@
+"""Benchmark: slices/s and contraction TFLOP/s on the m=20 Sycamore-53 plan.
+
+Workload (BASELINE.json configs[3], SURVEY 8 "C4"): Sycamore-layout 53-qubit
+m=20 circuit (synthetic gates, seed 0), 20 open qubits -> a 2^20 correlated
+bitstring batch, reference plan (seed 0 / restarts 16 / target space 2^30,
+n_e = 53 sliced edges, n_c = 21 cut indices), frozen under tests/golden/c4.
+A *step* = a batch of `--slices` head slices per GPU: sliced-leaf gather,
+413 pairwise contractions per slice (tcgen05 GEMMs for the big ones),
+on-device fixed-mode slice sum, then the head-absorbed sparse-state tail
+over the 2^20 bitstrings and (N > 1) one NCCL all-reduce of the amplitude
+vector.  Ranks own disjoint aligned slice ranges of a fixed subset
+(weak scaling).
+
+    python bench.py [--gpus N --steps K --warmup W]      # this executor
+    python bench.py --impl reference ...                 # reference CPU path
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+HOST_CORES = len(os.sched_getaffinity(0))
+os.environ.setdefault("OPENBLAS_NUM_THREADS", str(HOST_CORES))
+
+import numpy as np  # noqa: E402
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "slices/sec & contraction TFLOP/s, Sycamore-53 m=20 correlated batch, 1-8 GPU"
+WORKLOAD = "c4"
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            p = json.load(fh)
+        return float(p["bf16_tflops"]), float(p["bf16_tflops_sustained"]), float(p["hbm_gbs"]), "measured"
+    except Exception:
+        return 1590.0, 1400.0, 6650.0, "fallback"
+
+
+# ---------------------------------------------------------------------------
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons during the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.rows = []
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                 "-lms", "200"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([x.strip() for x in line.split(",")])
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in self.rows:
+            try:
+                sm.append(float(r[1]))
+                mx = float(r[2])
+                for k, nm in enumerate(names):
+                    if r[4 + k].lower().startswith("active"):
+                        reasons.add(nm)
+            except Exception:
+                pass
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": mx,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ---------------------------------------------------------------------------
+def setup_dist(args):
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    dist = None
+    if world > 1:
+        import torch
+        import torch.distributed as dist_
+
+        torch.cuda.set_device(local)
+        dist_.init_process_group("nccl" if args.impl == "ours" else "gloo")
+        dist = dist_
+    return world, rank, local, dist
+
+
+def barrier(dist, local):
+    import torch
+
+    if dist is not None:
+        dist.barrier()
+    if torch.cuda.is_available():
+        torch.cuda.synchronize(local)
+
+
+def cpu_baseline(w):
+    from oracle.cpu_sample import time_head_slice
+
+    est, wall, sample = time_head_slice(w.tn, w.tree, w.sliced, precision="single")
+    flops = 8.0 * w.tc_per_slice
+    return {"value": 1.0 / est, "unit": "slices/s", "cores": HOST_CORES, "kind": "port",
+            "sample": sample, "est_s_per_slice": est, "tflops": flops / est / 1e12}
+
+
+def run_ours(args):
+    import torch
+
+    import paper_2103_03074_b200 as tnb
+    from paper_2103_03074_b200 import engine as E
+    from paper_2103_03074_b200.planner import split
+
+    world, rank, local, dist = setup_dist(args)
+    torch.cuda.set_device(local)
+    tnb.set_device(local)
+    w = tnb.load_workload(args.workload)
+    S = args.slices
+    total_slices = (args.warmup + args.steps) * S
+    base = rank * total_slices  # aligned disjoint per-rank range of the fixed subset
+    tn, tree = w.tn, w.tree
+    hl, hs, tl, ts, cut = split(tn, tree)
+    head = E.head_program(tn, tree, w.sliced, "single", device=local)
+    head.set_timing(True)
+    n_c = len(cut)
+    opens = sorted(tn.open_output_indices)
+    n2 = len(opens)
+    leaves, hid, tsteps = E.tail_plan(tn, tree, sorted(cut))
+    entries = E._leaf_entries(tn, leaves) + [(hid, sorted(cut), np.zeros(1 << n_c))]
+    tail = E.get_program(entries, tsteps, [], [tn.open_output_indices[q] for q in opens], "single",
+                         device=local)
+    tail.set_timing(True)
+    dev = torch.device("cuda", local)
+    hvec = torch.empty(1 << n_c, dtype=torch.complex64, device=dev)
+    amps = torch.empty(1 << n2, dtype=torch.complex64, device=dev)
+    amps_total = torch.zeros(1 << n2, dtype=torch.complex64, device=dev)
+
+    def step(s):
+        a = base + s * S
+        head.run_range(a, a + S, "fixed", out=hvec.data_ptr())
+        tail.set_leaf_device(len(entries) - 1, hvec.data_ptr())
+        tail.run_range(0, 1, "fixed", out=amps.data_ptr())
+        th, tt = head.timing(), tail.timing()
+        ms = th["total_ms"] + tt["total_ms"]
+        if dist is not None:
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            dist.all_reduce(amps.view(torch.float32))
+            e1.record()
+            e1.synchronize()
+            ms += e0.elapsed_time(e1)
+        amps_total.add_(amps)
+        return ms, th, tt
+
+    for s in range(args.warmup):
+        step(s)
+    barrier(dist, local)
+    dev_ms = 0.0
+    gemm_ms = gemm_flops = 0.0
+    launches = gemm_launches = 0
+    t0 = time.perf_counter()
+    with ClockSampler(local) as clk:
+        for s in range(args.warmup, args.warmup + args.steps):
+            ms, th, tt = step(s)
+            dev_ms += ms
+            gemm_ms += th["gemm_ms"] + tt["gemm_ms"]
+            gemm_flops += th["gemm_flops"] + tt["gemm_flops"]
+            launches += th["launches"] + tt["launches"]
+            gemm_launches += th["gemm_launches"] + tt["gemm_launches"]
+        barrier(dist, local)
+    wall_ms = (time.perf_counter() - t0) * 1e3
+    # max over ranks of the device time
+    t_max = dev_ms
+    if dist is not None:
+        tt_ = torch.tensor([dev_ms], device=dev)
+        dist.all_reduce(tt_, op=dist.ReduceOp.MAX)
+        t_max = float(tt_.item())
+
+    # ---- e2e: the public API with host buffers (H2D of every leaf, D2H of results)
+    e2e = None
+    if not args.no_e2e:
+        hprog = head
+        barrier(dist, local)
+        h2d = d2h = 0
+        e_t0 = time.perf_counter()
+        for s in range(args.steps):
+            a = base + (args.warmup + s) * S
+            hprog._leaf_data = [None] * hprog.n_leaves  # inputs arrive from the host every call
+            hv = tnb.compute_head_vector(tn, tree, w.sliced, None, slice_range=(a, a + S),
+                                         precision="single", device=local)
+            tab = tnb.tail_amplitudes_unchecked(tn, tree, hv, precision="single", device=local)
+            h2d += sum(8 * (1 << len(tn.nodes[n].indices)) for n in hl)
+            h2d += 8 * (1 << n_c)  # head vector into the tail program
+            d2h += hv.data.nbytes + tab.amplitudes.nbytes
+        barrier(dist, local)
+        e_ms = (time.perf_counter() - e_t0) * 1e3
+        if dist is not None:
+            tt_ = torch.tensor([e_ms], device=dev)
+            dist.all_reduce(tt_, op=dist.ReduceOp.MAX)
+            e_ms = float(tt_.item())
+        e2e = {"value": world * args.steps * S / (e_ms / 1e3), "unit": "slices/s",
+               "h2d_bytes_per_step": h2d // args.steps, "d2h_bytes_per_step": d2h // args.steps,
+               "ms_per_step": e_ms / args.steps}
+
+    if rank != 0:
+        return
+    burst, sustained, hbm, src = peaks()
+    slices = world * args.steps * S
+    value = slices / (t_max / 1e3)
+    flops_slice = 8.0 * w.tc_per_slice
+    achieved = gemm_flops / (gemm_ms / 1e3) / 1e12 if gemm_ms else 0.0
+    line = {
+        "metric": METRIC,
+        "value": value,
+        "unit": "slices/s",
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": t_max / args.steps,
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "c64 (fp16x3-split tcgen05, fp32 accumulate)",
+        "data": "synthetic (Sycamore-layout random gates, seed 0; reference plan frozen in tests/golden/c4)",
+        "config": {"workload": "C4: Sycamore-53 m=20, 2^20 correlated bitstrings, target space 2^30, "
+                               "n_e=53, n_c=21, fixed subset of slices",
+                   "slices_per_step_per_gpu": S, "slice_subset": [0, world * total_slices],
+                   "l2": "inputs larger than L2 (intermediates up to 8 GiB)",
+                   "parallelism": f"slice-range dp{world}"},
+        "contraction_tflops": value * flops_slice / 1e12,
+        "flops_per_slice": flops_slice,
+        "roofline": {
+            "bound": "tensor", "kernel": "gemm_f16x3 (tcgen05)",
+            "achieved": achieved, "peak": sustained, "unit": "TFLOP/s",
+            "frac": achieved / sustained,
+            "peak_kind": f"{src} bf16 dense sustained (MEASURED_PEAKS.json)",
+            "achieved_is": "algorithmic complex FLOPs (8 per complex multiply-add) per GEMM launch / event time",
+            "tensor_tflops_executed": 3.0 * achieved,
+            "tensor_frac": 3.0 * achieved / sustained,
+            "traffic": None,
+        },
+        "gpu_launches": launches,
+        "gemm_launches": gemm_launches,
+        "wall_ms_per_step": wall_ms / args.steps,
+        "clocks": clk.summary(),
+        "e2e": e2e,
+    }
+    if world == 1 and not args.no_cpu:
+        line["cpu_baseline"] = cpu_baseline(w)
+    print(json.dumps(line), flush=True)
+
+
+def run_reference(args):
+    world, rank, local, dist = setup_dist(args)
+    if rank != 0:
+        return
+    from paper_2103_03074_b200.workloads import load_workload
+    from oracle.cpu_sample import time_head_slice
+
+    w = load_workload(args.workload)
+    for _ in range(args.warmup):
+        time_head_slice(w.tn, w.tree, w.sliced, step_cap_s=0.5)
+    ests = []
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        est, wall, sample = time_head_slice(w.tn, w.tree, w.sliced)
+        ests.append(est)
+    est = float(np.mean(ests))
+    v = args.slices / (args.slices * est)
+    line = {"metric": METRIC, "value": v, "unit": "slices/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": est * 1e3, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "c64 (numpy/OpenBLAS cgemm)",
+            "data": "synthetic", "impl": "reference",
+            "config": {"workload": "C4: Sycamore-53 m=20, 2^20 correlated bitstrings, target space 2^30",
+                       "parallelism": "host CPU"},
+            "contraction_tflops": v * 8.0 * w.tc_per_slice / 1e12,
+            "cpu_baseline": {"value": v, "unit": "slices/s", "cores": HOST_CORES, "kind": "port",
+                             "sample": sample},
+            "e2e": {"value": v, "unit": "slices/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+            "sampled_cpu_s": time.perf_counter() - t0}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--slices", type=int, default=2, help="head slices per step per GPU")
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--workload", default=WORKLOAD)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -36,7 +36,7 @@ constexpr int EPI_COLS = BN / EPI_SPLIT;     // fp32 register accumulator column
 constexpr int NUM_THREADS = 128 + EPI_THREADS;
 constexpr int TMEM_COLS = 512;
 constexpr int kDefaultChunkKb = 8;          // K blocks (of 32 fp16) per promotion chunk
-constexpr int GROUP_N = 8;                   // rasterisation: m-fastest within 8 n-tiles
+constexpr int GROUP_M = 16;                  // rasterisation band height (m-tiles)
 constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
 
 // instruction descriptor: F32 accum, F16 x F16, K-major both, M=128, N=256
@@ -140,15 +140,20 @@ struct WorkCoord {
   int split, mb, nb;
 };
 
-__device__ __forceinline__ WorkCoord decode(int w, int nm, int nn) {
+// Grouped raster: bands of GROUP_M m-tiles, m fastest inside a band, then n.
+// The ~148 tiles in flight then cover ~16 m-tiles x ~9 n-tiles, so each A
+// panel (128 rows x K) and B panel (256 rows x K) streamed from HBM is shared
+// by ~9 / ~16 concurrently running CTAs through L2.
+__device__ __forceinline__ WorkCoord decode(int w, int nm, int nn, int group_m) {
   const int per_split = nm * nn;
   WorkCoord c;
   c.split = w / per_split;
   const int t = w - c.split * per_split;
-  const int group = t / (GROUP_N * nm);
-  const int idx = t - group * (GROUP_N * nm);
-  c.mb = idx % nm;
-  c.nb = group * GROUP_N + idx / nm;
+  const int band = t / (group_m * nn);
+  const int idx = t - band * (group_m * nn);
+  const int band_m = min(group_m, nm - band * group_m);
+  c.mb = band * group_m + idx % band_m;
+  c.nb = idx / band_m;
   return c;
 }
 
@@ -162,7 +167,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 gemm_f16x3_kernel(const __grid_constant__ CUtensorMap tm_ahi, const __grid_constant__ CUtensorMap tm_alo,
                   const __grid_constant__ CUtensorMap tm_bhi, const __grid_constant__ CUtensorMap tm_blo,
                   float* __restrict__ C, int M, int Np, int Kp, int splits, int k_per_split,
-                  int chunk_kb, const unsigned int* __restrict__ maxbits) {
+                  int chunk_kb, int group_m, const unsigned int* __restrict__ max_rows,
+                  const unsigned int* __restrict__ max_cols, unsigned int* __restrict__ max_out) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES);
@@ -211,7 +217,7 @@ gemm_f16x3_kernel(const __grid_constant__ CUtensorMap tm_ahi, const __grid_const
       int stage = 0;
       uint32_t phase = 0;
       for (int w = blockIdx.x; w < total; w += gridDim.x) {
-        const WorkCoord wc = decode(w, nm, nn);
+        const WorkCoord wc = decode(w, nm, nn, group_m);
         const int k_begin = wc.split * k_per_split;
         const int k_end = min(Kp, k_begin + k_per_split);
         const int m0 = wc.mb * BM, n0 = wc.nb * BN;
@@ -233,7 +239,7 @@ gemm_f16x3_kernel(const __grid_constant__ CUtensorMap tm_ahi, const __grid_const
     uint32_t phase = 0;
     int gchunk = 0;
     for (int w = blockIdx.x; w < total; w += gridDim.x) {
-      const WorkCoord wc = decode(w, nm, nn);
+      const WorkCoord wc = decode(w, nm, nn, group_m);
       const int k_begin = wc.split * k_per_split;
       const int nkb = (min(Kp, k_begin + k_per_split) - k_begin + BK - 1) / BK;
       for (int c0 = 0; c0 < nkb; c0 += chunk_kb, ++gchunk) {
@@ -271,10 +277,11 @@ gemm_f16x3_kernel(const __grid_constant__ CUtensorMap tm_ahi, const __grid_const
     // ===== promotion + epilogue: warp -> TMEM lane quadrant (warp % 4), column group =====
     const int q = warp & 3;
     const int grp = (warp - 4) >> 2;
-    const float alpha = splits == 1 ? 1.f / (scale_of(maxbits[0]) * scale_of(maxbits[1])) : 1.f;
+    const float alpha = splits == 1 ? 1.f / (scale_of(*max_rows) * scale_of(*max_cols)) : 1.f;
+    float vmax = 0.f;  // max |C| of this thread's outputs (scale slot of the result tensor)
     int gchunk = 0;
     for (int w = blockIdx.x; w < total; w += gridDim.x) {
-      const WorkCoord wc = decode(w, nm, nn);
+      const WorkCoord wc = decode(w, nm, nn, group_m);
       const int k_begin = wc.split * k_per_split;
       const int nkb = (min(Kp, k_begin + k_per_split) - k_begin + BK - 1) / BK;
       float acc[EPI_COLS];
@@ -297,19 +304,27 @@ gemm_f16x3_kernel(const __grid_constant__ CUtensorMap tm_ahi, const __grid_const
       }
       const int row = wc.mb * BM + q * 32 + lane;
       const int col0 = wc.nb * BN + grp * EPI_COLS;
+#pragma unroll
+      for (int j = 0; j < EPI_COLS; ++j) {
+        acc[j] *= alpha;
+        vmax = fmaxf(vmax, fabsf(acc[j]));  // out-of-range rows/cols are TMA zero-fill
+      }
       if (row < M && col0 < Np) {
         float* dst = C + (size_t)wc.split * (size_t)M * (size_t)Np + (size_t)row * Np + col0;
         if (col0 + EPI_COLS <= Np) {
 #pragma unroll
           for (int j = 0; j < EPI_COLS; j += 4)
-            *reinterpret_cast<float4*>(dst + j) =
-                make_float4(acc[j] * alpha, acc[j + 1] * alpha, acc[j + 2] * alpha, acc[j + 3] * alpha);
+            *reinterpret_cast<float4*>(dst + j) = make_float4(acc[j], acc[j + 1], acc[j + 2], acc[j + 3]);
         } else {
 #pragma unroll
           for (int j = 0; j < EPI_COLS; ++j)
-            if (col0 + j < Np) dst[j] = acc[j] * alpha;
+            if (col0 + j < Np) dst[j] = acc[j];
         }
       }
+    }
+    if (splits == 1 && max_out != nullptr) {
+      for (int o = 16; o > 0; o >>= 1) vmax = fmaxf(vmax, __shfl_xor_sync(0xffffffffu, vmax, o));
+      if (lane == 0 && vmax > 0.f) atomicMax(max_out, __float_as_uint(vmax));
     }
   }
 
@@ -350,10 +365,18 @@ void make_map(void* out, const __half* base, int64_t rows, int64_t kp, int box_r
   cuuint64_t strides[1] = {(cuuint64_t)kp * 2};
   cuuint32_t box[2] = {(cuuint32_t)BK, (cuuint32_t)box_rows};
   cuuint32_t estr[2] = {1, 1};
+  static const int promo_env = [] {
+    const char* e = getenv("TNB_L2_PROMO");
+    return e ? atoi(e) : -1;
+  }();
+  CUtensorMapL2promotion promo = CU_TENSOR_MAP_L2_PROMOTION_L2_256B;
+  if (promo_env == 0) promo = CU_TENSOR_MAP_L2_PROMOTION_NONE;
+  if (promo_env == 64) promo = CU_TENSOR_MAP_L2_PROMOTION_L2_64B;
+  if (promo_env == 128) promo = CU_TENSOR_MAP_L2_PROMOTION_L2_128B;
   CUresult r = get_encode()(reinterpret_cast<CUtensorMap*>(out), CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2,
                             const_cast<__half*>(base), dims, strides, box, estr,
-                            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B,
-                            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+                            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B, promo,
+                            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) throw Error(TNB_ERR_CUDA, "cuTensorMapEncodeTiled failed: " + std::to_string((int)r));
 }
 
@@ -381,7 +404,8 @@ int64_t tc_workspace_elems(int64_t M, int64_t Np, int64_t Kp, int num_sms) {
 
 void tc_plan_gemm(TcGemmPlan* p, const __half* Ahi, const __half* Alo, const __half* Bhi,
                   const __half* Blo, int64_t M, int64_t Np, int64_t Kp, float* C, float* workspace,
-                  int64_t workspace_elems, const unsigned int* maxbits, int num_sms) {
+                  int64_t workspace_elems, const unsigned int* max_rows,
+                  const unsigned int* max_cols, unsigned int* max_out, int num_sms) {
   if (M > (1ll << 31) - 1 || Np > (1ll << 31) - 1 || Kp > (1ll << 31) - 1)
     throw Error(TNB_ERR_SHAPE, "tensor-core GEMM dimension too large");
   p->M = M; p->Np = Np; p->Kp = Kp;
@@ -397,9 +421,14 @@ void tc_plan_gemm(TcGemmPlan* p, const __half* Ahi, const __half* Alo, const __h
   } else {
     p->C = C;
   }
-  p->maxbits = maxbits;
+  p->max_rows = max_rows;
+  p->max_cols = max_cols;
+  p->max_out = max_out;
   const char* env = getenv("TNB_CHUNK_KB");
   p->chunk_kb = env ? atoi(env) : kDefaultChunkKb;
+  const char* genv = getenv("TNB_GROUP_M");
+  p->group_m = genv ? atoi(genv) : GROUP_M;
+  if (p->group_m <= 0) p->group_m = 1 << 30;
   if (p->chunk_kb <= 0) p->chunk_kb = 1 << 30;  // no promotion: whole K in TMEM
   make_map(p->tmap[0], Ahi, M, Kp, BM);
   make_map(p->tmap[1], Alo, M, Kp, BM);
@@ -413,7 +442,7 @@ void tc_launch_gemm(const TcGemmPlan* p, cudaStream_t s) {
   const CUtensorMap* maps = reinterpret_cast<const CUtensorMap*>(p->tmap);
   gemm_f16x3_kernel<<<p->grid, NUM_THREADS, SMEM_BYTES, s>>>(
       maps[0], maps[1], maps[2], maps[3], p->C, (int)p->M, (int)p->Np, (int)p->Kp, p->splits,
-      (int)p->k_per_split, p->chunk_kb, p->maxbits);
+      (int)p->k_per_split, p->chunk_kb, p->group_m, p->max_rows, p->max_cols, p->max_out);
   check_launch("gemm_f16x3");
 }
 

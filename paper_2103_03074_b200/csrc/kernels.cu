@@ -10,6 +10,8 @@
 
 #include <cuda_fp16.h>
 
+#include <algorithm>
+
 namespace tnb {
 
 namespace {
@@ -26,6 +28,21 @@ template <> struct Scalar<double2> { using type = double; };
 
 template <typename T>
 __device__ __forceinline__ T cadd(T a, T b) { T r; r.x = a.x + b.x; r.y = a.y + b.y; return r; }
+
+// block-wide max of non-negative floats -> one atomicMax on the bit pattern
+__device__ __forceinline__ void block_max_atomic(float m, unsigned int* out) {
+  for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+  __shared__ float red[32];
+  __syncthreads();
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = m;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    m = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : 0.f;
+    for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+    if (threadIdx.x == 0 && m > 0.f) atomicMax(out, __float_as_uint(m));
+  }
+}
+
 
 // ---------------------------------------------------------------------------
 // K1: sliced-leaf preparation.  One block per sliced leaf; the selected
@@ -49,7 +66,7 @@ template <typename T>
 __global__ void __launch_bounds__(256)
 contract_simt_kernel(const T* __restrict__ A, const T* __restrict__ B, T* __restrict__ C,
                      int64_t M, int64_t N, int64_t K, const ByteLut* __restrict__ gla,
-                     const ByteLut* __restrict__ glb) {
+                     const ByteLut* __restrict__ glb, unsigned int* __restrict__ max_out) {
   using S = typename Scalar<T>::type;
   constexpr int BM = 32, BN = 32, BK = 16;
   __shared__ uint32_t la[4][256];
@@ -61,7 +78,8 @@ contract_simt_kernel(const T* __restrict__ A, const T* __restrict__ B, T* __rest
     la[i >> 8][i & 255] = gla->t[i >> 8][i & 255];
     lb[i >> 8][i & 255] = glb->t[i >> 8][i & 255];
   }
-  const int64_t m0 = (int64_t)blockIdx.y * BM, n0 = (int64_t)blockIdx.x * BN;
+  const int64_t nbn = (N + BN - 1) / BN;
+  const int64_t m0 = ((int64_t)blockIdx.x / nbn) * BM, n0 = ((int64_t)blockIdx.x % nbn) * BN;
   const int tx = tid & 15, ty = tid >> 4;
   S acc_re[2][2] = {{0, 0}, {0, 0}}, acc_im[2][2] = {{0, 0}, {0, 0}};
   __syncthreads();
@@ -97,6 +115,7 @@ contract_simt_kernel(const T* __restrict__ A, const T* __restrict__ B, T* __rest
     }
     __syncthreads();
   }
+  float vmax = 0.f;
 #pragma unroll
   for (int i = 0; i < 2; ++i)
 #pragma unroll
@@ -105,8 +124,10 @@ contract_simt_kernel(const T* __restrict__ A, const T* __restrict__ B, T* __rest
       if (m < M && n < N) {
         T v; v.x = acc_re[i][j]; v.y = acc_im[i][j];
         C[m * N + n] = v;
+        vmax = fmaxf(vmax, (float)fmax(fabs(v.x), fabs(v.y)));
       }
     }
+  if (max_out) block_max_atomic(vmax, max_out);
 }
 
 // ---------------------------------------------------------------------------
@@ -166,26 +187,14 @@ __device__ __forceinline__ float scale_from_bits(unsigned int bits) {
   return ldexpf(1.f, p);
 }
 
-__global__ void absmax2_kernel(const float2* __restrict__ A, int64_t nA,
-                               const float2* __restrict__ B, int64_t nB,
-                               unsigned int* __restrict__ maxbits) {
-  const float2* src = blockIdx.y == 0 ? A : B;
-  const int64_t n = blockIdx.y == 0 ? nA : nB;
+__global__ void absmax_kernel(const float2* __restrict__ A, int64_t n, unsigned int* __restrict__ maxbits) {
   float m = 0.f;
   for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n;
        j += (int64_t)gridDim.x * blockDim.x) {
-    const float2 v = src[j];
+    const float2 v = A[j];
     m = fmaxf(m, fmaxf(fabsf(v.x), fabsf(v.y)));
   }
-  for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
-  __shared__ float red[32];
-  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = m;
-  __syncthreads();
-  if (threadIdx.x < 32) {
-    m = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : 0.f;
-    for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
-    if (threadIdx.x == 0) atomicMax(&maxbits[blockIdx.y], __float_as_uint(m));
-  }
+  block_max_atomic(m, maxbits);
 }
 
 __device__ __forceinline__ void split2(float a, float b, __half2& hi, __half2& lo) {
@@ -194,58 +203,82 @@ __device__ __forceinline__ void split2(float a, float b, __half2& hi, __half2& l
   lo = __floats2half2_rn(a - h.x, b - h.y);
 }
 
-// rows operand: hi/lo[m][2k + c] (K-major, Kp = 2K)
-__global__ void split_rows_kernel(const float2* __restrict__ src, const ByteLut* __restrict__ glut,
-                                  int64_t M, int64_t K, const unsigned int* __restrict__ maxbits,
-                                  __half2* __restrict__ hi, __half2* __restrict__ lo) {
-  __shared__ uint32_t l[4][256];
-  for (int i = threadIdx.x; i < 1024; i += blockDim.x) l[i >> 8][i & 255] = glut->t[i >> 8][i & 255];
-  __syncthreads();
-  const float s = scale_from_bits(maxbits[0]);
-  const int64_t n = M * K;
-  for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n;
-       j += (int64_t)gridDim.x * blockDim.x) {
-    const float2 v = src[lut_map(l, (uint32_t)j)];
-    __half2 h, o;
-    split2(v.x * s, v.y * s, h, o);
-    hi[j] = h;  // element j = m*K + k -> half2 at [m][2k..2k+1]
-    lo[j] = o;
+// Tiled permute + fp16 split (+ 2x2 real expansion for the cols operand).
+// A tile is the set of canonical indices spanned by the low destination
+// bits and the canonical bits that land on the low source bits: it is read
+// in source order (coalesced 256-B runs) into shared memory and written in
+// destination order (coalesced runs).  rows: hi/lo[j] for j = r*K + k;
+// cols (expand): rows 2n / 2n+1 of the 2x2 real representation.
+template <bool kExpand>
+__global__ void __launch_bounds__(256)
+stage_kernel(const float2* __restrict__ src, StageTables tb, int64_t K, int logK,
+             const unsigned int* __restrict__ maxbits, __half2* __restrict__ hi,
+             __half2* __restrict__ lo) {
+  extern __shared__ float2 tile_smem[];
+  float2* tile = tile_smem;
+  // tile padded by one element per 32 (conflict-free transposed stores)
+  uint32_t* rd_t = reinterpret_cast<uint32_t*>(tile + (1 << tb.nU) + (1 << tb.nU) / 32);
+  uint32_t* rd_src = rd_t + (1 << tb.nU);
+  uint32_t* t_dst = rd_src + (1 << tb.nU);
+  __shared__ uint32_t ls[4][256];
+  __shared__ uint32_t ld[4][256];
+  const int tsize = 1 << tb.nU;
+  for (int i = threadIdx.x; i < tsize; i += blockDim.x) {
+    rd_t[i] = tb.rd_t[i];
+    rd_src[i] = tb.rd_src[i];
+    t_dst[i] = tb.t_dst[i];
   }
-}
-
-// cols operand, expanded to the real 2x2 representation:
-// row 2n: (br, -bi), row 2n+1: (bi, br) along k' = 2k, 2k+1.
-__global__ void split_cols_expand_kernel(const float2* __restrict__ src,
-                                         const ByteLut* __restrict__ glut, int64_t N, int64_t K,
-                                         const unsigned int* __restrict__ maxbits,
-                                         __half2* __restrict__ hi, __half2* __restrict__ lo) {
-  __shared__ uint32_t l[4][256];
-  for (int i = threadIdx.x; i < 1024; i += blockDim.x) l[i >> 8][i & 255] = glut->t[i >> 8][i & 255];
+  for (int i = threadIdx.x; i < 1024; i += blockDim.x) {
+    ls[i >> 8][i & 255] = tb.tile_src->t[i >> 8][i & 255];
+    ld[i >> 8][i & 255] = tb.tile_dst->t[i >> 8][i & 255];
+  }
+  const float s = scale_from_bits(*maxbits);
   __syncthreads();
-  const float s = scale_from_bits(maxbits[1]);
-  const int64_t n = N * K;
-  for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n;
-       j += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t nn = j / K, k = j - nn * K;
-    const float2 v = src[lut_map(l, (uint32_t)j)];
-    __half2 h0, o0, h1, o1;
-    split2(v.x * s, -v.y * s, h0, o0);
-    split2(v.y * s, v.x * s, h1, o1);
-    const int64_t r0 = (2 * nn) * K + k, r1 = (2 * nn + 1) * K + k;  // half2 units per row = K
-    hi[r0] = h0; lo[r0] = o0;
-    hi[r1] = h1; lo[r1] = o1;
+  for (int64_t T = blockIdx.x; T < tb.n_tiles; T += gridDim.x) {
+    const uint32_t sbase = lut_map(ls, (uint32_t)T);
+    const uint32_t dbase = lut_map(ld, (uint32_t)T);
+    for (int i = threadIdx.x; i < tsize; i += blockDim.x) {
+      const uint32_t t = rd_t[i];
+      tile[t + (t >> 5)] = src[sbase + rd_src[i]];
+    }
+    __syncthreads();
+    for (int t = threadIdx.x; t < tsize; t += blockDim.x) {
+      const float2 v = tile[t + (t >> 5)];
+      const uint32_t j = dbase + t_dst[t];
+      if (!kExpand) {
+        __half2 h, o;
+        split2(v.x * s, v.y * s, h, o);
+        hi[j] = h;
+        lo[j] = o;
+      } else {
+        const uint64_t n = j >> logK;
+        const uint64_t r0 = (uint64_t)j + n * (uint64_t)K, r1 = r0 + (uint64_t)K;
+        __half2 h0, o0, h1, o1;
+        split2(v.x * s, -v.y * s, h0, o0);
+        split2(v.y * s, v.x * s, h1, o1);
+        hi[r0] = h0; lo[r0] = o0;
+        hi[r1] = h1; lo[r1] = o1;
+      }
+    }
+    __syncthreads();
   }
 }
 
 __global__ void splitk_reduce_kernel(const float* __restrict__ ws, int splits, int64_t elems,
-                                     float* __restrict__ C, const unsigned int* __restrict__ maxbits) {
-  const float alpha = 1.f / (scale_from_bits(maxbits[0]) * scale_from_bits(maxbits[1]));
+                                     float* __restrict__ C, const unsigned int* __restrict__ max_rows,
+                                     const unsigned int* __restrict__ max_cols,
+                                     unsigned int* __restrict__ max_out) {
+  const float alpha = 1.f / (scale_from_bits(*max_rows) * scale_from_bits(*max_cols));
+  float m = 0.f;
   for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < elems;
        j += (int64_t)gridDim.x * blockDim.x) {
     float acc = 0.f;
     for (int s = 0; s < splits; ++s) acc += ws[(int64_t)s * elems + j];
-    C[j] = acc * alpha;
+    acc *= alpha;
+    C[j] = acc;
+    m = fmaxf(m, fabsf(acc));
   }
+  if (max_out) block_max_atomic(m, max_out);
 }
 
 inline int grid_for(int64_t elems, int threads) {
@@ -281,10 +314,11 @@ void launch_prepare_leaves(const T* leaf_pool, T* slice_pool, const SlicedLeafDe
 
 template <typename T>
 void launch_contract_simt(const T* A, const T* B, T* C, int64_t M, int64_t N, int64_t K,
-                          const ByteLut* lutA, const ByteLut* lutB, cudaStream_t s) {
-  dim3 grid((unsigned)((N + 31) / 32), (unsigned)((M + 31) / 32));
-  if (grid.y > 65535) throw Error(TNB_ERR_SHAPE, "SIMT contraction: M too large");
-  contract_simt_kernel<T><<<grid, 256, 0, s>>>(A, B, C, M, N, K, lutA, lutB);
+                          const ByteLut* lutA, const ByteLut* lutB, unsigned int* max_out,
+                          cudaStream_t s) {
+  const int64_t blocks = ((M + 31) / 32) * ((N + 31) / 32);
+  if (blocks > 0x7fffffffll) throw Error(TNB_ERR_SHAPE, "SIMT contraction too large");
+  contract_simt_kernel<T><<<(unsigned)blocks, 256, 0, s>>>(A, B, C, M, N, K, lutA, lutB, max_out);
   check_launch("contract_simt");
 }
 
@@ -313,33 +347,86 @@ void launch_copy(const T* a, T* out, int64_t elems, cudaStream_t s) {
   check_launch("copy");
 }
 
-void launch_absmax2(const float2* A, int64_t nA, const float2* B, int64_t nB,
-                    unsigned int* maxbits, cudaStream_t s) {
-  TNB_CUDA(cudaMemsetAsync(maxbits, 0, 2 * sizeof(unsigned int), s));
-  const int64_t n = nA > nB ? nA : nB;
-  dim3 grid(grid_for(n, 512), 2);
-  absmax2_kernel<<<grid, 512, 0, s>>>(A, nA, B, nB, maxbits);
-  check_launch("absmax2");
+void launch_absmax(const float2* A, int64_t n, unsigned int* maxbits, cudaStream_t s) {
+  TNB_CUDA(cudaMemsetAsync(maxbits, 0, sizeof(unsigned int), s));
+  absmax_kernel<<<grid_for(n, 512), 512, 0, s>>>(A, n, maxbits);
+  check_launch("absmax");
 }
 
-void launch_split_rows(const float2* src, const ByteLut* lut, int64_t M, int64_t K,
-                       const unsigned int* maxbits, __half* hi, __half* lo, cudaStream_t s) {
-  split_rows_kernel<<<grid_for(M * K, 256), 256, 0, s>>>(src, lut, M, K, maxbits,
-                                                          reinterpret_cast<__half2*>(hi),
-                                                          reinterpret_cast<__half2*>(lo));
-  check_launch("split_rows");
+void build_stage_tables(const std::vector<int>& canon_to_src, int64_t K, StageHost* out) {
+  const int r = (int)canon_to_src.size();
+  const int Ld = std::min(5, r), Ls = std::min(5, r);
+  std::vector<int> src_to_canon(r, -1);
+  for (int p = 0; p < r; ++p) src_to_canon[canon_to_src[p]] = p;
+  std::vector<char> inU(r, 0);
+  for (int p = 0; p < Ld; ++p) inU[p] = 1;
+  for (int q = 0; q < Ls; ++q) inU[src_to_canon[q]] = 1;
+  // grow the tile to >= 2^10 elements (or the whole tensor) with the next
+  // lowest canonical bits so every tile keeps 256 threads busy
+  {
+    int cnt = 0;
+    for (int p = 0; p < r; ++p) cnt += inU[p];
+    for (int p = 0; p < r && cnt < std::min(r, 10); ++p)
+      if (!inU[p]) { inU[p] = 1; ++cnt; }
+  }
+  std::vector<int> U, V;
+  for (int p = 0; p < r; ++p) (inU[p] ? U : V).push_back(p);
+  std::vector<int> upos(r, -1);
+  for (int u = 0; u < (int)U.size(); ++u) upos[U[u]] = u;
+  // read order: source bits 0..Ls-1 fastest, then the remaining tile bits
+  std::vector<int> read_map;
+  std::vector<char> used(U.size(), 0);
+  for (int q = 0; q < Ls; ++q) { read_map.push_back(upos[src_to_canon[q]]); used[upos[src_to_canon[q]]] = 1; }
+  for (int u = 0; u < (int)U.size(); ++u) if (!used[u]) read_map.push_back(u);
+  const int nU = (int)U.size();
+  out->nU = nU;
+  out->n_tiles = (int64_t)1 << (r - nU);
+  out->rd_t.assign((size_t)1 << nU, 0);
+  out->rd_src.assign((size_t)1 << nU, 0);
+  out->t_dst.assign((size_t)1 << nU, 0);
+  for (uint32_t i = 0; i < (1u << nU); ++i) {
+    uint32_t t = 0, so = 0;
+    for (int b = 0; b < nU; ++b)
+      if ((i >> b) & 1) { t |= 1u << read_map[b]; so |= 1u << canon_to_src[U[read_map[b]]]; }
+    out->rd_t[i] = t;
+    out->rd_src[i] = so;
+  }
+  for (uint32_t t = 0; t < (1u << nU); ++t) {
+    uint32_t d = 0;
+    for (int u = 0; u < nU; ++u) if ((t >> u) & 1) d |= 1u << U[u];
+    out->t_dst[t] = d;
+  }
+  std::vector<int> vs, vd;
+  for (int p : V) { vs.push_back(canon_to_src[p]); vd.push_back(p); }
+  build_lut(vs, &out->tile_src);
+  build_lut(vd, &out->tile_dst);
+  (void)K;
 }
 
-void launch_split_cols_expand(const float2* src, const ByteLut* lut, int64_t N, int64_t K,
-                              const unsigned int* maxbits, __half* hi, __half* lo, cudaStream_t s) {
-  split_cols_expand_kernel<<<grid_for(N * K, 256), 256, 0, s>>>(
-      src, lut, N, K, maxbits, reinterpret_cast<__half2*>(hi), reinterpret_cast<__half2*>(lo));
-  check_launch("split_cols_expand");
+void launch_stage(const float2* src, const StageTables& tb, int64_t K, bool expand,
+                  const unsigned int* maxbits, __half* hi, __half* lo, cudaStream_t s) {
+  int logK = 0;
+  while ((1ll << logK) < K) ++logK;
+  const size_t smem = ((size_t)1 << tb.nU) * (8 + 12) + (((size_t)1 << tb.nU) / 32) * 8;
+  int64_t g = tb.n_tiles;
+  const int64_t cap = (int64_t)kSms * 6;
+  if (g > cap) g = cap;
+  if (expand)
+    stage_kernel<true><<<(unsigned)g, 256, smem, s>>>(src, tb, K, logK, maxbits,
+                                                       reinterpret_cast<__half2*>(hi),
+                                                       reinterpret_cast<__half2*>(lo));
+  else
+    stage_kernel<false><<<(unsigned)g, 256, smem, s>>>(src, tb, K, logK, maxbits,
+                                                        reinterpret_cast<__half2*>(hi),
+                                                        reinterpret_cast<__half2*>(lo));
+  check_launch("stage");
 }
 
 void launch_splitk_reduce(const float* ws, int splits, int64_t elems, float* C,
-                          const unsigned int* maxbits, cudaStream_t s) {
-  splitk_reduce_kernel<<<grid_for(elems, 256), 256, 0, s>>>(ws, splits, elems, C, maxbits);
+                          const unsigned int* max_rows, const unsigned int* max_cols,
+                          unsigned int* max_out, cudaStream_t s) {
+  splitk_reduce_kernel<<<grid_for(elems, 256), 256, 0, s>>>(ws, splits, elems, C, max_rows, max_cols,
+                                                            max_out);
   check_launch("splitk_reduce");
 }
 
@@ -347,7 +434,8 @@ void launch_splitk_reduce(const float* ws, int splits, int64_t elems, float* C,
   template void launch_prepare_leaves<T>(const T*, T*, const SlicedLeafDesc*, int,         \
                                          const uint32_t*, uint64_t, cudaStream_t);         \
   template void launch_contract_simt<T>(const T*, const T*, T*, int64_t, int64_t, int64_t, \
-                                        const ByteLut*, const ByteLut*, cudaStream_t);     \
+                                        const ByteLut*, const ByteLut*, unsigned int*,     \
+                                        cudaStream_t);                                     \
   template void launch_permute<T>(const T*, T*, int64_t, const ByteLut*, cudaStream_t);    \
   template void launch_counter_merge<T>(const T*, const T*, int64_t, int, T*, int64_t, cudaStream_t); \
   template void launch_add<T>(const T*, const T*, T*, int64_t, cudaStream_t);              \

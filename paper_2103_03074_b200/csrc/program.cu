@@ -19,6 +19,7 @@
 #include "tnb_internal.h"
 
 #include <algorithm>
+#include <cmath>
 #include <cstring>
 #include <map>
 #include <memory>
@@ -101,7 +102,9 @@ struct StepRec {
   bool hoisted = false;
   int64_t M = 1, N = 1, K = 1;   // SIMT: rows of a, cols of b, shared. TC: rows/cols operand.
   int rows_t = -1, cols_t = -1;  // TC operand tensors (rows unexpanded, cols expanded)
-  int lut_a = -1, lut_b = -1;    // indices into the LUT table
+  int lut_a = -1, lut_b = -1;    // SIMT: indices into the LUT table
+  std::vector<int> canon_rows, canon_cols;  // TC: canonical bit -> source bit
+  int st_rows = -1, st_cols = -1;           // TC: indices into Program::stages
   double mults = 0;
   TcGemmPlan tc;
 };
@@ -137,7 +140,12 @@ struct Program {
   ByteLut* d_luts = nullptr;
   SlicedLeafDesc* d_sl_descs = nullptr; int n_sl_descs = 0;
   uint32_t* d_keep = nullptr;
-  unsigned int* d_maxbits = nullptr;
+  unsigned int* d_tmax = nullptr;   // per-tensor max|re|,|im| slots (fp32 bits)
+  std::vector<int> slot;            // tensor -> slot
+  int inv_slot_begin = 0, inv_slot_count = 0, var_slot_begin = 0, var_slot_count = 0;
+  std::vector<StageTables> stages;  // device views of the TC staging tables
+  uint32_t* d_stage_u32 = nullptr;
+  ByteLut* d_stage_luts = nullptr;
   void* d_acc = nullptr;          // (n_sliced + 2) accumulator slots of out_elems
   int n_acc_slots = 0;
   bool invariant_valid = false;
@@ -154,7 +162,7 @@ struct Program {
   ~Program() {
     if (device >= 0) cudaSetDevice(device);
     void* ptrs[] = {d_leaf_pool, d_slice_pool, d_persist, d_arena, d_scratch, d_luts,
-                    d_sl_descs, d_keep, d_maxbits, d_acc};
+                    d_sl_descs, d_keep, d_tmax, d_acc, d_stage_u32, d_stage_luts};
     for (void* p : ptrs)
       if (p) cudaFree(p);
     for (auto e : ev_pool) cudaEventDestroy(e);
@@ -204,6 +212,8 @@ template <typename T>
 void run_range_t(Program* P, uint64_t a, uint64_t b, int mode, void* out, bool out_dev);
 
 }  // namespace
+
+void upload_leaf_max(Program* P, int leaf_pos, const double* data);
 
 // ---------------------------------------------------------------------------
 Program* program_create(const tnb_program_desc* d) {
@@ -332,14 +342,14 @@ Program* program_create(const tnb_program_desc* d) {
         s.rows_t = s.a; s.cols_t = s.b;
         o.axes = afree; o.axes.insert(o.axes.end(), bfree.begin(), bfree.end());
         s.M = (int64_t)1 << na; s.N = (int64_t)1 << nb;
-        s.lut_a = add_lut(P.get(), canon_bits(A.axes, afree, shared));
-        s.lut_b = add_lut(P.get(), canon_bits(B.axes, bfree, shared));
+        s.canon_rows = canon_bits(A.axes, afree, shared);
+        s.canon_cols = canon_bits(B.axes, bfree, shared);
       } else {
         s.rows_t = s.b; s.cols_t = s.a;
         o.axes = bfree; o.axes.insert(o.axes.end(), afree.begin(), afree.end());
         s.M = (int64_t)1 << nb; s.N = (int64_t)1 << na;
-        s.lut_a = add_lut(P.get(), canon_bits(B.axes, bfree, shared));
-        s.lut_b = add_lut(P.get(), canon_bits(A.axes, afree, shared));
+        s.canon_rows = canon_bits(B.axes, bfree, shared);
+        s.canon_cols = canon_bits(A.axes, afree, shared);
       }
     } else {
       s.kind = KIND_SIMT;
@@ -436,7 +446,63 @@ Program* program_create(const tnb_program_desc* d) {
   dmalloc((void**)&P->d_keep, (int64_t)keep.size() * 4);
   if (!keep.empty())
     TNB_CUDA(cudaMemcpy(P->d_keep, keep.data(), keep.size() * 4, cudaMemcpyHostToDevice));
-  dmalloc((void**)&P->d_maxbits, 64);
+  // per-tensor max slots: leaves | invariant step results | variant step results
+  {
+    const int nt = (int)P->tensors.size();
+    P->slot.assign(nt, -1);
+    int next = 0;
+    for (int t = 0; t < nt; ++t) if (P->tensors[t].def_step < 0) P->slot[t] = next++;
+    P->inv_slot_begin = next;
+    for (int t = 0; t < nt; ++t)
+      if (P->tensors[t].def_step >= 0 && P->tensors[t].pool == POOL_PERSIST) P->slot[t] = next++;
+    P->inv_slot_count = next - P->inv_slot_begin;
+    P->var_slot_begin = next;
+    for (int t = 0; t < nt; ++t) if (P->slot[t] < 0) P->slot[t] = next++;
+    P->var_slot_count = next - P->var_slot_begin;
+    dmalloc((void**)&P->d_tmax, (int64_t)next * 4);
+    TNB_CUDA(cudaMemset(P->d_tmax, 0, (size_t)next * 4));
+  }
+  // tensor-core staging tables (tiled permute + split), one per TC operand
+  {
+    std::vector<StageHost> hosts;
+    for (auto& s : P->steps) {
+      if (s.kind != KIND_TC) continue;
+      hosts.emplace_back();
+      build_stage_tables(s.canon_rows, s.K, &hosts.back());
+      s.st_rows = (int)hosts.size() - 1;
+      hosts.emplace_back();
+      build_stage_tables(s.canon_cols, s.K, &hosts.back());
+      s.st_cols = (int)hosts.size() - 1;
+    }
+    size_t n32 = 0;
+    for (auto& h : hosts) n32 += 3 * h.rd_t.size();
+    dmalloc((void**)&P->d_stage_u32, (int64_t)n32 * 4);
+    dmalloc((void**)&P->d_stage_luts, (int64_t)hosts.size() * 2 * sizeof(ByteLut));
+    std::vector<uint32_t> u32;
+    u32.reserve(n32);
+    std::vector<ByteLut> luts;
+    for (size_t i = 0; i < hosts.size(); ++i) {
+      const StageHost& h = hosts[i];
+      StageTables tb;
+      tb.nU = h.nU;
+      tb.n_tiles = h.n_tiles;
+      tb.rd_t = P->d_stage_u32 + u32.size();
+      u32.insert(u32.end(), h.rd_t.begin(), h.rd_t.end());
+      tb.rd_src = P->d_stage_u32 + u32.size();
+      u32.insert(u32.end(), h.rd_src.begin(), h.rd_src.end());
+      tb.t_dst = P->d_stage_u32 + u32.size();
+      u32.insert(u32.end(), h.t_dst.begin(), h.t_dst.end());
+      tb.tile_src = P->d_stage_luts + luts.size();
+      luts.push_back(h.tile_src);
+      tb.tile_dst = P->d_stage_luts + luts.size();
+      luts.push_back(h.tile_dst);
+      P->stages.push_back(tb);
+    }
+    if (!u32.empty())
+      TNB_CUDA(cudaMemcpy(P->d_stage_u32, u32.data(), u32.size() * 4, cudaMemcpyHostToDevice));
+    if (!luts.empty())
+      TNB_CUDA(cudaMemcpy(P->d_stage_luts, luts.data(), luts.size() * sizeof(ByteLut), cudaMemcpyHostToDevice));
+  }
   P->n_acc_slots = P->n_sliced + 3;  // counter levels + total + permuted output
   dmalloc(&P->d_acc, (int64_t)P->n_acc_slots * align_up(P->out_elems, 128) * (int64_t)P->esize);
 
@@ -452,7 +518,8 @@ Program* program_create(const tnb_program_desc* d) {
     float* ws = (float*)(base + align_up(2 * s.M * Kp * 2 + 2 * Np * Kp * 2, kAlign));
     const int64_t ws_elems = tc_workspace_elems(s.M, Np, Kp, P->num_sms);
     tc_plan_gemm(&s.tc, ahi, alo, bhi, blo, s.M, Np, Kp, (float*)P->tensor_ptr(s.out), ws, ws_elems,
-                 P->d_maxbits, P->num_sms);
+                 P->d_tmax + P->slot[s.rows_t], P->d_tmax + P->slot[s.cols_t],
+                 P->d_tmax + P->slot[s.out], P->num_sms);
   }
 
   // ---- upload leaf values
@@ -465,11 +532,23 @@ Program* program_create(const tnb_program_desc* d) {
       std::memcpy(host.data(), d->leaf_data, host.size());
     }
     TNB_CUDA(cudaMemcpy(P->d_leaf_pool, host.data(), host.size(), cudaMemcpyHostToDevice));
+    for (int i = 0; i < d->n_leaves; ++i) upload_leaf_max(P.get(), i, d->leaf_data + 2 * P->leaf_pool_off[i]);
   }
   return P.release();
 }
 
 void program_destroy(Program* P) { delete P; }
+
+// max|re|,|im| of a leaf (its fp32 values): the fp16 scale bound of the leaf
+// and of every sliced sub-tensor prepared from it.
+void upload_leaf_max(Program* P, int leaf_pos, const double* data) {
+  const int64_t n = (int64_t)1 << P->leaf_ranks[leaf_pos];
+  float m = 0.f;
+  for (int64_t i = 0; i < 2 * n; ++i) m = std::max(m, std::fabs((float)data[i]));
+  unsigned int bits;
+  std::memcpy(&bits, &m, 4);
+  TNB_CUDA(cudaMemcpy(P->d_tmax + P->slot[leaf_pos], &bits, 4, cudaMemcpyHostToDevice));
+}
 
 void program_info(const Program* P, tnb_program_info* info) {
   info->out_elems = P->out_elems;
@@ -503,6 +582,7 @@ void program_set_leaf(Program* P, int leaf_pos, const double* data) {
     TNB_CUDA(cudaMemcpyAsync(dst, data, (size_t)n * 16, cudaMemcpyHostToDevice, P->stream));
     TNB_CUDA(cudaStreamSynchronize(P->stream));
   }
+  upload_leaf_max(P, leaf_pos, data);
   P->invariant_valid = false;
 }
 
@@ -512,6 +592,8 @@ void program_set_leaf_device(Program* P, int leaf_pos, const void* dev) {
   const int64_t n = (int64_t)1 << P->leaf_ranks[leaf_pos];
   char* dst = (char*)P->d_leaf_pool + (size_t)P->leaf_pool_off[leaf_pos] * P->esize;
   TNB_CUDA(cudaMemcpyAsync(dst, dev, (size_t)n * P->esize, cudaMemcpyDeviceToDevice, P->stream));
+  if (P->precision == TNB_SINGLE)
+    launch_absmax((const float2*)dst, n, P->d_tmax + P->slot[leaf_pos], P->stream);
   TNB_CUDA(cudaStreamSynchronize(P->stream));
   P->invariant_valid = false;
 }
@@ -556,7 +638,9 @@ void exec_step(Program* P, StepRec& s) {
     cudaEvent_t e = C.mark();
     launch_contract_simt<T>((const T*)P->tensor_ptr(s.a), (const T*)P->tensor_ptr(s.b),
                             (T*)P->tensor_ptr(s.out), s.M, s.N, s.K, P->d_luts + s.lut_a,
-                            P->d_luts + s.lut_b, P->stream);
+                            P->d_luts + s.lut_b,
+                            P->precision == TNB_SINGLE ? P->d_tmax + P->slot[s.out] : nullptr,
+                            P->stream);
     C.close(2, e);
     C.launches++;
     return;
@@ -571,19 +655,19 @@ void exec_step(Program* P, StepRec& s) {
     __half* bhi = alo + s.M * Kp;
     __half* blo = bhi + Np * Kp;
     cudaEvent_t e = C.mark();
-    launch_absmax2(rows, s.M * s.K, cols, s.N * s.K, P->d_maxbits, P->stream);
-    launch_split_rows(rows, P->d_luts + s.lut_a, s.M, s.K, P->d_maxbits, ahi, alo, P->stream);
-    launch_split_cols_expand(cols, P->d_luts + s.lut_b, s.N, s.K, P->d_maxbits, bhi, blo, P->stream);
+    launch_stage(rows, P->stages[s.st_rows], s.K, false, P->d_tmax + P->slot[s.rows_t], ahi, alo, P->stream);
+    launch_stage(cols, P->stages[s.st_cols], s.K, true, P->d_tmax + P->slot[s.cols_t], bhi, blo, P->stream);
     C.close(1, e);
     e = C.mark();
     tc_launch_gemm(&s.tc, P->stream);
     C.close(0, e);
-    C.launches += 4;
+    C.launches += 3;
     C.gemm_launches++;
     C.gemm_flops += 8.0 * s.mults;
     if (s.tc.splits > 1) {
       e = C.mark();
-      launch_splitk_reduce(s.tc.C, s.tc.splits, s.M * Np, (float*)P->tensor_ptr(s.out), P->d_maxbits,
+      launch_splitk_reduce(s.tc.C, s.tc.splits, s.M * Np, (float*)P->tensor_ptr(s.out),
+                           s.tc.max_rows, s.tc.max_cols, s.tc.max_out,
                            P->stream);
       C.close(1, e);
       C.launches++;
@@ -610,6 +694,8 @@ void run_range_t(Program* P, uint64_t a, uint64_t b, int mode, void* out, bool o
 
   // hoisted slice-invariant steps (once per leaf-data version)
   if (!P->invariant_valid) {
+    if (P->inv_slot_count)
+      TNB_CUDA(cudaMemsetAsync(P->d_tmax + P->inv_slot_begin, 0, (size_t)P->inv_slot_count * 4, st));
     for (auto& s : P->steps)
       if (s.hoisted) exec_step<T>(P, s);
     P->invariant_valid = true;
@@ -625,6 +711,8 @@ void run_range_t(Program* P, uint64_t a, uint64_t b, int mode, void* out, bool o
                              P->n_sl_descs, P->d_keep, mask, st);
     if (P->n_sl_descs) ctx.launches++;
     ctx.close(3, e);
+    if (P->var_slot_count)
+      TNB_CUDA(cudaMemsetAsync(P->d_tmax + P->var_slot_begin, 0, (size_t)P->var_slot_count * 4, st));
     for (auto& s : P->steps)
       if (!s.hoisted) exec_step<T>(P, s);
     e = ctx.mark();

@@ -155,35 +155,62 @@ int tnb_cgemm(int32_t device, int64_t M, int64_t N, int64_t K, const void* A, co
     for (int p = 0; p < bk + bm; ++p) la.push_back(p);
     for (int p = 0; p < bk; ++p) lb.push_back(bn + p);   // k bits sit above n bits in B
     for (int p = 0; p < bn; ++p) lb.push_back(p);
-    ByteLut hl[2];
-    build_lut(la, &hl[0]);
-    build_lut(lb, &hl[1]);
-    DevBuf dl(sizeof(hl));
-    TNB_CUDA(cudaMemcpyAsync(dl.p, hl, sizeof(hl), cudaMemcpyHostToDevice, st));
-    const ByteLut* lut = (const ByteLut*)dl.p;
     const bool tc = use_tc && tc_available(device);
     if (use_tc && !tc) throw Error(TNB_ERR_NODEV, "tensor-core path needs an sm_100 device");
     if (!tc) {
+      ByteLut hl[2];
+      build_lut(la, &hl[0]);
+      build_lut(lb, &hl[1]);
+      DevBuf dl(sizeof(hl));
+      TNB_CUDA(cudaMemcpyAsync(dl.p, hl, sizeof(hl), cudaMemcpyHostToDevice, st));
+      const ByteLut* lut = (const ByteLut*)dl.p;
       launch_contract_simt<float2>((const float2*)pa, (const float2*)pb, (float2*)pc, M, N, K, lut,
-                                   lut + 1, st);
+                                   lut + 1, nullptr, st);
+      TNB_CUDA(cudaStreamSynchronize(st));
     } else {
       const int64_t Kp = 2 * K, Np = 2 * N;
       const int64_t ws = tc_workspace_elems(M, Np, Kp, sms);
       DevBuf scratch((size_t)(2 * M * Kp + 2 * Np * Kp) * 2 + 1024 + (size_t)ws * 4);
       DevBuf maxbits(64);
+      TNB_CUDA(cudaMemsetAsync(maxbits.p, 0, 64, st));
+      unsigned* mx = (unsigned*)maxbits.p;
       __half* ahi = (__half*)scratch.p;
       __half* alo = ahi + M * Kp;
       __half* bhi = alo + M * Kp;
       __half* blo = bhi + Np * Kp;
       float* wsp = (float*)((char*)scratch.p + (((size_t)(2 * M * Kp + 2 * Np * Kp) * 2 + 1023) / 1024) * 1024);
-      launch_absmax2((const float2*)pa, M * K, (const float2*)pb, N * K, (unsigned*)maxbits.p, st);
-      launch_split_rows((const float2*)pa, lut, M, K, (unsigned*)maxbits.p, ahi, alo, st);
-      launch_split_cols_expand((const float2*)pb, lut + 1, N, K, (unsigned*)maxbits.p, bhi, blo, st);
+      StageHost sh[2];
+      build_stage_tables(la, K, &sh[0]);
+      build_stage_tables(lb, K, &sh[1]);
+      std::vector<std::unique_ptr<DevBuf>> keep;
+      StageTables tb[2];
+      for (int i = 0; i < 2; ++i) {
+        const size_t n = sh[i].rd_t.size();
+        keep.emplace_back(new DevBuf(3 * n * 4 + 2 * sizeof(ByteLut)));
+        char* b = (char*)keep.back()->p;
+        TNB_CUDA(cudaMemcpyAsync(b, sh[i].rd_t.data(), n * 4, cudaMemcpyHostToDevice, st));
+        TNB_CUDA(cudaMemcpyAsync(b + n * 4, sh[i].rd_src.data(), n * 4, cudaMemcpyHostToDevice, st));
+        TNB_CUDA(cudaMemcpyAsync(b + 2 * n * 4, sh[i].t_dst.data(), n * 4, cudaMemcpyHostToDevice, st));
+        TNB_CUDA(cudaMemcpyAsync(b + 3 * n * 4, &sh[i].tile_src, sizeof(ByteLut), cudaMemcpyHostToDevice, st));
+        TNB_CUDA(cudaMemcpyAsync(b + 3 * n * 4 + sizeof(ByteLut), &sh[i].tile_dst, sizeof(ByteLut),
+                                 cudaMemcpyHostToDevice, st));
+        tb[i].rd_t = (const uint32_t*)b;
+        tb[i].rd_src = (const uint32_t*)(b + n * 4);
+        tb[i].t_dst = (const uint32_t*)(b + 2 * n * 4);
+        tb[i].tile_src = (const ByteLut*)(b + 3 * n * 4);
+        tb[i].tile_dst = (const ByteLut*)(b + 3 * n * 4 + sizeof(ByteLut));
+        tb[i].nU = sh[i].nU;
+        tb[i].n_tiles = sh[i].n_tiles;
+      }
+      launch_absmax((const float2*)pa, M * K, mx, st);
+      launch_absmax((const float2*)pb, N * K, mx + 1, st);
+      launch_stage((const float2*)pa, tb[0], K, false, mx, ahi, alo, st);
+      launch_stage((const float2*)pb, tb[1], K, true, mx + 1, bhi, blo, st);
       TcGemmPlan plan;
-      tc_plan_gemm(&plan, ahi, alo, bhi, blo, M, Np, Kp, (float*)pc, wsp, ws, (unsigned*)maxbits.p, sms);
+      tc_plan_gemm(&plan, ahi, alo, bhi, blo, M, Np, Kp, (float*)pc, wsp, ws, mx, mx + 1, mx + 2, sms);
       tc_launch_gemm(&plan, st);
       if (plan.splits > 1)
-        launch_splitk_reduce(plan.C, plan.splits, M * Np, (float*)pc, (unsigned*)maxbits.p, st);
+        launch_splitk_reduce(plan.C, plan.splits, M * Np, (float*)pc, mx, mx + 1, mx + 2, st);
       TNB_CUDA(cudaStreamSynchronize(st));
     }
     if (!on_device) TNB_CUDA(cudaMemcpyAsync(C, pc, ec, cudaMemcpyDeviceToHost, st));

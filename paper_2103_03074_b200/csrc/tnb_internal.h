@@ -69,7 +69,8 @@ void launch_prepare_leaves(const T* leaf_pool, T* slice_pool, const SlicedLeafDe
 
 template <typename T>
 void launch_contract_simt(const T* A, const T* B, T* C, int64_t M, int64_t N, int64_t K,
-                          const ByteLut* lutA, const ByteLut* lutB, cudaStream_t s);
+                          const ByteLut* lutA, const ByteLut* lutB, unsigned int* max_out,
+                          cudaStream_t s);
 
 template <typename T>
 void launch_permute(const T* in, T* out, int64_t elems, const ByteLut* lut, cudaStream_t s);
@@ -84,15 +85,34 @@ void launch_add(const T* a, const T* b, T* out, int64_t elems, cudaStream_t s);
 template <typename T>
 void launch_copy(const T* a, T* out, int64_t elems, cudaStream_t s);
 
-// Tensor-core operand staging (single precision only).
-void launch_absmax2(const float2* A, int64_t nA, const float2* B, int64_t nB,
-                    unsigned int* maxbits /*2*/, cudaStream_t s);
-void launch_split_rows(const float2* src, const ByteLut* lut, int64_t M, int64_t K,
-                       const unsigned int* maxbits, __half* hi, __half* lo, cudaStream_t s);
-void launch_split_cols_expand(const float2* src, const ByteLut* lut, int64_t N, int64_t K,
-                              const unsigned int* maxbits, __half* hi, __half* lo, cudaStream_t s);
+// Tensor-core operand staging (single precision only).  Every single-
+// precision tensor carries a device max|re|,|im| slot (fp32 bits) written by
+// its producer; the staging kernels derive the power-of-two fp16 scale from it.
+void launch_absmax(const float2* A, int64_t n, unsigned int* maxbits, cudaStream_t s);
+
+// Tiled permute tables for one operand (see stage_kernel in kernels.cu).
+struct StageHost {
+  int nU = 0;
+  int64_t n_tiles = 0;
+  std::vector<uint32_t> rd_t, rd_src, t_dst;
+  ByteLut tile_src, tile_dst;
+};
+struct StageTables {  // device view
+  const uint32_t* rd_t;
+  const uint32_t* rd_src;
+  const uint32_t* t_dst;
+  const ByteLut* tile_src;
+  const ByteLut* tile_dst;
+  int nU;
+  int64_t n_tiles;
+};
+// canon_to_src[p] = source bit of canonical (row*K + k) bit p
+void build_stage_tables(const std::vector<int>& canon_to_src, int64_t K, StageHost* out);
+void launch_stage(const float2* src, const StageTables& tb, int64_t K, bool expand,
+                  const unsigned int* maxbits, __half* hi, __half* lo, cudaStream_t s);
 void launch_splitk_reduce(const float* ws, int splits, int64_t elems, float* C,
-                          const unsigned int* maxbits, cudaStream_t s);
+                          const unsigned int* max_rows, const unsigned int* max_cols,
+                          unsigned int* max_out, cudaStream_t s);
 
 // ---------------------------------------------------------------------------
 // tcgen05 GEMM (gemm_tc.cu):  C[M][Np] (fp32) = alpha * sum over the three
@@ -101,18 +121,21 @@ struct TcGemmPlan {
   int64_t M = 0, Np = 0, Kp = 0;
   int splits = 1;
   int chunk_kb = 8;              // promotion chunk (K blocks); see gemm_tc.cu
+  int group_m = 16;              // raster band height (m-tiles)
   int64_t k_per_split = 0;       // multiple of the K block
   int grid = 0;
   alignas(64) unsigned char tmap[4][128];  // CUtensorMap x4: Ahi, Alo, Bhi, Blo
   float* C = nullptr;            // output (splits == 1) or workspace [splits][M][Np]
-  const unsigned int* maxbits = nullptr;  // device: absmax bits of A, B
+  const unsigned int* max_rows = nullptr;  // device: max bits of the rows operand
+  const unsigned int* max_cols = nullptr;  // device: max bits of the cols operand
+  unsigned int* max_out = nullptr;         // device: max bits of the result (atomicMax)
 };
 
 bool tc_available(int device);
 void tc_plan_gemm(TcGemmPlan* p, const __half* Ahi, const __half* Alo, const __half* Bhi,
                   const __half* Blo, int64_t M, int64_t Np, int64_t Kp, float* C,
-                  float* workspace, int64_t workspace_elems, const unsigned int* maxbits,
-                  int num_sms);
+                  float* workspace, int64_t workspace_elems, const unsigned int* max_rows,
+                  const unsigned int* max_cols, unsigned int* max_out, int num_sms);
 void tc_launch_gemm(const TcGemmPlan* p, cudaStream_t s);
 int64_t tc_workspace_elems(int64_t M, int64_t Np, int64_t Kp, int num_sms);
 

@@ -1,0 +1,138 @@
+"""Multi-GPU slice sharding (one process per GPU, torch.distributed/NCCL).
+
+Slices are independent: rank r of N owns the
+aligned contiguous slice range [a + r*w, a + (r+1)*w), w = (b-a)/N -- the
+same layout as the reference's thread fan-out (cli.py:367-371).  Each rank
+sums its range on its own device; the exchange is ONE collective:
+
+* ``sharded_amplitudes`` -- every rank contracts the (linear) tail with its
+  partial head vector and a single NCCL all-reduce(sum) combines the 2^n2
+  amplitude partials (BASELINE north_star);
+* ``sharded_head_vector(mode="fixed")`` -- all-gather of the partial head
+  vectors, then the aligned binary-tree combine of ``reduce_partials``
+  (engine.py:428-442) on the device: bit-identical to the single-GPU
+  fixed-mode result.  ``mode="free"`` uses an all-reduce instead.
+
+The partial computation and the add are injectable so the collective
+choreography is testable with ``gloo`` on CPU (tests/test_distributed.py);
+the defaults run libtnb on the rank's GPU.
+"""
+
+from __future__ import annotations
+
+import dataclasses
+
+import numpy as np
+
+from .errors import RangeOutOfBounds
+
+
+def aligned_ranges(a: int, b: int, parts: int) -> list:
+    """Split [a, b) into `parts` contiguous ranges; equal and aligned when
+    parts is a power of two dividing b - a (required for bit-exact fixed mode)."""
+    if parts <= 0:
+        raise ValueError("parts must be positive")
+    n = b - a
+    if n < parts:
+        raise RangeOutOfBounds(f"{n} slices cannot be split over {parts} ranks")
+    base, extra = divmod(n, parts)
+    out, lo = [], a
+    for r in range(parts):
+        hi = lo + base + (1 if r < extra else 0)
+        out.append((lo, hi))
+        lo = hi
+    return out
+
+
+def tree_combine(items, add):
+    """reduce_partials' aligned binary tree over equal-width ranges."""
+    if len(items) == 1:
+        return items[0]
+    if len(items) & (len(items) - 1):
+        acc = items[0]
+        for x in items[1:]:
+            acc = add(acc, x)
+        return acc
+    mid = len(items) // 2
+    return add(tree_combine(items[:mid], add), tree_combine(items[mid:], add))
+
+
+def _torch_add(x, y):
+    return x + y
+
+
+def _device_add(x, y):
+    import torch
+
+    from .device import add_tree_device
+
+    if not x.is_cuda:
+        return x + y
+    out = torch.empty_like(x)
+    add_tree_device([x, y], out, x.device.index)
+    return out
+
+
+def _rank_world(group):
+    import torch.distributed as dist
+
+    return dist.get_rank(group), dist.get_world_size(group)
+
+
+def sharded_head_vector(tn, tree, sliced_indices, s1, slice_range=None, precision="single",
+                        mode="fixed", group=None, partial_fn=None, add=None):
+    """Full head vector of [a, b) computed across the process group."""
+    import torch
+    import torch.distributed as dist
+
+    from . import engine
+
+    rank, world = _rank_world(group)
+    n_e = len(sliced_indices)
+    a, b = slice_range if slice_range is not None else (0, 1 << n_e)
+    lo, hi = aligned_ranges(a, b, world)[rank]
+    if partial_fn is None:
+        hv = engine.compute_head_vector(tn, tree, sliced_indices, s1, slice_range=(lo, hi),
+                                        precision=precision, mode=mode)
+        local = torch.from_numpy(hv.data).to(torch.device("cuda", torch.cuda.current_device()))
+        template = hv
+        add = add or _device_add
+    else:
+        local, template = partial_fn(lo, hi)
+        add = add or _torch_add
+    flat = torch.view_as_real(local).reshape(-1)
+    if mode == "fixed":
+        bufs = [torch.empty_like(flat) for _ in range(world)]
+        dist.all_gather(bufs, flat, group=group)
+        parts = [torch.view_as_complex(x.reshape(-1, 2)) for x in bufs]
+        total = tree_combine(parts, add)
+    else:
+        dist.all_reduce(flat, group=group)
+        total = torch.view_as_complex(flat.reshape(-1, 2))
+    data = total.cpu().numpy()
+    return dataclasses.replace(template, data=data, slice_range=(a, b))
+
+
+def sharded_amplitudes(tn, tree, sliced_indices, s1, slice_range=None, precision="single",
+                       mode="fixed", group=None, partial_fn=None):
+    """Amplitudes of the slice range with one all-reduce of the amplitude vector."""
+    import torch
+    import torch.distributed as dist
+
+    from . import engine
+
+    rank, world = _rank_world(group)
+    n_e = len(sliced_indices)
+    a, b = slice_range if slice_range is not None else (0, 1 << n_e)
+    lo, hi = aligned_ranges(a, b, world)[rank]
+    if partial_fn is None:
+        hv = engine.compute_head_vector(tn, tree, sliced_indices, s1, slice_range=(lo, hi),
+                                        precision=precision, mode=mode)
+        tab = engine.tail_amplitudes_unchecked(tn, tree, hv, precision=precision)
+        local = torch.from_numpy(tab.amplitudes).to(torch.device("cuda", torch.cuda.current_device()))
+    else:
+        local, tab = partial_fn(lo, hi)
+    flat = torch.view_as_real(local).reshape(-1)
+    dist.all_reduce(flat, group=group)
+    amps = torch.view_as_complex(flat.reshape(-1, 2)).cpu().numpy()
+    return dataclasses.replace(tab, amplitudes=amps.astype(np.asarray(tab.amplitudes).dtype))
