@@ -7,12 +7,13 @@
 // whose fp32 output rows are exactly the interleaved complex64 rows of C.
 // fp32 accuracy comes from a 2-term fp16 split with power-of-two scaling
 // (x s = hi + lo): C' = Ahi Blo + Alo Bhi + Ahi Bhi, three kind::f16 UMMAs
-// per K step into one fp32 TMEM accumulator.
+// per K step.
 //
-// Structure (one CTA per SM, persistent over output tiles):
-//   warp 0  : TMA producer (4 tiles per stage: Ahi, Alo, Bhi, Blo), mbarrier ring
-//   warp 1  : single-thread tcgen05.mma issuer, commits to the ring / TMEM barriers
-//   warp 2  : TMEM allocator (512 columns = 2 partial accumulators of 128 x 256 fp32)
+// Structure (persistent, one CTA per SM; CG = 2 pairs two SMs on a 256-row
+// tile with cta_group::2, each CTA staging its 128 rows of A and half of B):
+//   warp 0    : TMA producer (4 tiles per stage: Ahi, Alo, Bhi, Blo), mbarrier ring
+//   warp 1    : single-thread tcgen05.mma issuer (leader CTA only)
+//   warp 2    : TMEM allocator (512 columns = 2 partial accumulators of 128 x 256 fp32)
 //   warps 4-19: promotion + epilogue (TMEM partials -> fp32 registers -> global)
 #include "tnb_internal.h"
 
@@ -23,27 +24,43 @@
 namespace tnb {
 namespace {
 
-constexpr int BM = 128;
-constexpr int BN = 256;
+constexpr int BM = 128;                      // rows per CTA
+constexpr int BN = 256;                      // accumulator columns (fp32) per tile
 constexpr int BK = 32;                       // fp16 elements per stage row (64 B, SWIZZLE_64B)
-constexpr int STAGES = 4;
 constexpr int A_TILE = BM * BK * 2;          // 8 KB
-constexpr int B_TILE = BN * BK * 2;          // 16 KB
-constexpr int STAGE_BYTES = 2 * A_TILE + 2 * B_TILE;
 constexpr int EPI_SPLIT = 4;                 // column groups per TMEM lane quadrant
 constexpr int EPI_THREADS = 128 * EPI_SPLIT; // 16 epilogue warps: 4 lane quadrants x 4 column groups
 constexpr int EPI_COLS = BN / EPI_SPLIT;     // fp32 register accumulator columns per epilogue thread
 constexpr int NUM_THREADS = 128 + EPI_THREADS;
 constexpr int TMEM_COLS = 512;
-constexpr int kDefaultChunkKb = 8;          // K blocks (of 32 fp16) per promotion chunk
+constexpr int kDefaultChunkKb = 8;           // K blocks (of 32 fp16) per promotion chunk
 constexpr int GROUP_M = 16;                  // rasterisation band height (m-tiles)
-constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
 
-// instruction descriptor: F32 accum, F16 x F16, K-major both, M=128, N=256
-constexpr uint32_t IDESC = (1u << 4) | ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
+template <int CG>
+struct Cfg {
+  static constexpr int B_ROWS = BN / CG;                 // B rows staged by each CTA
+  static constexpr int B_TILE = B_ROWS * BK * 2;
+  static constexpr int STAGE_BYTES = 2 * A_TILE + 2 * B_TILE;
+  static constexpr int STAGES = CG == 1 ? 4 : 6;
+  static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
+  // instruction descriptor: F32 accum, F16 x F16, K-major both, M = 128*CG, N = 256
+  static constexpr uint32_t IDESC =
+      (1u << 4) | ((uint32_t)(BN >> 3) << 17) | ((uint32_t)((BM * CG) >> 4) << 24);
+};
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
+  asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
 
 __device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
@@ -74,13 +91,34 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
 
+// arrive on the same-offset barrier of CTA `rank` in the cluster
+__device__ __forceinline__ void mbar_arrive_remote(uint64_t* bar, uint32_t rank) {
+  asm volatile(
+      "{\n\t.reg .b32 ra;\n\t"
+      "mapa.shared::cluster.u32 ra, %0, %1;\n\t"
+      "mbarrier.arrive.shared::cluster.b64 _, [ra];\n\t}" ::"r"(smem_u32(bar)),
+      "r"(rank)
+      : "memory");
+}
+
+template <int CG>
 __device__ __forceinline__ void tma_load_2d(void* smem_dst, const CUtensorMap* map, uint64_t* bar,
                                             int c0, int c1) {
-  asm volatile(
-      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes"
-      " [%0], [%1, {%3, %4}], [%2];" ::"r"(smem_u32(smem_dst)),
-      "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1)
-      : "memory");
+  if constexpr (CG == 1) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%3, %4}], [%2];" ::"r"(smem_u32(smem_dst)),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1)
+        : "memory");
+  } else {
+    // bytes land in this CTA's smem; completion is signalled on the LEADER's
+    // barrier (peer bit of the shared::cluster address cleared)
+    asm volatile(
+        "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%3, %4}], [%2];" ::"r"(smem_u32(smem_dst)),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar) & 0xFEFFFFFFu), "r"(c0), "r"(c1)
+        : "memory");
+  }
 }
 
 __device__ __forceinline__ uint64_t make_desc_sw64(const void* smem_ptr) {
@@ -94,18 +132,37 @@ __device__ __forceinline__ uint64_t make_desc_sw64(const void* smem_ptr) {
   return d;
 }
 
+template <int CG>
 __device__ __forceinline__ void umma_f16(uint32_t tmem_c, uint64_t da, uint64_t db, uint32_t acc) {
-  asm volatile(
-      "{\n\t.reg .pred p;\n\t"
-      "setp.ne.b32 p, %4, 0;\n\t"
-      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_c),
-      "l"(da), "l"(db), "r"(IDESC), "r"(acc));
+  if constexpr (CG == 1) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_c),
+        "l"(da), "l"(db), "r"(Cfg<1>::IDESC), "r"(acc));
+  } else {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_c),
+        "l"(da), "l"(db), "r"(Cfg<2>::IDESC), "r"(acc));
+  }
 }
 
+// MMA completion -> barrier(s): CG=1 own CTA; CG=2 the same barrier in both CTAs
+template <int CG>
 __device__ __forceinline__ void umma_commit(uint64_t* bar) {
-  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
-                   smem_u32(bar))
-               : "memory");
+  if constexpr (CG == 1) {
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                     smem_u32(bar))
+                 : "memory");
+  } else {
+    asm volatile(
+        "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+            smem_u32(bar)),
+        "h"((uint16_t)0x3)
+        : "memory");
+  }
 }
 
 __device__ __forceinline__ void tc_fence_after() {
@@ -140,10 +197,10 @@ struct WorkCoord {
   int split, mb, nb;
 };
 
-// Grouped raster: bands of GROUP_M m-tiles, m fastest inside a band, then n.
-// The ~148 tiles in flight then cover ~16 m-tiles x ~9 n-tiles, so each A
-// panel (128 rows x K) and B panel (256 rows x K) streamed from HBM is shared
-// by ~9 / ~16 concurrently running CTAs through L2.
+// Grouped raster: bands of group_m m-tiles, m fastest inside a band, then n.
+// The tiles in flight then cover ~16 m-tiles x ~9 n-tiles, so each A panel
+// (rows x K) and B panel streamed from HBM is shared through L2 by the
+// concurrently running CTAs.
 __device__ __forceinline__ WorkCoord decode(int w, int nm, int nn, int group_m) {
   const int per_split = nm * nn;
   WorkCoord c;
@@ -163,15 +220,18 @@ __device__ __forceinline__ WorkCoord decode(int w, int nm, int nn, int group_m) 
 // partial accumulators; the epilogue warps promote every finished partial
 // into an IEEE fp32 register accumulator (DeepGEMM-style promotion), while
 // the MMA warp fills the other partial.
+template <int CG>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
 gemm_f16x3_kernel(const __grid_constant__ CUtensorMap tm_ahi, const __grid_constant__ CUtensorMap tm_alo,
                   const __grid_constant__ CUtensorMap tm_bhi, const __grid_constant__ CUtensorMap tm_blo,
                   float* __restrict__ C, int M, int Np, int Kp, int splits, int k_per_split,
                   int chunk_kb, int group_m, const unsigned int* __restrict__ max_rows,
                   const unsigned int* __restrict__ max_cols, unsigned int* __restrict__ max_out) {
+  using CF = Cfg<CG>;
+  constexpr int STAGES = CF::STAGES;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES);
+  uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + STAGES * CF::STAGE_BYTES);
   uint64_t* empty_bar = full_bar + STAGES;
   uint64_t* pfull_bar = empty_bar + STAGES;
   uint64_t* pempty_bar = pfull_bar + 2;
@@ -179,7 +239,11 @@ gemm_f16x3_kernel(const __grid_constant__ CUtensorMap tm_ahi, const __grid_const
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
-  const int nm = (M + BM - 1) / BM;
+  const uint32_t rank = CG == 1 ? 0u : cluster_rank();
+  const bool leader = rank == 0;
+  const int unit = blockIdx.x / CG;       // tile-processing unit (CTA or CTA pair)
+  const int n_units = gridDim.x / CG;
+  const int nm = (M + BM * CG - 1) / (BM * CG);
   const int nn = (Np + BN - 1) / BN;
   const int total = nm * nn * splits;
 
@@ -191,86 +255,97 @@ gemm_f16x3_kernel(const __grid_constant__ CUtensorMap tm_ahi, const __grid_const
   }
   if (warp == 1 && lane == 0) {
     for (int i = 0; i < STAGES; ++i) {
-      mbar_init(&full_bar[i], 1);
-      mbar_init(&empty_bar[i], 1);
+      mbar_init(&full_bar[i], CG);          // leader: own arrive(+tx) and the peer's arrive
+      mbar_init(&empty_bar[i], 1);          // MMA commit (multicast to both CTAs)
     }
     for (int i = 0; i < 2; ++i) {
-      mbar_init(&pfull_bar[i], 1);
-      mbar_init(&pempty_bar[i], EPI_THREADS);
+      mbar_init(&pfull_bar[i], 1);          // MMA commit (multicast)
+      mbar_init(&pempty_bar[i], CG * EPI_THREADS);  // leader: epilogue threads of both CTAs
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 2) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
-                     smem_u32(tmem_slot)),
-                 "r"(TMEM_COLS));
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    if constexpr (CG == 1) {
+      asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                       smem_u32(tmem_slot)),
+                   "r"(TMEM_COLS));
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    } else {
+      asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                       smem_u32(tmem_slot)),
+                   "r"(TMEM_COLS));
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+    }
   }
   tc_fence_before();
-  __syncthreads();
+  if constexpr (CG == 1) __syncthreads(); else cluster_sync_all();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
 
   if (warp == 0) {
     if (lane == 0) {
-      // ===== TMA producer =====
+      // ===== TMA producer (both CTAs) =====
       int stage = 0;
       uint32_t phase = 0;
-      for (int w = blockIdx.x; w < total; w += gridDim.x) {
+      for (int w = unit; w < total; w += n_units) {
         const WorkCoord wc = decode(w, nm, nn, group_m);
         const int k_begin = wc.split * k_per_split;
         const int k_end = min(Kp, k_begin + k_per_split);
-        const int m0 = wc.mb * BM, n0 = wc.nb * BN;
+        const int m0 = wc.mb * BM * CG + (int)rank * BM;
+        const int n0 = wc.nb * BN + (int)rank * CF::B_ROWS;
         for (int k = k_begin; k < k_end; k += BK) {
           mbar_wait(&empty_bar[stage], phase ^ 1);
-          uint8_t* st = smem + stage * STAGE_BYTES;
-          mbar_arrive_expect_tx(&full_bar[stage], STAGE_BYTES);
-          tma_load_2d(st, &tm_ahi, &full_bar[stage], k, m0);
-          tma_load_2d(st + A_TILE, &tm_alo, &full_bar[stage], k, m0);
-          tma_load_2d(st + 2 * A_TILE, &tm_bhi, &full_bar[stage], k, n0);
-          tma_load_2d(st + 2 * A_TILE + B_TILE, &tm_blo, &full_bar[stage], k, n0);
+          uint8_t* st = smem + stage * CF::STAGE_BYTES;
+          if (leader) mbar_arrive_expect_tx(&full_bar[stage], CG * CF::STAGE_BYTES);
+          else mbar_arrive_remote(&full_bar[stage], 0);
+          tma_load_2d<CG>(st, &tm_ahi, &full_bar[stage], k, m0);
+          tma_load_2d<CG>(st + A_TILE, &tm_alo, &full_bar[stage], k, m0);
+          tma_load_2d<CG>(st + 2 * A_TILE, &tm_bhi, &full_bar[stage], k, n0);
+          tma_load_2d<CG>(st + 2 * A_TILE + CF::B_TILE, &tm_blo, &full_bar[stage], k, n0);
           if (++stage == STAGES) { stage = 0; phase ^= 1; }
         }
       }
     }
   } else if (warp == 1) {
-    // ===== MMA issuer =====
-    int stage = 0;
-    uint32_t phase = 0;
-    int gchunk = 0;
-    for (int w = blockIdx.x; w < total; w += gridDim.x) {
-      const WorkCoord wc = decode(w, nm, nn, group_m);
-      const int k_begin = wc.split * k_per_split;
-      const int nkb = (min(Kp, k_begin + k_per_split) - k_begin + BK - 1) / BK;
-      for (int c0 = 0; c0 < nkb; c0 += chunk_kb, ++gchunk) {
-        const int buf = gchunk & 1;
-        mbar_wait(&pempty_bar[buf], ((gchunk >> 1) & 1) ^ 1);
-        tc_fence_after();
-        const uint32_t tmem_c = tmem_base + buf * BN;
-        const int c1 = min(nkb, c0 + chunk_kb);
-        for (int kb = c0; kb < c1; ++kb) {
-          mbar_wait(&full_bar[stage], phase);
+    if (leader) {
+      // ===== MMA issuer (leader CTA) =====
+      int stage = 0;
+      uint32_t phase = 0;
+      int gchunk = 0;
+      for (int w = unit; w < total; w += n_units) {
+        const WorkCoord wc = decode(w, nm, nn, group_m);
+        const int k_begin = wc.split * k_per_split;
+        const int nkb = (min(Kp, k_begin + k_per_split) - k_begin + BK - 1) / BK;
+        for (int c0 = 0; c0 < nkb; c0 += chunk_kb, ++gchunk) {
+          const int buf = gchunk & 1;
+          mbar_wait(&pempty_bar[buf], ((gchunk >> 1) & 1) ^ 1);
           tc_fence_after();
-          if (lane == 0) {
-            uint8_t* st = smem + stage * STAGE_BYTES;
-            const uint64_t d_ahi = make_desc_sw64(st);
-            const uint64_t d_alo = make_desc_sw64(st + A_TILE);
-            const uint64_t d_bhi = make_desc_sw64(st + 2 * A_TILE);
-            const uint64_t d_blo = make_desc_sw64(st + 2 * A_TILE + B_TILE);
+          const uint32_t tmem_c = tmem_base + buf * BN;
+          const int c1 = min(nkb, c0 + chunk_kb);
+          for (int kb = c0; kb < c1; ++kb) {
+            mbar_wait(&full_bar[stage], phase);
+            tc_fence_after();
+            if (lane == 0) {
+              uint8_t* st = smem + stage * CF::STAGE_BYTES;
+              const uint64_t d_ahi = make_desc_sw64(st);
+              const uint64_t d_alo = make_desc_sw64(st + A_TILE);
+              const uint64_t d_bhi = make_desc_sw64(st + 2 * A_TILE);
+              const uint64_t d_blo = make_desc_sw64(st + 2 * A_TILE + CF::B_TILE);
 #pragma unroll
-            for (int kk = 0; kk < BK / 16; ++kk) {
-              const uint64_t adv = (uint64_t)(kk * 32) >> 4;  // 16 fp16 = 32 B along K
-              umma_f16(tmem_c, d_ahi + adv, d_blo + adv, (kb == c0 && kk == 0) ? 0u : 1u);
-              umma_f16(tmem_c, d_alo + adv, d_bhi + adv, 1u);
-              umma_f16(tmem_c, d_ahi + adv, d_bhi + adv, 1u);
+              for (int kk = 0; kk < BK / 16; ++kk) {
+                const uint64_t adv = (uint64_t)(kk * 32) >> 4;  // 16 fp16 = 32 B along K
+                umma_f16<CG>(tmem_c, d_ahi + adv, d_blo + adv, (kb == c0 && kk == 0) ? 0u : 1u);
+                umma_f16<CG>(tmem_c, d_alo + adv, d_bhi + adv, 1u);
+                umma_f16<CG>(tmem_c, d_ahi + adv, d_bhi + adv, 1u);
+              }
+              umma_commit<CG>(&empty_bar[stage]);
             }
-            umma_commit(&empty_bar[stage]);
+            __syncwarp();
+            if (++stage == STAGES) { stage = 0; phase ^= 1; }
           }
+          if (lane == 0) umma_commit<CG>(&pfull_bar[buf]);
           __syncwarp();
-          if (++stage == STAGES) { stage = 0; phase ^= 1; }
         }
-        if (lane == 0) umma_commit(&pfull_bar[buf]);
-        __syncwarp();
       }
     }
   } else if (warp >= 4) {
@@ -280,7 +355,7 @@ gemm_f16x3_kernel(const __grid_constant__ CUtensorMap tm_ahi, const __grid_const
     const float alpha = splits == 1 ? 1.f / (scale_of(*max_rows) * scale_of(*max_cols)) : 1.f;
     float vmax = 0.f;  // max |C| of this thread's outputs (scale slot of the result tensor)
     int gchunk = 0;
-    for (int w = blockIdx.x; w < total; w += gridDim.x) {
+    for (int w = unit; w < total; w += n_units) {
       const WorkCoord wc = decode(w, nm, nn, group_m);
       const int k_begin = wc.split * k_per_split;
       const int nkb = (min(Kp, k_begin + k_per_split) - k_begin + BK - 1) / BK;
@@ -300,9 +375,10 @@ gemm_f16x3_kernel(const __grid_constant__ CUtensorMap tm_ahi, const __grid_const
           for (int j = 0; j < 16; ++j) acc[s * 16 + j] += __uint_as_float(r[j]);
         }
         tc_fence_before();
-        mbar_arrive(&pempty_bar[buf]);
+        if (CG == 1 || leader) mbar_arrive(&pempty_bar[buf]);
+        else mbar_arrive_remote(&pempty_bar[buf], 0);
       }
-      const int row = wc.mb * BM + q * 32 + lane;
+      const int row = wc.mb * BM * CG + (int)rank * BM + q * 32 + lane;
       const int col0 = wc.nb * BN + grp * EPI_COLS;
 #pragma unroll
       for (int j = 0; j < EPI_COLS; ++j) {
@@ -329,11 +405,15 @@ gemm_f16x3_kernel(const __grid_constant__ CUtensorMap tm_ahi, const __grid_const
   }
 
   tc_fence_before();
-  __syncthreads();
+  if constexpr (CG == 1) __syncthreads(); else cluster_sync_all();
   if (warp == 2) {
     tc_fence_after();
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
-                 "r"(TMEM_COLS));
+    if constexpr (CG == 1)
+      asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
+                   "r"(TMEM_COLS));
+    else
+      asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
+                   "r"(TMEM_COLS));
   }
 }
 
@@ -358,6 +438,11 @@ EncodeTiledFn get_encode() {
   return fn;
 }
 
+int env_int(const char* name, int dflt) {
+  const char* e = getenv(name);
+  return e ? atoi(e) : dflt;
+}
+
 void make_map(void* out, const __half* base, int64_t rows, int64_t kp, int box_rows) {
   if ((reinterpret_cast<uintptr_t>(base) & 15) != 0 || (kp % 8) != 0)
     throw Error(TNB_ERR_SHAPE, "tensor-core operand not 16-byte aligned");
@@ -365,10 +450,7 @@ void make_map(void* out, const __half* base, int64_t rows, int64_t kp, int box_r
   cuuint64_t strides[1] = {(cuuint64_t)kp * 2};
   cuuint32_t box[2] = {(cuuint32_t)BK, (cuuint32_t)box_rows};
   cuuint32_t estr[2] = {1, 1};
-  static const int promo_env = [] {
-    const char* e = getenv("TNB_L2_PROMO");
-    return e ? atoi(e) : -1;
-  }();
+  static const int promo_env = env_int("TNB_L2_PROMO", -1);
   CUtensorMapL2promotion promo = CU_TENSOR_MAP_L2_PROMOTION_L2_256B;
   if (promo_env == 0) promo = CU_TENSOR_MAP_L2_PROMOTION_NONE;
   if (promo_env == 64) promo = CU_TENSOR_MAP_L2_PROMOTION_L2_64B;
@@ -380,12 +462,21 @@ void make_map(void* out, const __half* base, int64_t rows, int64_t kp, int box_r
   if (r != CUDA_SUCCESS) throw Error(TNB_ERR_CUDA, "cuTensorMapEncodeTiled failed: " + std::to_string((int)r));
 }
 
+// CTA group for a GEMM: pairs (cta_group::2) whenever the rows fill 256-row tiles
+int choose_cg(int64_t M) {
+  static const int forced = env_int("TNB_CTA_GROUP", 0);
+  if (forced == 1 || forced == 2) return forced;
+  return M >= 256 ? 2 : 1;
+}
+
 int choose_splits(int64_t M, int64_t Np, int64_t Kp, int num_sms) {
-  const int64_t tiles = ((M + BM - 1) / BM) * ((Np + BN - 1) / BN);
+  const int cg = choose_cg(M);
+  const int64_t units = num_sms / cg;
+  const int64_t tiles = ((M + BM * cg - 1) / (BM * cg)) * ((Np + BN - 1) / BN);
   const int64_t kblocks = (Kp + BK - 1) / BK;
   int s = 1;
   // split K while tiles leave SMs idle and every split keeps >= 16 K blocks
-  while (tiles * s * 2 <= num_sms && kblocks / (s * 2) >= 16 && s < 32) s *= 2;
+  while (tiles * s * 2 <= units && kblocks / (s * 2) >= 16 && s < 32) s *= 2;
   return s;
 }
 
@@ -409,11 +500,13 @@ void tc_plan_gemm(TcGemmPlan* p, const __half* Ahi, const __half* Alo, const __h
   if (M > (1ll << 31) - 1 || Np > (1ll << 31) - 1 || Kp > (1ll << 31) - 1)
     throw Error(TNB_ERR_SHAPE, "tensor-core GEMM dimension too large");
   p->M = M; p->Np = Np; p->Kp = Kp;
+  p->cta_group = choose_cg(M);
   p->splits = choose_splits(M, Np, Kp, num_sms);
   const int64_t kblocks = (Kp + BK - 1) / BK;
   p->k_per_split = ((kblocks + p->splits - 1) / p->splits) * BK;
-  const int64_t work = ((M + BM - 1) / BM) * ((Np + BN - 1) / BN) * p->splits;
-  p->grid = (int)(work < num_sms ? work : num_sms);
+  const int64_t units = num_sms / p->cta_group;
+  const int64_t work = ((M + BM * p->cta_group - 1) / (BM * p->cta_group)) * ((Np + BN - 1) / BN) * p->splits;
+  p->grid = (int)((work < units ? work : units) * p->cta_group);
   if (p->splits > 1) {
     if (workspace == nullptr || workspace_elems < (int64_t)p->splits * M * Np)
       throw Error(TNB_ERR_ARG, "split-K workspace too small");
@@ -424,25 +517,42 @@ void tc_plan_gemm(TcGemmPlan* p, const __half* Ahi, const __half* Alo, const __h
   p->max_rows = max_rows;
   p->max_cols = max_cols;
   p->max_out = max_out;
-  const char* env = getenv("TNB_CHUNK_KB");
-  p->chunk_kb = env ? atoi(env) : kDefaultChunkKb;
-  const char* genv = getenv("TNB_GROUP_M");
-  p->group_m = genv ? atoi(genv) : GROUP_M;
-  if (p->group_m <= 0) p->group_m = 1 << 30;
+  p->chunk_kb = env_int("TNB_CHUNK_KB", kDefaultChunkKb);
   if (p->chunk_kb <= 0) p->chunk_kb = 1 << 30;  // no promotion: whole K in TMEM
+  p->group_m = env_int("TNB_GROUP_M", GROUP_M);
+  if (p->group_m <= 0) p->group_m = 1 << 30;
+  const int b_rows = BN / p->cta_group;
   make_map(p->tmap[0], Ahi, M, Kp, BM);
   make_map(p->tmap[1], Alo, M, Kp, BM);
-  make_map(p->tmap[2], Bhi, Np, Kp, BN);
-  make_map(p->tmap[3], Blo, Np, Kp, BN);
+  make_map(p->tmap[2], Bhi, Np, Kp, b_rows);
+  make_map(p->tmap[3], Blo, Np, Kp, b_rows);
+}
+
+template <int CG>
+void launch_cg(const TcGemmPlan* p, cudaStream_t s) {
+  auto kern = gemm_f16x3_kernel<CG>;
+  TNB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg<CG>::SMEM_BYTES));
+  const CUtensorMap* maps = reinterpret_cast<const CUtensorMap*>(p->tmap);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(p->grid);
+  cfg.blockDim = dim3(NUM_THREADS);
+  cfg.dynamicSmemBytes = Cfg<CG>::SMEM_BYTES;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = CG;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  TNB_CUDA(cudaLaunchKernelEx(&cfg, kern, maps[0], maps[1], maps[2], maps[3], p->C, (int)p->M,
+                              (int)p->Np, (int)p->Kp, p->splits, (int)p->k_per_split, p->chunk_kb,
+                              p->group_m, p->max_rows, p->max_cols, p->max_out));
 }
 
 void tc_launch_gemm(const TcGemmPlan* p, cudaStream_t s) {
-  TNB_CUDA(cudaFuncSetAttribute(gemm_f16x3_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                SMEM_BYTES));
-  const CUtensorMap* maps = reinterpret_cast<const CUtensorMap*>(p->tmap);
-  gemm_f16x3_kernel<<<p->grid, NUM_THREADS, SMEM_BYTES, s>>>(
-      maps[0], maps[1], maps[2], maps[3], p->C, (int)p->M, (int)p->Np, (int)p->Kp, p->splits,
-      (int)p->k_per_split, p->chunk_kb, p->group_m, p->max_rows, p->max_cols, p->max_out);
+  if (p->cta_group == 2) launch_cg<2>(p, s);
+  else launch_cg<1>(p, s);
   check_launch("gemm_f16x3");
 }
 
