@@ -35,6 +35,7 @@ constexpr int NUM_THREADS = 128 + EPI_THREADS;
 constexpr int TMEM_COLS = 512;
 constexpr int kDefaultChunkKb = 8;           // K blocks (of 32 fp16) per promotion chunk
 constexpr int GROUP_M = 16;                  // rasterisation band height (m-tiles)
+constexpr int kDefaultPaceSlack = 64;        // K blocks a unit may run ahead of the slowest
 
 template <int CG>
 struct Cfg {
@@ -226,7 +227,8 @@ gemm_f16x3_kernel(const __grid_constant__ CUtensorMap tm_ahi, const __grid_const
                   const __grid_constant__ CUtensorMap tm_bhi, const __grid_constant__ CUtensorMap tm_blo,
                   float* __restrict__ C, int M, int Np, int Kp, int splits, int k_per_split,
                   int chunk_kb, int group_m, const unsigned int* __restrict__ max_rows,
-                  const unsigned int* __restrict__ max_cols, unsigned int* __restrict__ max_out) {
+                  const unsigned int* __restrict__ max_cols, unsigned int* __restrict__ max_out,
+                  unsigned int* __restrict__ progress, int pace_slack) {
   using CF = Cfg<CG>;
   constexpr int STAGES = CF::STAGES;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -283,17 +285,32 @@ gemm_f16x3_kernel(const __grid_constant__ CUtensorMap tm_ahi, const __grid_const
   const uint32_t tmem_base = *tmem_slot;
 
   if (warp == 0) {
-    if (lane == 0) {
-      // ===== TMA producer (both CTAs) =====
-      int stage = 0;
-      uint32_t phase = 0;
-      for (int w = unit; w < total; w += n_units) {
-        const WorkCoord wc = decode(w, nm, nn, group_m);
-        const int k_begin = wc.split * k_per_split;
-        const int k_end = min(Kp, k_begin + k_per_split);
-        const int m0 = wc.mb * BM * CG + (int)rank * BM;
-        const int n0 = wc.nb * BN + (int)rank * CF::B_ROWS;
-        for (int k = k_begin; k < k_end; k += BK) {
+    // ===== TMA producer (both CTAs; lane 0 issues, the warp helps pacing) =====
+    // Soft pacing (leader): every unit publishes its K-block count; a unit
+    // more than `pace_slack` blocks ahead of the slowest one waits, so the
+    // CTAs streaming the same A/B panels stay within the L2 reuse window.
+    int stage = 0;
+    uint32_t phase = 0;
+    uint32_t issued = 0;
+    const bool pace = pace_slack > 0 && leader && progress != nullptr;
+    for (int w = unit; w < total; w += n_units) {
+      const WorkCoord wc = decode(w, nm, nn, group_m);
+      const int k_begin = wc.split * k_per_split;
+      const int k_end = min(Kp, k_begin + k_per_split);
+      const int m0 = wc.mb * BM * CG + (int)rank * BM;
+      const int n0 = wc.nb * BN + (int)rank * CF::B_ROWS;
+      for (int k = k_begin; k < k_end; k += BK, ++issued) {
+        if (pace && (issued & 15) == 0) {
+          if (lane == 0) atomicExch(progress + unit, issued);
+          for (;;) {
+            unsigned int mn = 0xFFFFFFFFu;
+            for (int u = lane; u < n_units; u += 32) mn = min(mn, __ldcg(progress + u));
+            mn = __reduce_min_sync(0xffffffffu, mn);
+            if (mn == 0xFFFFFFFFu || issued <= mn + (unsigned)pace_slack) break;
+            __nanosleep(128);
+          }
+        }
+        if (lane == 0) {
           mbar_wait(&empty_bar[stage], phase ^ 1);
           uint8_t* st = smem + stage * CF::STAGE_BYTES;
           if (leader) mbar_arrive_expect_tx(&full_bar[stage], CG * CF::STAGE_BYTES);
@@ -302,10 +319,12 @@ gemm_f16x3_kernel(const __grid_constant__ CUtensorMap tm_ahi, const __grid_const
           tma_load_2d<CG>(st + A_TILE, &tm_alo, &full_bar[stage], k, m0);
           tma_load_2d<CG>(st + 2 * A_TILE, &tm_bhi, &full_bar[stage], k, n0);
           tma_load_2d<CG>(st + 2 * A_TILE + CF::B_TILE, &tm_blo, &full_bar[stage], k, n0);
-          if (++stage == STAGES) { stage = 0; phase ^= 1; }
         }
+        __syncwarp();
+        if (++stage == STAGES) { stage = 0; phase ^= 1; }
       }
     }
+    if (pace && lane == 0) atomicExch(progress + unit, 0xFFFFFFFFu);  // done: never hold others back
   } else if (warp == 1) {
     if (leader) {
       // ===== MMA issuer (leader CTA) =====
@@ -521,6 +540,7 @@ void tc_plan_gemm(TcGemmPlan* p, const __half* Ahi, const __half* Alo, const __h
   if (p->chunk_kb <= 0) p->chunk_kb = 1 << 30;  // no promotion: whole K in TMEM
   p->group_m = env_int("TNB_GROUP_M", GROUP_M);
   if (p->group_m <= 0) p->group_m = 1 << 30;
+  p->pace_slack = env_int("TNB_PACE", kDefaultPaceSlack);
   const int b_rows = BN / p->cta_group;
   make_map(p->tmap[0], Ahi, M, Kp, BM);
   make_map(p->tmap[1], Alo, M, Kp, BM);
@@ -545,9 +565,12 @@ void launch_cg(const TcGemmPlan* p, cudaStream_t s) {
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
+  if (p->progress && p->pace_slack > 0)
+    TNB_CUDA(cudaMemsetAsync(p->progress, 0, sizeof(unsigned int) * (p->grid / CG), s));
   TNB_CUDA(cudaLaunchKernelEx(&cfg, kern, maps[0], maps[1], maps[2], maps[3], p->C, (int)p->M,
                               (int)p->Np, (int)p->Kp, p->splits, (int)p->k_per_split, p->chunk_kb,
-                              p->group_m, p->max_rows, p->max_cols, p->max_out));
+                              p->group_m, p->max_rows, p->max_cols, p->max_out, p->progress,
+                              p->pace_slack));
 }
 
 void tc_launch_gemm(const TcGemmPlan* p, cudaStream_t s) {

@@ -141,6 +141,7 @@ struct Program {
   SlicedLeafDesc* d_sl_descs = nullptr; int n_sl_descs = 0;
   uint32_t* d_keep = nullptr;
   unsigned int* d_tmax = nullptr;   // per-tensor max|re|,|im| slots (fp32 bits)
+  unsigned int* d_progress = nullptr;  // GEMM soft-pacing counters (one per CTA unit)
   std::vector<int> slot;            // tensor -> slot
   int inv_slot_begin = 0, inv_slot_count = 0, var_slot_begin = 0, var_slot_count = 0;
   std::vector<StageTables> stages;  // device views of the TC staging tables
@@ -162,7 +163,7 @@ struct Program {
   ~Program() {
     if (device >= 0) cudaSetDevice(device);
     void* ptrs[] = {d_leaf_pool, d_slice_pool, d_persist, d_arena, d_scratch, d_luts,
-                    d_sl_descs, d_keep, d_tmax, d_acc, d_stage_u32, d_stage_luts};
+                    d_sl_descs, d_keep, d_tmax, d_acc, d_stage_u32, d_stage_luts, d_progress};
     for (void* p : ptrs)
       if (p) cudaFree(p);
     for (auto e : ev_pool) cudaEventDestroy(e);
@@ -507,6 +508,7 @@ Program* program_create(const tnb_program_desc* d) {
   dmalloc(&P->d_acc, (int64_t)P->n_acc_slots * align_up(P->out_elems, 128) * (int64_t)P->esize);
 
   // ---- tensor-core plans (fixed addresses -> TMA descriptors built once)
+  dmalloc((void**)&P->d_progress, (int64_t)P->num_sms * 4);
   for (auto& s : P->steps) {
     if (s.kind != KIND_TC) continue;
     const int64_t Kp = 2 * s.K, Np = 2 * s.N;
@@ -520,6 +522,7 @@ Program* program_create(const tnb_program_desc* d) {
     tc_plan_gemm(&s.tc, ahi, alo, bhi, blo, s.M, Np, Kp, (float*)P->tensor_ptr(s.out), ws, ws_elems,
                  P->d_tmax + P->slot[s.rows_t], P->d_tmax + P->slot[s.cols_t],
                  P->d_tmax + P->slot[s.out], P->num_sms);
+    s.tc.progress = P->d_progress;
   }
 
   // ---- upload leaf values

@@ -208,6 +208,8 @@ int tnb_cgemm(int32_t device, int64_t M, int64_t N, int64_t K, const void* A, co
       launch_stage((const float2*)pb, tb[1], K, true, mx + 1, bhi, blo, st);
       TcGemmPlan plan;
       tc_plan_gemm(&plan, ahi, alo, bhi, blo, M, Np, Kp, (float*)pc, wsp, ws, mx, mx + 1, mx + 2, sms);
+      DevBuf progress((size_t)sms * 4);
+      plan.progress = (unsigned int*)progress.p;
       tc_launch_gemm(&plan, st);
       if (plan.splits > 1)
         launch_splitk_reduce(plan.C, plan.splits, M * Np, (float*)pc, mx, mx + 1, mx + 2, st);
