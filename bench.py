@@ -186,12 +186,15 @@ def run_ours(args):
     dev_ms = 0.0
     gemm_ms = gemm_flops = 0.0
     launches = gemm_launches = 0
+    breakdown = {"convert_ms": 0.0, "simt_ms": 0.0, "other_ms": 0.0}
     t0 = time.perf_counter()
     with ClockSampler(local) as clk:
         for s in range(args.warmup, args.warmup + args.steps):
             ms, th, tt = step(s)
             dev_ms += ms
             gemm_ms += th["gemm_ms"] + tt["gemm_ms"]
+            for key in ("convert_ms", "simt_ms", "other_ms"):
+                breakdown[key] += th[key] + tt[key]
             gemm_flops += th["gemm_flops"] + tt["gemm_flops"]
             launches += th["launches"] + tt["launches"]
             gemm_launches += th["gemm_launches"] + tt["gemm_launches"]
@@ -229,6 +232,38 @@ def run_ours(args):
         e2e = {"value": world * args.steps * S / (e_ms / 1e3), "unit": "slices/s",
                "h2d_bytes_per_step": h2d // args.steps, "d2h_bytes_per_step": d2h // args.steps,
                "ms_per_step": e_ms / args.steps}
+
+    # ---- optional: cross-slice reuse (TNB_FLAG_REUSE_SLICES) -- reported beside the
+    # headline, NOT as it: it skips re-computing results whose mask bits did not change
+    reuse = None
+    if args.reuse:
+        from paper_2103_03074_b200 import _lib as L
+
+        E.clear_cache()
+        del head, tail
+        rprog = E.head_program(tn, tree, w.sliced, "single", device=local,
+                               flags=L.TNB_FLAG_REUSE_SLICES)
+        rprog.set_timing(True)
+        rbase = base + total_slices  # fresh slices beyond the headline subset
+        for s in range(args.warmup):
+            rprog.run_range(rbase + s * S, rbase + (s + 1) * S, "fixed", out=hvec.data_ptr())
+        barrier(dist, local)
+        r_ms = r_gemm_ms = r_gemm_flops = 0.0
+        r_reused = 0
+        for s in range(args.warmup, args.warmup + args.steps):
+            rprog.run_range(rbase + s * S, rbase + (s + 1) * S, "fixed", out=hvec.data_ptr())
+            t = rprog.timing()
+            r_ms += t["total_ms"]
+            r_gemm_ms += t["gemm_ms"]
+            r_gemm_flops += t["gemm_flops"]
+            r_reused += t["steps_reused"]
+        reuse = {"value": world * args.steps * S / (r_ms / 1e3), "unit": "slices/s",
+                 "executed_gemm_tflops": r_gemm_flops / (r_gemm_ms / 1e3) / 1e12 if r_gemm_ms else 0,
+                 "executed_flop_fraction": r_gemm_flops / (args.steps * S * 8.0 * w.tc_per_slice),
+                 "steps_reused": r_reused, "cache_bytes": int(rprog.info.reuse_bytes),
+                 "note": "head slices with TNB_FLAG_REUSE_SLICES: steps whose mask bits did not "
+                         "change between consecutive slices are not recomputed (results "
+                         "bit-identical, tests/test_gpu_parity.py); tail excluded"}
 
     if rank != 0:
         return
@@ -268,10 +303,14 @@ def run_ours(args):
             "traffic": None,
         },
         "gpu_launches": launches,
+        "device_ms_per_step": {"total": dev_ms / args.steps, "gemm": gemm_ms / args.steps,
+                               **{k: v / args.steps for k, v in breakdown.items()},
+                               "gaps": (dev_ms - gemm_ms - sum(breakdown.values())) / args.steps},
         "gemm_launches": gemm_launches,
         "wall_ms_per_step": wall_ms / args.steps,
         "clocks": clk.summary(),
         "e2e": e2e,
+        "cross_slice_reuse": reuse,
     }
     if world == 1 and not args.no_cpu:
         line["cpu_baseline"] = cpu_baseline(w)
@@ -319,6 +358,7 @@ def main():
     ap.add_argument("--workload", default=WORKLOAD)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--reuse", type=int, default=1, help="also time TNB_FLAG_REUSE_SLICES (reported separately)")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)

@@ -60,6 +60,9 @@ typedef enum { TNB_FIXED = 0, TNB_FREE = 1 } tnb_mode;          /* engine.py:293
 /* program flags */
 #define TNB_FLAG_NO_TENSOR_CORES 0x1u  /* force the SIMT contraction kernel      */
 #define TNB_FLAG_NO_HOIST        0x2u  /* recompute slice-invariant subtrees     */
+#define TNB_FLAG_REUSE_SLICES    0x4u  /* reuse results whose mask bits did not
+                                          change between consecutive slices
+                                          (bit-identical; skips recomputation)  */
 
 typedef struct tnb_program tnb_program;
 
@@ -93,6 +96,7 @@ typedef struct {
   int32_t n_steps_simt;         /* steps on the SIMT path                           */
   int32_t n_steps_hoisted;      /* slice-invariant steps computed once              */
   int32_t kernels_per_slice;    /* launches per slice                               */
+  int64_t reuse_bytes;          /* TNB_FLAG_REUSE_SLICES: dedicated cached buffers  */
 } tnb_program_info;
 
 typedef struct {
@@ -104,6 +108,7 @@ typedef struct {
   int64_t launches;             /* kernels launched by the last run_range           */
   int64_t gemm_launches;
   double gemm_flops;            /* algorithmic complex FLOPs executed on tcgen05    */
+  int64_t steps_reused;         /* steps skipped by TNB_FLAG_REUSE_SLICES           */
 } tnb_timing;
 
 int tnb_abi_version(void);

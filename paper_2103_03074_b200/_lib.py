@@ -20,6 +20,7 @@ TNB_DOUBLE, TNB_SINGLE = 0, 1
 TNB_FIXED, TNB_FREE = 0, 1
 TNB_FLAG_NO_TENSOR_CORES = 0x1
 TNB_FLAG_NO_HOIST = 0x2
+TNB_FLAG_REUSE_SLICES = 0x4
 
 i32, i64, u32, u64, f64 = C.c_int32, C.c_int64, C.c_uint32, C.c_uint64, C.c_double
 P = C.c_void_p
@@ -41,7 +42,7 @@ class ProgramInfo(C.Structure):
         ("out_elems", i64), ("flops_per_slice", f64), ("tc_flops_per_slice", f64),
         ("arena_bytes", i64), ("persistent_bytes", i64), ("scratch_bytes", i64),
         ("n_steps_tc", i32), ("n_steps_simt", i32), ("n_steps_hoisted", i32),
-        ("kernels_per_slice", i32),
+        ("kernels_per_slice", i32), ("reuse_bytes", i64),
     ]
 
 
@@ -49,6 +50,7 @@ class Timing(C.Structure):
     _fields_ = [
         ("total_ms", f64), ("gemm_ms", f64), ("convert_ms", f64), ("simt_ms", f64),
         ("other_ms", f64), ("launches", i64), ("gemm_launches", i64), ("gemm_flops", f64),
+        ("steps_reused", i64),
     ]
 
 

@@ -86,6 +86,8 @@ enum Pool { POOL_LEAF = 0, POOL_SLICE = 1, POOL_PERSIST = 2, POOL_ARENA = 3 };
 struct TensorRec {
   std::vector<int64_t> axes;
   bool variant = false;
+  uint64_t dep = 0;     // mask bits this tensor depends on (reuse mode)
+  bool cached = false;  // reuse mode: value must survive across masks (dedicated buffer)
   int pool = POOL_LEAF;
   int64_t off = 0;  // element offset within the pool
   int64_t elems = 1;
@@ -100,6 +102,8 @@ struct StepRec {
   int a = -1, b = -1, out = -1;
   int kind = KIND_SIMT;
   bool hoisted = false;
+  bool has_key = false;   // reuse mode: output valid for mask bits `last_key`
+  uint64_t last_key = 0;
   int64_t M = 1, N = 1, K = 1;   // SIMT: rows of a, cols of b, shared. TC: rows/cols operand.
   int rows_t = -1, cols_t = -1;  // TC operand tensors (rows unexpanded, cols expanded)
   int lut_a = -1, lut_b = -1;    // SIMT: indices into the LUT table
@@ -150,6 +154,8 @@ struct Program {
   void* d_acc = nullptr;          // (n_sliced + 2) accumulator slots of out_elems
   int n_acc_slots = 0;
   bool invariant_valid = false;
+  bool reuse = false;               // TNB_FLAG_REUSE_SLICES
+  int64_t reuse_bytes = 0;          // dedicated buffers of cross-slice cached tensors
 
   // timing
   bool timing = false;
@@ -233,6 +239,7 @@ Program* program_create(const tnb_program_desc* d) {
   P->flags = d->flags;
   P->esize = d->precision == TNB_SINGLE ? 8 : 16;
   P->n_sliced = d->n_sliced;
+  P->reuse = (d->flags & TNB_FLAG_REUSE_SLICES) != 0;
   TNB_CUDA(cudaSetDevice(P->device));
   TNB_CUDA(cudaDeviceGetAttribute(&P->num_sms, cudaDevAttrMultiProcessorCount, P->device));
   TNB_CUDA(cudaStreamCreateWithFlags(&P->stream, cudaStreamNonBlocking));
@@ -265,6 +272,7 @@ Program* program_create(const tnb_program_desc* d) {
       auto it = slice_bit.find(full[ax]);
       if (it != slice_bit.end()) {
         sl.push_back({it->second, 1u << (r - 1 - ax)});
+        t.dep |= 1ull << it->second;
       } else {
         t.axes.push_back(full[ax]);
         keep_src.push_back(r - 1 - ax);
@@ -328,6 +336,13 @@ Program* program_create(const tnb_program_desc* d) {
     s.mults = std::ldexp(1.0, na + nb + nab);
     TensorRec o;
     o.variant = A.variant || B.variant;
+    o.dep = A.dep | B.dep;
+    if (P->reuse) {
+      // an operand whose mask dependence is narrower than its consumer's can be
+      // reused across consecutive masks: it needs a buffer of its own
+      if (A.variant && A.dep != o.dep && A.leaf_pos < 0) P->tensors[s.a].cached = true;
+      if (B.variant && B.dep != o.dep && B.leaf_pos < 0) P->tensors[s.b].cached = true;
+    }
     o.def_step = i;
     s.M = (int64_t)1 << na;
     s.N = (int64_t)1 << nb;
@@ -403,10 +418,11 @@ Program* program_create(const tnb_program_desc* d) {
   for (int i = 0; i < n_steps; ++i) {
     StepRec& s = P->steps[i];
     TensorRec& o = P->tensors[s.out];
-    if (s.hoisted || !o.variant) {
+    if (s.hoisted || !o.variant || o.cached) {
       o.pool = POOL_PERSIST;
       o.off = persist_off;
       persist_off += align_up(o.elems, 128);
+      if (o.cached) P->reuse_bytes += o.elems * (int64_t)P->esize;
     } else {
       o.pool = POOL_ARENA;
       o.off = arena.alloc(o.elems * (int64_t)P->esize) / (int64_t)P->esize;
@@ -569,6 +585,7 @@ void program_info(const Program* P, tnb_program_info* info) {
     k += s.kind == KIND_TC ? (3 + (s.tc.splits > 1 ? 1 : 0)) : 1;
   }
   info->kernels_per_slice = k + 1;
+  info->reuse_bytes = P->reuse_bytes;
 }
 
 void program_set_leaf(Program* P, int leaf_pos, const double* data) {
@@ -609,7 +626,7 @@ struct RunCtx {
   Program* P;
   std::vector<EvRec> recs;
   size_t ev_next = 0;
-  int64_t launches = 0, gemm_launches = 0;
+  int64_t launches = 0, gemm_launches = 0, reused = 0;
   double gemm_flops = 0;
   cudaEvent_t get() {
     if (ev_next == P->ev_pool.size()) {
@@ -699,8 +716,10 @@ void run_range_t(Program* P, uint64_t a, uint64_t b, int mode, void* out, bool o
   if (!P->invariant_valid) {
     if (P->inv_slot_count)
       TNB_CUDA(cudaMemsetAsync(P->d_tmax + P->inv_slot_begin, 0, (size_t)P->inv_slot_count * 4, st));
-    for (auto& s : P->steps)
+    for (auto& s : P->steps) {
       if (s.hoisted) exec_step<T>(P, s);
+      s.has_key = false;  // leaf data changed: every cached result is stale
+    }
     P->invariant_valid = true;
   }
 
@@ -714,10 +733,25 @@ void run_range_t(Program* P, uint64_t a, uint64_t b, int mode, void* out, bool o
                              P->n_sl_descs, P->d_keep, mask, st);
     if (P->n_sl_descs) ctx.launches++;
     ctx.close(3, e);
-    if (P->var_slot_count)
-      TNB_CUDA(cudaMemsetAsync(P->d_tmax + P->var_slot_begin, 0, (size_t)P->var_slot_count * 4, st));
-    for (auto& s : P->steps)
-      if (!s.hoisted) exec_step<T>(P, s);
+    if (!P->reuse) {
+      if (P->var_slot_count)
+        TNB_CUDA(cudaMemsetAsync(P->d_tmax + P->var_slot_begin, 0, (size_t)P->var_slot_count * 4, st));
+      for (auto& s : P->steps)
+        if (!s.hoisted) exec_step<T>(P, s);
+    } else {
+      // cross-slice reuse: a step re-executes only when the mask bits its
+      // result depends on change; skipped results are bit-identical to a
+      // recomputation (deterministic kernels, fresh fp16 scale per result)
+      for (auto& s : P->steps) {
+        if (s.hoisted) continue;
+        const uint64_t key = mask & P->tensors[s.out].dep;
+        if (s.has_key && s.last_key == key) { ctx.reused++; continue; }
+        TNB_CUDA(cudaMemsetAsync(P->d_tmax + P->slot[s.out], 0, 4, st));
+        exec_step<T>(P, s);
+        s.has_key = true;
+        s.last_key = key;
+      }
+    }
     e = ctx.mark();
     if (mode == TNB_FIXED) {
       // binary-counter increment: the new chunk merges with the levels
@@ -778,6 +812,7 @@ void run_range_t(Program* P, uint64_t a, uint64_t b, int mode, void* out, bool o
   tm.launches = ctx.launches;
   tm.gemm_launches = ctx.gemm_launches;
   tm.gemm_flops = ctx.gemm_flops;
+  tm.steps_reused = ctx.reused;
   P->last = tm;
 }
 

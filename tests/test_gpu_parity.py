@@ -226,3 +226,22 @@ def test_head_program_info(gpu, workloads):
     prog = tnb.head_program(w.tn, w.tree, w.sliced, "single")
     assert prog.info.n_steps_tc >= 5
     assert abs(prog.info.flops_per_slice - 8.0 * w.tc_per_slice) / (8.0 * w.tc_per_slice) < 1e-12
+
+
+@pytest.mark.parametrize("name,rng_", [("s8", (0, 16)), ("m12", (0, 4))])
+def test_cross_slice_reuse_bit_identical(gpu, workloads, name, rng_):
+    """TNB_FLAG_REUSE_SLICES skips steps whose mask bits did not change; the
+    head vector must be bit-identical to full recomputation."""
+    from paper_2103_03074_b200 import _lib, engine as E
+
+    w = workloads(name)
+    base = E.head_program(w.tn, w.tree, w.sliced, "single", flags=0)
+    ref = base.run_range(*rng_)
+    reuse = E.head_program(w.tn, w.tree, w.sliced, "single", flags=_lib.TNB_FLAG_REUSE_SLICES)
+    reuse.set_timing(True)
+    got = reuse.run_range(*rng_)
+    assert np.array_equal(got, ref)
+    assert reuse.timing()["steps_reused"] > 0
+    # continuing with the next range reuses across calls, still bit-identical
+    a, b = rng_
+    assert np.array_equal(reuse.run_range(b, 2 * b - a), base.run_range(b, 2 * b - a))
