@@ -11,12 +11,24 @@
 #include <cuda_fp16.h>
 
 #include <algorithm>
+#include <cstdlib>
+#include <type_traits>
 
 namespace tnb {
 
 namespace {
 
 constexpr int kSms = 148;
+// staging tiles: 2^kStageTileBits elements; contiguous runs of 2^kStageRunBits
+// elements on both the source (reads) and the destination (writes) side
+int stage_tile_bits() {
+  static const int v = [] { const char* e = getenv("TNB_STAGE_TILE"); int x = e ? atoi(e) : 11; return x < 8 ? 8 : (x > 12 ? 12 : x); }();
+  return v;
+}
+int stage_run_bits() {
+  static const int v = [] { const char* e = getenv("TNB_STAGE_RUN"); int x = e ? atoi(e) : 5; return x < 3 ? 3 : (x > 7 ? 7 : x); }();
+  return v;
+}
 
 __device__ __forceinline__ uint32_t lut_map(const uint32_t (*t)[256], uint32_t j) {
   return t[0][j & 255u] | t[1][(j >> 8) & 255u] | t[2][(j >> 16) & 255u] | t[3][j >> 24];
@@ -209,53 +221,59 @@ __device__ __forceinline__ void split2(float a, float b, __half2& hi, __half2& l
 // in source order (coalesced 256-B runs) into shared memory and written in
 // destination order (coalesced runs).  rows: hi/lo[j] for j = r*K + k;
 // cols (expand): rows 2n / 2n+1 of the 2x2 real representation.
-template <bool kExpand>
+template <bool kExpand, int EPT>
 __global__ void __launch_bounds__(256)
 stage_kernel(const float2* __restrict__ src, StageTables tb, int64_t K, int logK,
              const unsigned int* __restrict__ maxbits, __half2* __restrict__ hi,
              __half2* __restrict__ lo) {
-  extern __shared__ float2 tile_smem[];
-  float2* tile = tile_smem;
-  // tile padded by one element per 32 (conflict-free transposed stores)
-  uint32_t* rd_t = reinterpret_cast<uint32_t*>(tile + (1 << tb.nU) + (1 << tb.nU) / 32);
-  uint32_t* rd_src = rd_t + (1 << tb.nU);
-  uint32_t* t_dst = rd_src + (1 << tb.nU);
+  extern __shared__ float2 tile[];  // padded by one element per 32
   __shared__ uint32_t ls[4][256];
   __shared__ uint32_t ld[4][256];
-  const int tsize = 1 << tb.nU;
-  for (int i = threadIdx.x; i < tsize; i += blockDim.x) {
-    rd_t[i] = tb.rd_t[i];
-    rd_src[i] = tb.rd_src[i];
-    t_dst[i] = tb.t_dst[i];
-  }
   for (int i = threadIdx.x; i < 1024; i += blockDim.x) {
     ls[i >> 8][i & 255] = tb.tile_src->t[i >> 8][i & 255];
     ld[i >> 8][i & 255] = tb.tile_dst->t[i >> 8][i & 255];
   }
+  const int tsize = 1 << tb.nU;
   const float s = scale_from_bits(*maxbits);
   __syncthreads();
   for (int64_t T = blockIdx.x; T < tb.n_tiles; T += gridDim.x) {
     const uint32_t sbase = lut_map(ls, (uint32_t)T);
     const uint32_t dbase = lut_map(ld, (uint32_t)T);
-    for (int i = threadIdx.x; i < tsize; i += blockDim.x) {
-      const uint32_t t = rd_t[i];
-      tile[t + (t >> 5)] = src[sbase + rd_src[i]];
+    // read phase: EPT independent loads in flight per thread (source order)
+    float2 v[EPT];
+    uint32_t tt[EPT];
+#pragma unroll
+    for (int j = 0; j < EPT; ++j) {
+      const int i = threadIdx.x + 256 * j;
+      if (i < tsize) {
+        tt[j] = __ldg(tb.rd_t + i);
+        v[j] = src[sbase + __ldg(tb.rd_src + i)];
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < EPT; ++j) {
+      const int i = threadIdx.x + 256 * j;
+      if (i < tsize) tile[tt[j] + (tt[j] >> 5)] = v[j];
     }
     __syncthreads();
-    for (int t = threadIdx.x; t < tsize; t += blockDim.x) {
-      const float2 v = tile[t + (t >> 5)];
-      const uint32_t j = dbase + t_dst[t];
+    // write phase: destination order
+#pragma unroll
+    for (int j = 0; j < EPT; ++j) {
+      const int t = threadIdx.x + 256 * j;
+      if (t >= tsize) break;
+      const float2 x = tile[t + (t >> 5)];
+      const uint32_t d = dbase + __ldg(tb.t_dst + t);
       if (!kExpand) {
         __half2 h, o;
-        split2(v.x * s, v.y * s, h, o);
-        hi[j] = h;
-        lo[j] = o;
+        split2(x.x * s, x.y * s, h, o);
+        hi[d] = h;
+        lo[d] = o;
       } else {
-        const uint64_t n = j >> logK;
-        const uint64_t r0 = (uint64_t)j + n * (uint64_t)K, r1 = r0 + (uint64_t)K;
+        const uint64_t n = d >> logK;
+        const uint64_t r0 = (uint64_t)d + n * (uint64_t)K, r1 = r0 + (uint64_t)K;
         __half2 h0, o0, h1, o1;
-        split2(v.x * s, -v.y * s, h0, o0);
-        split2(v.y * s, v.x * s, h1, o1);
+        split2(x.x * s, -x.y * s, h0, o0);
+        split2(x.y * s, x.x * s, h1, o1);
         hi[r0] = h0; lo[r0] = o0;
         hi[r1] = h1; lo[r1] = o1;
       }
@@ -355,18 +373,18 @@ void launch_absmax(const float2* A, int64_t n, unsigned int* maxbits, cudaStream
 
 void build_stage_tables(const std::vector<int>& canon_to_src, int64_t K, StageHost* out) {
   const int r = (int)canon_to_src.size();
-  const int Ld = std::min(5, r), Ls = std::min(5, r);
+  const int Ld = std::min(stage_run_bits(), r), Ls = std::min(stage_run_bits(), r);
   std::vector<int> src_to_canon(r, -1);
   for (int p = 0; p < r; ++p) src_to_canon[canon_to_src[p]] = p;
   std::vector<char> inU(r, 0);
   for (int p = 0; p < Ld; ++p) inU[p] = 1;
   for (int q = 0; q < Ls; ++q) inU[src_to_canon[q]] = 1;
-  // grow the tile to >= 2^10 elements (or the whole tensor) with the next
+  // grow the tile to 2^11 elements (or the whole tensor) with the next
   // lowest canonical bits so every tile keeps 256 threads busy
   {
     int cnt = 0;
     for (int p = 0; p < r; ++p) cnt += inU[p];
-    for (int p = 0; p < r && cnt < std::min(r, 10); ++p)
+    for (int p = 0; p < r && cnt < std::min(r, stage_tile_bits()); ++p)
       if (!inU[p]) { inU[p] = 1; ++cnt; }
   }
   std::vector<int> U, V;
@@ -407,18 +425,24 @@ void launch_stage(const float2* src, const StageTables& tb, int64_t K, bool expa
                   const unsigned int* maxbits, __half* hi, __half* lo, cudaStream_t s) {
   int logK = 0;
   while ((1ll << logK) < K) ++logK;
-  const size_t smem = ((size_t)1 << tb.nU) * (8 + 12) + (((size_t)1 << tb.nU) / 32) * 8;
+  const size_t smem = ((size_t)1 << tb.nU) * 8 + (((size_t)1 << tb.nU) / 32 + 1) * 8;
   int64_t g = tb.n_tiles;
-  const int64_t cap = (int64_t)kSms * 6;
+  const int64_t cap = (int64_t)kSms * 8;
   if (g > cap) g = cap;
-  if (expand)
-    stage_kernel<true><<<(unsigned)g, 256, smem, s>>>(src, tb, K, logK, maxbits,
-                                                       reinterpret_cast<__half2*>(hi),
-                                                       reinterpret_cast<__half2*>(lo));
-  else
-    stage_kernel<false><<<(unsigned)g, 256, smem, s>>>(src, tb, K, logK, maxbits,
-                                                        reinterpret_cast<__half2*>(hi),
-                                                        reinterpret_cast<__half2*>(lo));
+  const int ept = (1 << tb.nU) <= 256 ? 1 : (1 << tb.nU) / 256;
+  auto go = [&](auto kexp, auto kept) {
+    stage_kernel<decltype(kexp)::value, decltype(kept)::value><<<(unsigned)g, 256, smem, s>>>(
+        src, tb, K, logK, maxbits, reinterpret_cast<__half2*>(hi), reinterpret_cast<__half2*>(lo));
+  };
+  using T_ = std::true_type;
+  using F_ = std::false_type;
+  switch (ept) {
+    case 1: expand ? go(T_{}, std::integral_constant<int, 1>{}) : go(F_{}, std::integral_constant<int, 1>{}); break;
+    case 2: expand ? go(T_{}, std::integral_constant<int, 2>{}) : go(F_{}, std::integral_constant<int, 2>{}); break;
+    case 4: expand ? go(T_{}, std::integral_constant<int, 4>{}) : go(F_{}, std::integral_constant<int, 4>{}); break;
+    case 8: expand ? go(T_{}, std::integral_constant<int, 8>{}) : go(F_{}, std::integral_constant<int, 8>{}); break;
+    default: expand ? go(T_{}, std::integral_constant<int, 16>{}) : go(F_{}, std::integral_constant<int, 16>{}); break;
+  }
   check_launch("stage");
 }
 
