@@ -34,8 +34,8 @@ constexpr int EPI_COLS = BN / EPI_SPLIT;     // fp32 register accumulator column
 constexpr int NUM_THREADS = 128 + EPI_THREADS;
 constexpr int TMEM_COLS = 512;
 constexpr int kDefaultChunkKb = 8;           // K blocks (of 32 fp16) per promotion chunk
-constexpr int GROUP_M = 16;                  // rasterisation band height (m-tiles)
-constexpr int kDefaultPaceSlack = 64;        // K blocks a unit may run ahead of the slowest
+constexpr int GROUP_M = 8;                   // rasterisation band height (m-tiles / CTA pairs)
+constexpr int kDefaultPaceSlack = 32;        // K blocks a unit may run ahead of the slowest
 
 template <int CG>
 struct Cfg {
