@@ -29,5 +29,6 @@ from .errors import (  # noqa: F401
     ShapeMismatch,
     TncutError,
 )
+from .io import read_head_vector, write_amplitude_tsv, write_head_vector  # noqa: F401
 from .provenance import normalize_s1, provenance_hash  # noqa: F401
 from .workloads import load_workload  # noqa: F401

@@ -1,0 +1,32 @@
+"""File-based ranged partials from the GPU path (TNCUTHV1), reduced -- needs a B200."""
+
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+import paper_2103_03074_b200 as tnb
+from paper_2103_03074_b200 import io
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.mark.parametrize("precision", ["single", "double"])
+def test_gpu_partials_through_files_reduce_bit_exactly(gpu, workloads, tmp_path, precision):
+    w = workloads("c1")
+    full = tnb.compute_head_vector(w.tn, w.tree, w.sliced, None, precision=precision)
+    paths = []
+    for a in (8, 0):  # out of order, as separate workers would finish
+        hv = tnb.compute_head_vector(w.tn, w.tree, w.sliced, None, slice_range=(a, a + 8),
+                                     precision=precision)
+        paths.append(tmp_path / f"part{a}.hv")
+        io.write_head_vector(paths[-1], hv)
+    red = tnb.reduce_partials([io.read_head_vector(p) for p in paths])
+    assert np.array_equal(red.data, full.data)
+    tab = tnb.compute_tail_amplitudes(w.tn, w.tree, red, precision=precision)
+    ref = tnb.compute_tail_amplitudes(w.tn, w.tree, full, precision=precision)
+    assert np.array_equal(tab.amplitudes, ref.amplitudes)
+    io.write_amplitude_tsv(tmp_path / "amps.tsv", tab)
+    lines = (tmp_path / "amps.tsv").read_text().splitlines()
+    assert len(lines) == 2 + (1 << len(tab.open_qubits))
+    assert lines[2].split("\t")[0] == tab.bitstring(0)
