@@ -103,13 +103,19 @@ def setup_dist(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # test hook: TNB_SHARE_DEVICE=1 puts every rank on device 0 (gloo), so the
+    # multi-rank choreography can be exercised on a single-GPU box
+    if os.environ.get("TNB_SHARE_DEVICE") == "1":
+        local = 0
     dist = None
     if world > 1:
         import torch
         import torch.distributed as dist_
 
-        torch.cuda.set_device(local)
-        dist_.init_process_group("nccl" if args.impl == "ours" else "gloo")
+        if args.impl == "ours":
+            torch.cuda.set_device(local)
+        backend = os.environ.get("TNB_DIST_BACKEND") or ("nccl" if args.impl == "ours" else "gloo")
+        dist_.init_process_group(backend)
         dist = dist_
     return world, rank, local, dist
 
