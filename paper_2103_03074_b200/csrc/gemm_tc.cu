@@ -82,6 +82,23 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   } while (!ok);
 }
 
+// same, with a suspend-time hint: the waiting warp sleeps in hardware until
+// the phase completes instead of re-polling (used for the long waits of the
+// epilogue warps, which would otherwise keep issuing while the MMAs run)
+__device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity) {
+  const uint32_t addr = smem_u32(bar);
+  uint32_t ok = 0;
+  do {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(ok)
+        : "r"(addr), "r"(parity), "r"(0x989680u)
+        : "memory");
+  } while (!ok);
+}
+
 __device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
                "r"(bytes)
@@ -311,7 +328,7 @@ gemm_f16x3_kernel(const __grid_constant__ CUtensorMap tm_ahi, const __grid_const
           }
         }
         if (lane == 0) {
-          mbar_wait(&empty_bar[stage], phase ^ 1);
+          mbar_wait_sleep(&empty_bar[stage], phase ^ 1);
           uint8_t* st = smem + stage * CF::STAGE_BYTES;
           if (leader) mbar_arrive_expect_tx(&full_bar[stage], CG * CF::STAGE_BYTES);
           else mbar_arrive_remote(&full_bar[stage], 0);
@@ -337,12 +354,12 @@ gemm_f16x3_kernel(const __grid_constant__ CUtensorMap tm_ahi, const __grid_const
         const int nkb = (min(Kp, k_begin + k_per_split) - k_begin + BK - 1) / BK;
         for (int c0 = 0; c0 < nkb; c0 += chunk_kb, ++gchunk) {
           const int buf = gchunk & 1;
-          mbar_wait(&pempty_bar[buf], ((gchunk >> 1) & 1) ^ 1);
+          mbar_wait_sleep(&pempty_bar[buf], ((gchunk >> 1) & 1) ^ 1);
           tc_fence_after();
           const uint32_t tmem_c = tmem_base + buf * BN;
           const int c1 = min(nkb, c0 + chunk_kb);
           for (int kb = c0; kb < c1; ++kb) {
-            mbar_wait(&full_bar[stage], phase);
+            mbar_wait_sleep(&full_bar[stage], phase);
             tc_fence_after();
             if (lane == 0) {
               uint8_t* st = smem + stage * CF::STAGE_BYTES;
@@ -383,7 +400,7 @@ gemm_f16x3_kernel(const __grid_constant__ CUtensorMap tm_ahi, const __grid_const
       for (int j = 0; j < EPI_COLS; ++j) acc[j] = 0.f;
       for (int c0 = 0; c0 < nkb; c0 += chunk_kb, ++gchunk) {
         const int buf = gchunk & 1;
-        mbar_wait(&pfull_bar[buf], (gchunk >> 1) & 1);
+        mbar_wait_sleep(&pfull_bar[buf], (gchunk >> 1) & 1);
         tc_fence_after();
         const uint32_t taddr = tmem_base + ((uint32_t)(q * 32) << 16) + buf * BN + grp * EPI_COLS;
 #pragma unroll
