@@ -143,6 +143,51 @@ contract_simt_kernel(const T* __restrict__ A, const T* __restrict__ B, T* __rest
 }
 
 // ---------------------------------------------------------------------------
+// Small-K contraction (outer-product-like steps, K <= 8, big outputs): each
+// thread produces 4 consecutive output columns of one row with two 16-byte
+// (float2) or four 16-byte (double2) stores, so the kernel runs at HBM write
+// speed instead of the 32x32-tile kernel's padded K loop.
+template <typename T>
+__global__ void __launch_bounds__(256)
+contract_smallk_kernel(const T* __restrict__ A, const T* __restrict__ B, T* __restrict__ C,
+                       int64_t M, int64_t N, int K, const ByteLut* __restrict__ gla,
+                       const ByteLut* __restrict__ glb, unsigned int* __restrict__ max_out) {
+  using S = typename Scalar<T>::type;
+  __shared__ uint32_t la[4][256];
+  __shared__ uint32_t lb[4][256];
+  for (int i = threadIdx.x; i < 1024; i += 256) {
+    la[i >> 8][i & 255] = gla->t[i >> 8][i & 255];
+    lb[i >> 8][i & 255] = glb->t[i >> 8][i & 255];
+  }
+  __syncthreads();
+  const int64_t nq = N >> 2;
+  const int64_t total = M * nq;
+  float vmax = 0.f;
+  for (int64_t idx = (int64_t)blockIdx.x * 256 + threadIdx.x; idx < total;
+       idx += (int64_t)gridDim.x * 256) {
+    const int64_t m = idx / nq, n0 = (idx - m * nq) << 2;
+    S re[4] = {0, 0, 0, 0}, im[4] = {0, 0, 0, 0};
+    for (int k = 0; k < K; ++k) {
+      const T a = A[lut_map(la, (uint32_t)(m * K + k))];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const T b = B[lut_map(lb, (uint32_t)((n0 + j) * K + k))];
+        re[j] += a.x * b.x - a.y * b.y;
+        im[j] += a.x * b.y + a.y * b.x;
+      }
+    }
+    T* dst = C + m * N + n0;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      T v; v.x = re[j]; v.y = im[j];
+      dst[j] = v;
+      vmax = fmaxf(vmax, (float)fmax(fabs(v.x), fabs(v.y)));
+    }
+  }
+  if (max_out) block_max_atomic(vmax, max_out);
+}
+
+// ---------------------------------------------------------------------------
 // K4: bit permutation out[j] = in[lut(j)].
 template <typename T>
 __global__ void permute_kernel(const T* __restrict__ in, T* __restrict__ out, int64_t elems,
@@ -334,6 +379,13 @@ template <typename T>
 void launch_contract_simt(const T* A, const T* B, T* C, int64_t M, int64_t N, int64_t K,
                           const ByteLut* lutA, const ByteLut* lutB, unsigned int* max_out,
                           cudaStream_t s) {
+  if (K <= 8 && N >= 4 && M * N >= (1 << 16)) {
+    // outer-product-like: stream the output
+    contract_smallk_kernel<T><<<grid_for(M * (N >> 2), 256), 256, 0, s>>>(A, B, C, M, N, (int)K, lutA,
+                                                                            lutB, max_out);
+    check_launch("contract_smallk");
+    return;
+  }
   const int64_t blocks = ((M + 31) / 32) * ((N + 31) / 32);
   if (blocks > 0x7fffffffll) throw Error(TNB_ERR_SHAPE, "SIMT contraction too large");
   contract_simt_kernel<T><<<(unsigned)blocks, 256, 0, s>>>(A, B, C, M, N, K, lutA, lutB, max_out);
