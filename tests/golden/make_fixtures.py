@@ -118,6 +118,17 @@ CONFIGS = {
     # C4: m=20, n2=20, seed 0 / restarts 16 / t=2^30  (bench workload)
     "c4": (lambda: tsyc.sycamore_circuit(20, seed=0),
            sorted(tsyc.OPEN_QUBITS_M20)[:20], 0, 16, 30),
+    # C5: the C4 tree re-sliced at other space targets (sliced-edge sweep,
+    # SURVEY 8(d)): t=26/28/32 -> n_e 63/58/48
+    "c5_26": (lambda: tsyc.sycamore_circuit(20, seed=0),
+              sorted(tsyc.OPEN_QUBITS_M20)[:20], 0, 16, 26),
+    "c5_28": (lambda: tsyc.sycamore_circuit(20, seed=0),
+              sorted(tsyc.OPEN_QUBITS_M20)[:20], 0, 16, 28),
+    "c5_32": (lambda: tsyc.sycamore_circuit(20, seed=0),
+              sorted(tsyc.OPEN_QUBITS_M20)[:20], 0, 16, 32),
+    # C5 batch-size axis: 2^21 correlated bitstrings (all OPEN_QUBITS_M20), t=30
+    "c5_n21": (lambda: tsyc.sycamore_circuit(20, seed=0),
+               sorted(tsyc.OPEN_QUBITS_M20)[:21], 0, 16, 30),
 }
 
 

@@ -1,0 +1,49 @@
+"""Further BASELINE configs on the GPU: C3 (m=14, 2^16 bitstrings, t=2^30) and
+the C5 sweep point t=2^26 (n_e=63) -- needs a B200."""
+
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+import paper_2103_03074_b200 as tnb
+from conftest import golden, rel_l2
+from oracle import engine_np as O
+
+pytestmark = pytest.mark.gpu
+
+TOL = 1e-4
+
+
+@pytest.mark.parametrize("name,rng_", [("c3", (0, 1)), ("c5_26", (0, 2))])
+def test_config_head_tail_xeb_vs_reference(gpu, workloads, name, rng_):
+    w = workloads(name)
+    g = golden(name)
+    a, b = rng_
+    st = tnb.EngineStats()
+    hv = tnb.compute_head_vector(w.tn, w.tree, w.sliced, None, slice_range=rng_,
+                                 precision="single", stats=st)
+    key = f"head_single_{a}_{b}"
+    stride = int(g["stride"])
+    assert rel_l2(hv.data[::stride], g[key + "_sub"]) < TOL
+    assert abs(float(np.vdot(hv.data, hv.data).real) / float(g[key + "_norm2"]) - 1) < 2 * TOL
+    # exact reference counters (engine.py:138-140)
+    assert [st.multiplications, st.head_contractions] == [int(g[key + "_stats"][0]),
+                                                          int(g[key + "_stats"][1])]
+    tab = tnb.tail_amplitudes_unchecked(w.tn, w.tree, hv, precision="single")
+    s2 = int(g["amps_stride"])
+    assert rel_l2(tab.amplitudes[::s2], g["amps_sub"]) < TOL
+    probs = np.abs(tab.amplitudes.astype(np.complex128)) ** 2
+    f_ref = (2.0 ** 53 / probs.size) * float(g["amps_probsum"]) - 1.0
+    assert abs(O.xeb(probs, 53) - f_ref) < 1e-3
+
+
+def test_n_e_63_mask_bits(gpu, workloads):
+    """63 sliced edges: masks near 2^63 address the top mask bits correctly."""
+    w = workloads("c5_26")
+    assert w.n_e == 63
+    top = (1 << 63) - 2
+    hv = tnb.compute_head_vector(w.tn, w.tree, w.sliced, None, slice_range=(top, top + 2),
+                                 precision="single")
+    assert hv.slice_range == (top, top + 2)
+    assert np.isfinite(hv.data).all() and np.abs(hv.data).max() > 0

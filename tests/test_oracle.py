@@ -103,12 +103,18 @@ def test_s8_tail_formulations_agree(workloads):
     assert rel_l2(a, g["amps_absorbed"]) < 1e-12    # vs reference greedy+contract_tree
 
 
-@pytest.mark.parametrize("name", ["m12", "c2", "c4"])
-def test_large_config_goldens_consistent(workloads, name):
+@pytest.mark.parametrize("name,nslices", [("m12", 1), ("c2", 1), ("c3", 1), ("c4", 1),
+                                          ("c5_26", 2)])
+def test_large_config_goldens_consistent(workloads, name, nslices):
     """The big-config goldens exist and carry the reference's stats contract:
     multiplications per slice == the order file's per-subtask tc."""
     w = workloads(name)
     g = golden(name)
-    st = g["head_single_0_1_stats"]
-    assert int(st[0]) == w.tc_per_slice
-    assert int(st[1]) == 1
+    st = g[f"head_single_0_{nslices}_stats"]
+    assert int(st[0]) == nslices * w.tc_per_slice
+    assert int(st[1]) == nslices
+
+
+def test_sweep_plans_match_survey(workloads):
+    """C5: the C4 tree re-sliced at t = 26/28/30/32 gives n_e 63/58/53/48."""
+    assert [workloads(n).n_e for n in ("c5_26", "c5_28", "c4", "c5_32")] == [63, 58, 53, 48]
