@@ -110,6 +110,7 @@ struct StepRec {
   std::vector<int> canon_rows, canon_cols;  // TC: canonical bit -> source bit
   int st_rows = -1, st_cols = -1;           // TC: indices into Program::stages
   double mults = 0;
+  int64_t scratch_off = 0, scratch_bytes = 0;  // TC: staging region in the arena (bytes)
   TcGemmPlan tc;
 };
 
@@ -428,9 +429,13 @@ Program* program_create(const tnb_program_desc* d) {
       o.off = arena.alloc(o.elems * (int64_t)P->esize) / (int64_t)P->esize;
     }
     if (s.kind == KIND_TC) {
+      // operand staging (+ split-K workspace) lives in the arena for the
+      // duration of this step only: it shares memory with dead tensors
       const int64_t Kp = 2 * s.K, Np = 2 * s.N;
       int64_t need = 2 * s.M * Kp * 2 + 2 * Np * Kp * 2;  // hi+lo for both operands (fp16)
       need = align_up(need, kAlign) + tc_workspace_elems(s.M, Np, Kp, P->num_sms) * 4;
+      s.scratch_off = arena.alloc(need);
+      s.scratch_bytes = need;
       scratch_bytes = std::max(scratch_bytes, need);
     }
     // variant operands whose last use is this step are released after it
@@ -438,6 +443,7 @@ Program* program_create(const tnb_program_desc* d) {
       TensorRec& r = P->tensors[t];
       if (r.pool == POOL_ARENA) arena.release(r.off * (int64_t)P->esize, r.elems * (int64_t)P->esize);
     }
+    if (s.kind == KIND_TC) arena.release(s.scratch_off, s.scratch_bytes);
   }
   P->persist_elems = persist_off;
   P->arena_bytes = arena.top;
@@ -452,7 +458,6 @@ Program* program_create(const tnb_program_desc* d) {
   dmalloc(&P->d_slice_pool, P->slice_pool_elems * (int64_t)P->esize);
   dmalloc(&P->d_persist, P->persist_elems * (int64_t)P->esize);
   dmalloc(&P->d_arena, P->arena_bytes);
-  dmalloc(&P->d_scratch, P->scratch_bytes);
   dmalloc((void**)&P->d_luts, (int64_t)P->luts.size() * sizeof(ByteLut));
   TNB_CUDA(cudaMemcpy(P->d_luts, P->luts.data(), P->luts.size() * sizeof(ByteLut), cudaMemcpyHostToDevice));
   P->n_sl_descs = (int)sl_descs.size();
@@ -528,7 +533,7 @@ Program* program_create(const tnb_program_desc* d) {
   for (auto& s : P->steps) {
     if (s.kind != KIND_TC) continue;
     const int64_t Kp = 2 * s.K, Np = 2 * s.N;
-    char* base = (char*)P->d_scratch;
+    char* base = (char*)P->d_arena + s.scratch_off;
     __half* ahi = (__half*)base;
     __half* alo = ahi + s.M * Kp;
     __half* bhi = alo + s.M * Kp;
@@ -669,7 +674,7 @@ void exec_step(Program* P, StepRec& s) {
     const int64_t Kp = 2 * s.K, Np = 2 * s.N;
     const float2* rows = (const float2*)P->tensor_ptr(s.rows_t);
     const float2* cols = (const float2*)P->tensor_ptr(s.cols_t);
-    char* base = (char*)P->d_scratch;
+    char* base = (char*)P->d_arena + s.scratch_off;
     __half* ahi = (__half*)base;
     __half* alo = ahi + s.M * Kp;
     __half* bhi = alo + s.M * Kp;
