@@ -148,7 +148,7 @@ def make_golden(name):
             out[f"head_single_{a}_{b}_stats"] = np.array([st.multiplications, st.head_contractions,
                                                           0, st.steps_executed])
             out[f"head_single_{a}_{b}_cpu_s"] = np.array(dt)
-            if name == "s8":
+            if name in ("s8", "m12"):
                 pd = tengine.compute_head_vector(tn, tree, sliced, None, slice_range=(a, b),
                                                  precision="double", mode="fixed")
                 out[f"head_double_{a}_{b}_sub"], out[f"head_double_{a}_{b}_norm2"] = sub(pd.data, stride)
