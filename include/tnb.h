@@ -91,7 +91,7 @@ typedef struct {
   double tc_flops_per_slice;    /* part of the above on the tensor-core path        */
   int64_t arena_bytes;          /* slice-variant intermediates                      */
   int64_t persistent_bytes;     /* leaves + hoisted slice-invariant results         */
-  int64_t scratch_bytes;        /* GEMM operand staging                             */
+  int64_t scratch_bytes;        /* largest per-step GEMM operand staging (in arena) */
   int32_t n_steps_tc;           /* steps on the tcgen05 path                        */
   int32_t n_steps_simt;         /* steps on the SIMT path                           */
   int32_t n_steps_hoisted;      /* slice-invariant steps computed once              */

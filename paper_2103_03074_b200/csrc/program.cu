@@ -12,7 +12,8 @@
 //     canonical-layout byte LUTs, and -- for the tensor-core path -- the
 //     operand roles (smaller operand is expanded) and TMA descriptors;
 //   * a first-fit arena for slice-variant intermediates (liveness in step
-//     order) and one scratch region for GEMM operand staging.
+//     order) that also holds each tensor-core step's operand staging for the
+//     duration of that step.
 // Execution of a slice range follows compute_head_vector's loop
 // (engine.py:275-298) with the binary-counter fixed-mode sum
 // (engine.py:207-222) or the free running sum.
@@ -141,7 +142,7 @@ struct Program {
   void* d_slice_pool = nullptr;  int64_t slice_pool_elems = 0;
   void* d_persist = nullptr;     int64_t persist_elems = 0;
   void* d_arena = nullptr;       int64_t arena_bytes = 0;
-  void* d_scratch = nullptr;     int64_t scratch_bytes = 0;
+  int64_t scratch_bytes = 0;     // largest per-step staging region (inside the arena)
   ByteLut* d_luts = nullptr;
   SlicedLeafDesc* d_sl_descs = nullptr; int n_sl_descs = 0;
   uint32_t* d_keep = nullptr;
@@ -169,7 +170,7 @@ struct Program {
 
   ~Program() {
     if (device >= 0) cudaSetDevice(device);
-    void* ptrs[] = {d_leaf_pool, d_slice_pool, d_persist, d_arena, d_scratch, d_luts,
+    void* ptrs[] = {d_leaf_pool, d_slice_pool, d_persist, d_arena, d_luts,
                     d_sl_descs, d_keep, d_tmax, d_acc, d_stage_u32, d_stage_luts, d_progress};
     for (void* p : ptrs)
       if (p) cudaFree(p);
