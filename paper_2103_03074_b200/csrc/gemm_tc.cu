@@ -510,10 +510,13 @@ int choose_splits(int64_t M, int64_t Np, int64_t Kp, int num_sms) {
   const int64_t units = num_sms / cg;
   const int64_t tiles = ((M + BM * cg - 1) / (BM * cg)) * ((Np + BN - 1) / BN);
   const int64_t kblocks = (Kp + BK - 1) / BK;
-  int s = 1;
-  // split K while tiles leave SMs idle and every split keeps >= 16 K blocks
-  while (tiles * s * 2 <= units && kblocks / (s * 2) >= 16 && s < 32) s *= 2;
-  return s;
+  // split K when the tiles leave CTA units idle: as many splits as fill the
+  // units (any count, not only powers of two), each keeping >= 16 K blocks
+  if (tiles * 2 > units) return 1;
+  int64_t s = units / tiles;
+  s = std::min<int64_t>(s, kblocks / 16);
+  s = std::min<int64_t>(s, 64);
+  return (int)std::max<int64_t>(s, 1);
 }
 
 }  // namespace
