@@ -129,6 +129,19 @@ def barrier(dist, local):
         torch.cuda.synchronize(local)
 
 
+def traffic_from_profile():
+    """DRAM bytes per GEMM launch from the committed ncu capture of this bench
+    (scripts/gpu_traffic.sh -> profiles/r1/gemm_traffic.json), else null."""
+    path = os.path.join(ROOT, "profiles", "r1", "gemm_traffic.json")
+    try:
+        with open(path) as fh:
+            t = json.load(fh)
+        return {"traffic": t["dram_bytes_per_launch"], "traffic_unit": "bytes/launch (DRAM read+write)",
+                "traffic_source": t["source"]}
+    except Exception:
+        return {"traffic": None}
+
+
 def cpu_baseline(w):
     from oracle.cpu_sample import time_head_slice
 
@@ -315,7 +328,7 @@ def run_ours(args):
             "achieved_is": "algorithmic complex FLOPs (8 per complex multiply-add) per GEMM launch / event time",
             "tensor_tflops_executed": 3.0 * achieved,
             "tensor_frac": 3.0 * achieved / sustained,
-            "traffic": None,
+            **traffic_from_profile(),
         },
         "gpu_launches": launches,
         "device_ms_per_step": {"total": dev_ms / args.steps, "gemm": gemm_ms / args.steps,
