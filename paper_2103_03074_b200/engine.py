@@ -171,7 +171,18 @@ def get_program(leaves, steps, sliced, out_order, precision, device=None, flags=
         if prog is None:
             if len(_cache) >= _CACHE_MAX:
                 _cache.pop(next(iter(_cache)))
-            prog = Program(leaves, steps, sliced, out_order, precision, device, flags)
+            try:
+                prog = Program(leaves, steps, sliced, out_order, precision, device, flags)
+            except RuntimeError as exc:
+                if "out of memory" not in str(exc) or not _cache:
+                    raise
+                # cached programs hold their arenas (tens of GB at 2^30 plans):
+                # evict them and retry once
+                _cache.clear()
+                import gc
+
+                gc.collect()
+                prog = Program(leaves, steps, sliced, out_order, precision, device, flags)
             _cache[key] = prog
         else:
             _cache[key] = _cache.pop(key)  # LRU touch
