@@ -121,6 +121,13 @@ int tnb_program_get_info(const tnb_program* p, tnb_program_info* info);
 
 /* Replace one leaf's values (interleaved complex128 host data, 2^rank). */
 int tnb_program_set_leaf(tnb_program* p, int32_t leaf_pos, const double* data);
+/* Replace n leaves at once: data = their interleaved complex128 values
+   concatenated in the order of `leaf_pos` (one staged upload, one sync). */
+int tnb_program_set_leaves(tnb_program* p, int32_t n, const int32_t* leaf_pos,
+                           const double* data);
+/* Replace one leaf of a single-precision program from HOST complex64
+   (interleaved float) data, no conversion. */
+int tnb_program_set_leaf_c64(tnb_program* p, int32_t leaf_pos, const float* data);
 /* Replace one leaf's values from DEVICE memory already in the program's
    precision (complex64 for single, complex128 for double). */
 int tnb_program_set_leaf_device(tnb_program* p, int32_t leaf_pos, const void* dev_data);

@@ -63,6 +63,8 @@ EXPORTS = {
     "tnb_program_get_info": (i32, [P, C.POINTER(ProgramInfo)]),
     "tnb_program_set_leaf": (i32, [P, i32, C.POINTER(f64)]),
     "tnb_program_set_leaf_device": (i32, [P, i32, P]),
+    "tnb_program_set_leaves": (i32, [P, i32, C.POINTER(i32), C.POINTER(f64)]),
+    "tnb_program_set_leaf_c64": (i32, [P, i32, C.POINTER(C.c_float)]),
     "tnb_program_run_range": (i32, [P, u64, u64, i32, P, i32]),
     "tnb_program_set_timing": (i32, [P, i32]),
     "tnb_program_get_timing": (i32, [P, C.POINTER(Timing)]),

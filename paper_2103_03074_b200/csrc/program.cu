@@ -612,6 +612,79 @@ void program_set_leaf(Program* P, int leaf_pos, const double* data) {
   P->invariant_valid = false;
 }
 
+// Batched repin: one staged host buffer, contiguous runs of leaves coalesced
+// into single copies, leaf max slots uploaded in one copy, one sync.
+void program_set_leaves(Program* P, int n, const int32_t* pos, const double* data) {
+  const int nl = (int)P->leaf_ranks.size();
+  TNB_CUDA(cudaSetDevice(P->device));
+  std::vector<char> host;
+  struct Run { int64_t dst_elem, n_elem; size_t host_off; };
+  std::vector<Run> runs;
+  std::vector<unsigned int> maxbits(nl, 0);
+  int lo = nl, hi = -1;
+  const double* src = data;
+  for (int i = 0; i < n; ++i) {
+    const int p = pos[i];
+    if (p < 0 || p >= nl) throw Error(TNB_ERR_ARG, "leaf index out of range");
+    const int64_t ne = (int64_t)1 << P->leaf_ranks[p];
+    const size_t off = host.size();
+    host.resize(off + (size_t)ne * P->esize);
+    float m = 0.f;
+    if (P->precision == TNB_SINGLE) {
+      float* h = reinterpret_cast<float*>(host.data() + off);
+      for (int64_t j = 0; j < 2 * ne; ++j) {
+        h[j] = (float)src[j];
+        m = std::max(m, std::fabs(h[j]));
+      }
+    } else {
+      std::memcpy(host.data() + off, src, (size_t)ne * 16);
+    }
+    std::memcpy(&maxbits[p], &m, 4);
+    lo = std::min(lo, p);
+    hi = std::max(hi, p);
+    const int64_t dst = P->leaf_pool_off[p];
+    if (!runs.empty() && runs.back().dst_elem + runs.back().n_elem == dst &&
+        runs.back().host_off + (size_t)runs.back().n_elem * P->esize == off)
+      runs.back().n_elem += ne;
+    else
+      runs.push_back({dst, ne, off});
+    src += 2 * ne;
+  }
+  for (const Run& r : runs)
+    TNB_CUDA(cudaMemcpyAsync((char*)P->d_leaf_pool + (size_t)r.dst_elem * P->esize,
+                             host.data() + r.host_off, (size_t)r.n_elem * P->esize,
+                             cudaMemcpyHostToDevice, P->stream));
+  if (hi >= lo && P->precision == TNB_SINGLE) {
+    // unchanged leaves in [lo, hi] keep their slot: merge with the current values
+    std::vector<unsigned int> cur(hi - lo + 1);
+    TNB_CUDA(cudaMemcpyAsync(cur.data(), P->d_tmax + lo, cur.size() * 4, cudaMemcpyDeviceToHost,
+                             P->stream));
+    TNB_CUDA(cudaStreamSynchronize(P->stream));
+    std::vector<char> touched(nl, 0);
+    for (int i = 0; i < n; ++i) touched[pos[i]] = 1;
+    for (int p = lo; p <= hi; ++p)
+      if (touched[p]) cur[p - lo] = maxbits[p];
+    TNB_CUDA(cudaMemcpyAsync(P->d_tmax + lo, cur.data(), cur.size() * 4, cudaMemcpyHostToDevice,
+                             P->stream));
+    TNB_CUDA(cudaStreamSynchronize(P->stream));
+  } else {
+    TNB_CUDA(cudaStreamSynchronize(P->stream));
+  }
+  P->invariant_valid = false;
+}
+
+void program_set_leaf_c64(Program* P, int leaf_pos, const float* data) {
+  if (leaf_pos < 0 || leaf_pos >= (int)P->leaf_ranks.size()) throw Error(TNB_ERR_ARG, "leaf index out of range");
+  if (P->precision != TNB_SINGLE) throw Error(TNB_ERR_ARG, "complex64 upload needs a single-precision program");
+  TNB_CUDA(cudaSetDevice(P->device));
+  const int64_t n = (int64_t)1 << P->leaf_ranks[leaf_pos];
+  char* dst = (char*)P->d_leaf_pool + (size_t)P->leaf_pool_off[leaf_pos] * P->esize;
+  TNB_CUDA(cudaMemcpyAsync(dst, data, (size_t)n * 8, cudaMemcpyHostToDevice, P->stream));
+  launch_absmax((const float2*)dst, n, P->d_tmax + P->slot[leaf_pos], P->stream);
+  TNB_CUDA(cudaStreamSynchronize(P->stream));
+  P->invariant_valid = false;
+}
+
 void program_set_leaf_device(Program* P, int leaf_pos, const void* dev) {
   if (leaf_pos < 0 || leaf_pos >= (int)P->leaf_ranks.size()) throw Error(TNB_ERR_ARG, "leaf index out of range");
   TNB_CUDA(cudaSetDevice(P->device));

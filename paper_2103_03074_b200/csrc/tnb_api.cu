@@ -15,6 +15,8 @@ void program_destroy(Program* P);
 void program_info(const Program* P, tnb_program_info* info);
 void program_set_leaf(Program* P, int leaf_pos, const double* data);
 void program_set_leaf_device(Program* P, int leaf_pos, const void* dev);
+void program_set_leaves(Program* P, int n, const int32_t* pos, const double* data);
+void program_set_leaf_c64(Program* P, int leaf_pos, const float* data);
 void program_run_range(Program* P, uint64_t a, uint64_t b, int mode, void* out, int out_dev);
 void program_set_timing(Program* P, int on);
 void program_get_timing(const Program* P, tnb_timing* t);
@@ -90,6 +92,20 @@ int tnb_program_set_leaf(tnb_program* p, int32_t leaf_pos, const double* data) {
   return guarded([&] {
     if (!p || !data) throw Error(TNB_ERR_ARG, "null argument");
     program_set_leaf(reinterpret_cast<Program*>(p), leaf_pos, data);
+  });
+}
+
+int tnb_program_set_leaves(tnb_program* p, int32_t n, const int32_t* leaf_pos, const double* data) {
+  return guarded([&] {
+    if (!p || (n > 0 && (!leaf_pos || !data))) throw Error(TNB_ERR_ARG, "null argument");
+    program_set_leaves(reinterpret_cast<Program*>(p), n, leaf_pos, data);
+  });
+}
+
+int tnb_program_set_leaf_c64(tnb_program* p, int32_t leaf_pos, const float* data) {
+  return guarded([&] {
+    if (!p || !data) throw Error(TNB_ERR_ARG, "null argument");
+    program_set_leaf_c64(reinterpret_cast<Program*>(p), leaf_pos, data);
   });
 }
 

@@ -113,15 +113,36 @@ class Program:
                 pass
 
     def update_leaves(self, leaves) -> None:
-        """Upload leaves whose values changed (repin), topology unchanged."""
+        """Upload leaves whose values changed (repin), topology unchanged --
+        one batched, staged upload through tnb_program_set_leaves."""
+        pos_list, datas = [], []
         for nid, _, d in leaves:
             pos = self.leaf_pos[nid]
+            d = np.asarray(d)
+            if d.size >= (1 << 16):
+                # big leaves (the tail's head vector): upload unconditionally,
+                # straight from complex64 when the program is single precision
+                if self.precision == "single" and d.dtype == np.complex64:
+                    buf = np.ascontiguousarray(d).reshape(-1).view(np.float32)
+                    _lib.check(self.lib.tnb_program_set_leaf_c64(
+                        self.handle, pos, buf.ctypes.data_as(C.POINTER(C.c_float))))
+                    self._leaf_data[pos] = None
+                    continue
+            else:
+                old = self._leaf_data[pos]
+                if old is not None and d.size == old.size and np.array_equal(d.reshape(-1), old):
+                    continue
             new = np.ascontiguousarray(d, dtype=np.complex128).reshape(-1)
-            if not np.array_equal(new, self._leaf_data[pos]):
-                buf = new.view(np.float64)
-                _lib.check(self.lib.tnb_program_set_leaf(
-                    self.handle, pos, buf.ctypes.data_as(C.POINTER(C.c_double))))
-                self._leaf_data[pos] = new
+            pos_list.append(pos)
+            datas.append(new)
+            self._leaf_data[pos] = new
+        if not pos_list:
+            return
+        posv = np.asarray(pos_list, dtype=np.int32)
+        flat = np.concatenate(datas).view(np.float64)
+        _lib.check(self.lib.tnb_program_set_leaves(
+            self.handle, len(pos_list), posv.ctypes.data_as(C.POINTER(C.c_int32)),
+            flat.ctypes.data_as(C.POINTER(C.c_double))))
 
     def set_leaf_device(self, pos: int, dev_ptr: int) -> None:
         _lib.check(self.lib.tnb_program_set_leaf_device(self.handle, pos, C.c_void_p(dev_ptr)))

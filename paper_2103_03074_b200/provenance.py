@@ -8,6 +8,7 @@ import at run time; tests check both against the reference here.
 from __future__ import annotations
 
 import hashlib
+import weakref
 import json
 
 from .errors import ProvenanceMismatch
@@ -23,9 +24,29 @@ def circuit_sha(tn) -> str:
     return tn.circuit.sha256() if getattr(tn, "circuit", None) is not None else "none"
 
 
+_order_cache: dict = {}
+
+
 def order_sha256(tree, tn, sliced_indices) -> str:
-    doc = tree_to_doc(tree, circuit_sha256=circuit_sha(tn), slices=list(sliced_indices))
-    return hashlib.sha256(dumps_order(doc).encode()).hexdigest()
+    """sha256 of the canonical order document; memoised per tree object
+    (serialising ~800 steps costs milliseconds per engine call)."""
+    csha = circuit_sha(tn)
+    sl = tuple(sliced_indices)
+    ann = getattr(tree, "annotations", None)
+    fp = (len(tree.steps), tree.first_cut, id(tree.steps), id(ann), len(ann or ()), csha, sl,
+          getattr(tree, "seed", None))
+    hit = _order_cache.get(id(tree))
+    if hit is not None and hit[0]() is tree and hit[1] == fp:
+        return hit[2]
+    doc = tree_to_doc(tree, circuit_sha256=csha, slices=list(sl))
+    digest = hashlib.sha256(dumps_order(doc).encode()).hexdigest()
+    try:
+        if len(_order_cache) > 64:
+            _order_cache.clear()
+        _order_cache[id(tree)] = (weakref.ref(tree), fp, digest)
+    except TypeError:  # not weak-referenceable: no memo
+        pass
+    return digest
 
 
 def provenance_hash(tn, tree, s1: dict, precision: str, mode: str, sliced_indices=()) -> str:
