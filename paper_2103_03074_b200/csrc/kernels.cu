@@ -466,6 +466,11 @@ void build_stage_tables(const std::vector<int>& canon_to_src, int64_t K, StageHo
     for (int u = 0; u < nU; ++u) if ((t >> u) & 1) d |= 1u << U[u];
     out->t_dst[t] = d;
   }
+  // tile-id bits in canonical (destination) order by default; TNB_STAGE_ORDER=1
+  // orders them by source bit instead (measured: no difference at C4)
+  static const int tile_order = [] { const char* e = getenv("TNB_STAGE_ORDER"); return e ? atoi(e) : 0; }();
+  if (tile_order == 1)
+    std::sort(V.begin(), V.end(), [&](int x, int y) { return canon_to_src[x] < canon_to_src[y]; });
   std::vector<int> vs, vd;
   for (int p : V) { vs.push_back(canon_to_src[p]); vd.push_back(p); }
   build_lut(vs, &out->tile_src);
