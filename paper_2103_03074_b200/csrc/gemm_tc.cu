@@ -119,22 +119,25 @@ __device__ __forceinline__ void mbar_arrive_remote(uint64_t* bar, uint32_t rank)
       : "memory");
 }
 
+// Operands are K-blocked ([Kp/BK][rows][BK], see kKBlockLog): 3-D maps
+// {BK, rows, K blocks}; a box {BK, rows, 1} is one contiguous tile.
 template <int CG>
-__device__ __forceinline__ void tma_load_2d(void* smem_dst, const CUtensorMap* map, uint64_t* bar,
-                                            int c0, int c1) {
+__device__ __forceinline__ void tma_load_tile(void* smem_dst, const CUtensorMap* map, uint64_t* bar,
+                                              int row, int kblock) {
   if constexpr (CG == 1) {
     asm volatile(
-        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes"
-        " [%0], [%1, {%3, %4}], [%2];" ::"r"(smem_u32(smem_dst)),
-        "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1)
+        "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%3, %4, %5}], [%2];" ::"r"(smem_u32(smem_dst)),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(0), "r"(row), "r"(kblock)
         : "memory");
   } else {
     // bytes land in this CTA's smem; completion is signalled on the LEADER's
     // barrier (peer bit of the shared::cluster address cleared)
     asm volatile(
-        "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
-        " [%0], [%1, {%3, %4}], [%2];" ::"r"(smem_u32(smem_dst)),
-        "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar) & 0xFEFFFFFFu), "r"(c0), "r"(c1)
+        "cp.async.bulk.tensor.3d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%3, %4, %5}], [%2];" ::"r"(smem_u32(smem_dst)),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar) & 0xFEFFFFFFu), "r"(0), "r"(row),
+        "r"(kblock)
         : "memory");
   }
 }
@@ -332,10 +335,11 @@ gemm_f16x3_kernel(const __grid_constant__ CUtensorMap tm_ahi, const __grid_const
           uint8_t* st = smem + stage * CF::STAGE_BYTES;
           if (leader) mbar_arrive_expect_tx(&full_bar[stage], CG * CF::STAGE_BYTES);
           else mbar_arrive_remote(&full_bar[stage], 0);
-          tma_load_2d<CG>(st, &tm_ahi, &full_bar[stage], k, m0);
-          tma_load_2d<CG>(st + A_TILE, &tm_alo, &full_bar[stage], k, m0);
-          tma_load_2d<CG>(st + 2 * A_TILE, &tm_bhi, &full_bar[stage], k, n0);
-          tma_load_2d<CG>(st + 2 * A_TILE + CF::B_TILE, &tm_blo, &full_bar[stage], k, n0);
+          const int kbk = k / BK;
+          tma_load_tile<CG>(st, &tm_ahi, &full_bar[stage], m0, kbk);
+          tma_load_tile<CG>(st + A_TILE, &tm_alo, &full_bar[stage], m0, kbk);
+          tma_load_tile<CG>(st + 2 * A_TILE, &tm_bhi, &full_bar[stage], n0, kbk);
+          tma_load_tile<CG>(st + 2 * A_TILE + CF::B_TILE, &tm_blo, &full_bar[stage], n0, kbk);
         }
         __syncwarp();
         if (++stage == STAGES) { stage = 0; phase ^= 1; }
@@ -414,14 +418,45 @@ gemm_f16x3_kernel(const __grid_constant__ CUtensorMap tm_ahi, const __grid_const
         if (CG == 1 || leader) mbar_arrive(&pempty_bar[buf]);
         else mbar_arrive_remote(&pempty_bar[buf], 0);
       }
-      const int row = wc.mb * BM * CG + (int)rank * BM + q * 32 + lane;
+      const int row0 = wc.mb * BM * CG + (int)rank * BM + q * 32;
+      const int row = row0 + lane;
       const int col0 = wc.nb * BN + grp * EPI_COLS;
 #pragma unroll
       for (int j = 0; j < EPI_COLS; ++j) {
         acc[j] *= alpha;
         vmax = fmaxf(vmax, fabsf(acc[j]));  // out-of-range rows/cols are TMA zero-fill
       }
-      if (row < M && col0 < Np) {
+      if (row0 + 32 <= M && col0 + EPI_COLS <= Np) {
+        // full 32-row x 64-column block: transpose float4 chunks inside each
+        // 8-lane group (3 xor-butterfly stages) so that every store writes
+        // 4 rows x 128 contiguous bytes instead of 32 rows x 16 bytes
+        const int g8 = lane & 7;
+        float* base = C + (size_t)wc.split * (size_t)M * (size_t)Np + (size_t)(row0 + (lane & ~7)) * Np + col0;
+#pragma unroll
+        for (int b = 0; b < EPI_COLS / 32; ++b) {
+          float* x = acc + b * 32;  // 8 float4 chunks: chunk c = x[4c..4c+3]
+#pragma unroll
+          for (int m = 4; m > 0; m >>= 1) {
+            const bool hi = (g8 & m) != 0;
+#pragma unroll
+            for (int c0 = 0; c0 < 8; ++c0) {
+              if (c0 & m) continue;
+              const int c1 = c0 | m;
+#pragma unroll
+              for (int e = 0; e < 4; ++e) {
+                const float send = hi ? x[4 * c0 + e] : x[4 * c1 + e];
+                const float recv = __shfl_xor_sync(0xffffffffu, send, m);
+                if (hi) x[4 * c0 + e] = recv; else x[4 * c1 + e] = recv;
+              }
+            }
+          }
+          // x chunk s now holds chunk g8 of row (lane & ~7) + s
+#pragma unroll
+          for (int s = 0; s < 8; ++s)
+            *reinterpret_cast<float4*>(base + (size_t)s * Np + b * 32 + 4 * g8) =
+                make_float4(x[4 * s], x[4 * s + 1], x[4 * s + 2], x[4 * s + 3]);
+        }
+      } else if (row < M && col0 < Np) {
         float* dst = C + (size_t)wc.split * (size_t)M * (size_t)Np + (size_t)row * Np + col0;
         if (col0 + EPI_COLS <= Np) {
 #pragma unroll
@@ -482,16 +517,19 @@ int env_int(const char* name, int dflt) {
 void make_map(void* out, const __half* base, int64_t rows, int64_t kp, int box_rows) {
   if ((reinterpret_cast<uintptr_t>(base) & 15) != 0 || (kp % 8) != 0)
     throw Error(TNB_ERR_SHAPE, "tensor-core operand not 16-byte aligned");
-  cuuint64_t dims[2] = {(cuuint64_t)kp, (cuuint64_t)rows};
-  cuuint64_t strides[1] = {(cuuint64_t)kp * 2};
-  cuuint32_t box[2] = {(cuuint32_t)BK, (cuuint32_t)box_rows};
-  cuuint32_t estr[2] = {1, 1};
+  // K-blocked layout [kp/BK][rows][BK] (plain [rows][kp] when kp <= BK)
+  static_assert(BK == 2 << kKBlockLog, "GEMM K block must match the staging block");
+  const int64_t inner = kp < BK ? kp : BK;
+  cuuint64_t dims[3] = {(cuuint64_t)inner, (cuuint64_t)rows, (cuuint64_t)(kp / inner)};
+  cuuint64_t strides[2] = {(cuuint64_t)inner * 2, (cuuint64_t)(inner * 2 * rows)};
+  cuuint32_t box[3] = {(cuuint32_t)BK, (cuuint32_t)box_rows, 1};
+  cuuint32_t estr[3] = {1, 1, 1};
   static const int promo_env = env_int("TNB_L2_PROMO", -1);
   CUtensorMapL2promotion promo = CU_TENSOR_MAP_L2_PROMOTION_L2_256B;
   if (promo_env == 0) promo = CU_TENSOR_MAP_L2_PROMOTION_NONE;
   if (promo_env == 64) promo = CU_TENSOR_MAP_L2_PROMOTION_L2_64B;
   if (promo_env == 128) promo = CU_TENSOR_MAP_L2_PROMOTION_L2_128B;
-  CUresult r = get_encode()(reinterpret_cast<CUtensorMap*>(out), CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2,
+  CUresult r = get_encode()(reinterpret_cast<CUtensorMap*>(out), CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 3,
                             const_cast<__half*>(base), dims, strides, box, estr,
                             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B, promo,
                             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);

@@ -314,8 +314,10 @@ stage_kernel(const float2* __restrict__ src, StageTables tb, int64_t K, int logK
         hi[d] = h;
         lo[d] = o;
       } else {
-        const uint64_t n = d >> logK;
-        const uint64_t r0 = (uint64_t)d + n * (uint64_t)K, r1 = r0 + (uint64_t)K;
+        // d = (k_hi, n, k_lo) with 2^logK = k_lo extent: rows 2n / 2n+1 of
+        // the block are 2^logK apart
+        const uint64_t r0 = (uint64_t)d + (((uint64_t)d >> logK) << logK);
+        const uint64_t r1 = r0 + (1ull << logK);
         __half2 h0, o0, h1, o1;
         split2(x.x * s, -x.y * s, h0, o0);
         split2(x.y * s, x.x * s, h1, o1);
@@ -423,8 +425,19 @@ void launch_absmax(const float2* A, int64_t n, unsigned int* maxbits, cudaStream
   check_launch("absmax");
 }
 
-void build_stage_tables(const std::vector<int>& canon_to_src, int64_t K, StageHost* out) {
-  const int r = (int)canon_to_src.size();
+void build_stage_tables(const std::vector<int>& canon_rowmajor, int64_t K, StageHost* out) {
+  const int r = (int)canon_rowmajor.size();
+  // destination bit order of the K-blocked layout: k_lo, row bits, k_hi
+  int logK = 0;
+  while ((1ll << logK) < K) ++logK;
+  std::vector<int> canon_to_src;
+  if (logK > kKBlockLog) {
+    for (int p = 0; p < kKBlockLog; ++p) canon_to_src.push_back(canon_rowmajor[p]);
+    for (int p = logK; p < r; ++p) canon_to_src.push_back(canon_rowmajor[p]);
+    for (int p = kKBlockLog; p < logK; ++p) canon_to_src.push_back(canon_rowmajor[p]);
+  } else {
+    canon_to_src = canon_rowmajor;
+  }
   const int Ld = std::min(stage_run_bits(), r), Ls = std::min(stage_run_bits(), r);
   std::vector<int> src_to_canon(r, -1);
   for (int p = 0; p < r; ++p) src_to_canon[canon_to_src[p]] = p;
@@ -475,13 +488,13 @@ void build_stage_tables(const std::vector<int>& canon_to_src, int64_t K, StageHo
   for (int p : V) { vs.push_back(canon_to_src[p]); vd.push_back(p); }
   build_lut(vs, &out->tile_src);
   build_lut(vd, &out->tile_dst);
-  (void)K;
 }
 
 void launch_stage(const float2* src, const StageTables& tb, int64_t K, bool expand,
                   const unsigned int* maxbits, __half* hi, __half* lo, cudaStream_t s) {
   int logK = 0;
   while ((1ll << logK) < K) ++logK;
+  if (logK > kKBlockLog) logK = kKBlockLog;  // row length of the K-blocked layout
   const size_t smem = ((size_t)1 << tb.nU) * 8 + (((size_t)1 << tb.nU) / 32 + 1) * 8;
   int64_t g = tb.n_tiles;
   const int64_t cap = (int64_t)kSms * 8;

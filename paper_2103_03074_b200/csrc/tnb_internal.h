@@ -106,6 +106,11 @@ struct StageTables {  // device view
   int nU;
   int64_t n_tiles;
 };
+// Staged operands are K-blocked: [K / 2^kKBlockLog][rows][2^kKBlockLog]
+// complex elements (one GEMM K block = 32 fp16 = 64 B per row), so every
+// TMA box of the GEMM is one contiguous 8 KB read.  When K <= 2^kKBlockLog
+// this is plain row-major [rows][K].
+constexpr int kKBlockLog = 4;
 // canon_to_src[p] = source bit of canonical (row*K + k) bit p
 void build_stage_tables(const std::vector<int>& canon_to_src, int64_t K, StageHost* out);
 void launch_stage(const float2* src, const StageTables& tb, int64_t K, bool expand,

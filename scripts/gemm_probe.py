@@ -83,10 +83,40 @@ def perf_sweep():
             del p
 
 
+def shape_sweep(specs):
+    """`ma,nb,kb` triples (log2 sizes): GEMM time, accuracy vs a complex128 check."""
+    rng = np.random.default_rng(2)
+    for spec in specs:
+        ma, nb, kb = (int(x) for x in spec.split(","))
+        leaves, steps, out, A, B = two_leaf(ma, nb, kb, rng, tiled=True)
+        p = Program(leaves, steps, [], out, "single", 0)
+        p.set_timing(True)
+        res = p.run_range(0, 1)
+        best = None
+        for _ in range(4):
+            p.update_leaves([(0, leaves[0][1], leaves[0][2] * (1.0 + 1e-7 * np.random.rand()))])
+            p.run_range(0, 1)
+            t = p.timing()
+            best = t if best is None or t["gemm_ms"] < best["gemm_ms"] else best
+        # accuracy on a sample of output rows (full reference would be too slow)
+        Am, Bm = A.reshape(1 << ma, 1 << kb), B.reshape(1 << kb, 1 << nb)
+        rows = np.arange(0, 1 << ma, max(1, (1 << ma) // 8))
+        ref = Am[rows] @ Bm
+        got = np.asarray(res).reshape(1 << ma, 1 << nb)[rows]
+        fl = 8.0 * 2.0 ** (ma + nb + kb)
+        print(f"M=2^{ma} N=2^{nb} K=2^{kb}: gemm {best['gemm_ms']:.3f} ms "
+              f"({best['gemm_launches']} launches) -> {fl / best['gemm_ms'] / 1e9:.1f} TFLOP/s "
+              f"complex-alg, convert {best['convert_ms']:.3f} ms, rel err {rel(got, ref):.2e}",
+              flush=True)
+        del p, res
+
+
 if __name__ == "__main__":
     t = time.time()
     if sys.argv[1] == "acc":
         acc_sweep()
+    elif sys.argv[1] == "shapes":
+        shape_sweep(sys.argv[2:])
     else:
         perf_sweep()
     print(f"done in {time.time() - t:.1f}s")
