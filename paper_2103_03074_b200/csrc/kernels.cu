@@ -329,6 +329,84 @@ stage_kernel(const float2* __restrict__ src, StageTables tb, int64_t K, int logK
   }
 }
 
+__device__ __forceinline__ void cp_async8(void* smem_dst, const void* gsrc) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(
+                   static_cast<uint32_t>(__cvta_generic_to_shared(smem_dst))),
+               "l"(gsrc)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait1() { asm volatile("cp.async.wait_group 1;" ::: "memory"); }
+
+// Same tiles as stage_kernel, with the gather of tile T+1 (cp.async, source
+// order, into the second shared buffer) in flight while tile T is split and
+// written: the HBM reads no longer wait behind each tile's write phase.
+template <bool kExpand, int EPT>
+__global__ void __launch_bounds__(256)
+stage_async_kernel(const float2* __restrict__ src, StageTables tb, int logK,
+                   const unsigned int* __restrict__ maxbits, __half2* __restrict__ hi,
+                   __half2* __restrict__ lo) {
+  extern __shared__ float2 tile[];  // two padded buffers
+  __shared__ uint32_t ls[4][256];
+  __shared__ uint32_t ld[4][256];
+  for (int i = threadIdx.x; i < 1024; i += blockDim.x) {
+    ls[i >> 8][i & 255] = tb.tile_src->t[i >> 8][i & 255];
+    ld[i >> 8][i & 255] = tb.tile_dst->t[i >> 8][i & 255];
+  }
+  const int tsize = 1 << tb.nU;
+  const int bstride = tsize + (tsize >> 5) + 1;
+  uint32_t tt[EPT], so[EPT];
+#pragma unroll
+  for (int j = 0; j < EPT; ++j) {
+    const int i = threadIdx.x + 256 * j;
+    tt[j] = i < tsize ? __ldg(tb.rd_t + i) : 0u;
+    so[j] = i < tsize ? __ldg(tb.rd_src + i) : 0u;
+  }
+  const float s = scale_from_bits(*maxbits);
+  __syncthreads();
+  auto gather = [&](int64_t T, int buf) {
+    const float2* sb = src + lut_map(ls, (uint32_t)T);
+    float2* tb_ = tile + buf * bstride;
+#pragma unroll
+    for (int j = 0; j < EPT; ++j)
+      if (threadIdx.x + 256 * j < tsize) cp_async8(tb_ + tt[j] + (tt[j] >> 5), sb + so[j]);
+  };
+  int buf = 0;
+  if ((int64_t)blockIdx.x < tb.n_tiles) gather(blockIdx.x, 0);
+  cp_async_commit();
+  for (int64_t T = blockIdx.x; T < tb.n_tiles; T += gridDim.x, buf ^= 1) {
+    const int64_t Tn = T + gridDim.x;
+    if (Tn < tb.n_tiles) gather(Tn, buf ^ 1);
+    cp_async_commit();
+    cp_async_wait1();  // this thread's copies of tile T have landed
+    __syncthreads();   // ... and everyone else's
+    const float2* tl = tile + buf * bstride;
+    const uint32_t dbase = lut_map(ld, (uint32_t)T);
+#pragma unroll
+    for (int j = 0; j < EPT; ++j) {
+      const int t = threadIdx.x + 256 * j;
+      if (t >= tsize) break;
+      const float2 x = tl[t + (t >> 5)];
+      const uint32_t d = dbase + __ldg(tb.t_dst + t);
+      if (!kExpand) {
+        __half2 h, o;
+        split2(x.x * s, x.y * s, h, o);
+        hi[d] = h;
+        lo[d] = o;
+      } else {
+        const uint64_t r0 = (uint64_t)d + (((uint64_t)d >> logK) << logK);
+        const uint64_t r1 = r0 + (1ull << logK);
+        __half2 h0, o0, h1, o1;
+        split2(x.x * s, -x.y * s, h0, o0);
+        split2(x.y * s, x.x * s, h1, o1);
+        hi[r0] = h0; lo[r0] = o0;
+        hi[r1] = h1; lo[r1] = o1;
+      }
+    }
+    __syncthreads();  // buffer `buf` is refilled by the next iteration's gather
+  }
+}
+
 __global__ void splitk_reduce_kernel(const float* __restrict__ ws, int splits, int64_t elems,
                                      float* __restrict__ C, const unsigned int* __restrict__ max_rows,
                                      const unsigned int* __restrict__ max_cols,
@@ -500,9 +578,27 @@ void launch_stage(const float2* src, const StageTables& tb, int64_t K, bool expa
   const int64_t cap = (int64_t)kSms * 8;
   if (g > cap) g = cap;
   const int ept = (1 << tb.nU) <= 256 ? 1 : (1 << tb.nU) / 256;
+  static const int async = [] { const char* e = getenv("TNB_STAGE_ASYNC"); return e ? atoi(e) : 1; }();
   auto go = [&](auto kexp, auto kept) {
-    stage_kernel<decltype(kexp)::value, decltype(kept)::value><<<(unsigned)g, 256, smem, s>>>(
-        src, tb, K, logK, maxbits, reinterpret_cast<__half2*>(hi), reinterpret_cast<__half2*>(lo));
+    constexpr bool kE = decltype(kexp)::value;
+    constexpr int kP = decltype(kept)::value;
+    auto kern = stage_async_kernel<kE, kP>;
+    const size_t smem2 = 2 * smem;
+    int per_sm = 0;
+    if (async) {
+      if (smem2 > 48 * 1024)
+        TNB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem2));
+      TNB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 256, smem2));
+    }
+    // persistent grid of resident blocks, each looping (and prefetching) over tiles
+    const int64_t g2 = (int64_t)kSms * per_sm;
+    if (per_sm > 0 && tb.n_tiles > 2 * g2) {
+      kern<<<(unsigned)g2, 256, smem2, s>>>(src, tb, logK, maxbits, reinterpret_cast<__half2*>(hi),
+                                           reinterpret_cast<__half2*>(lo));
+    } else {
+      stage_kernel<kE, kP><<<(unsigned)g, 256, smem, s>>>(
+          src, tb, K, logK, maxbits, reinterpret_cast<__half2*>(hi), reinterpret_cast<__half2*>(lo));
+    }
   };
   using T_ = std::true_type;
   using F_ = std::false_type;
