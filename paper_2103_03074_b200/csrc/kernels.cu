@@ -338,38 +338,51 @@ __device__ __forceinline__ void cp_async8(void* smem_dst, const void* gsrc) {
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 __device__ __forceinline__ void cp_async_wait1() { asm volatile("cp.async.wait_group 1;" ::: "memory"); }
 
-// Same tiles as stage_kernel, with the gather of tile T+1 (cp.async, source
-// order, into the second shared buffer) in flight while tile T is split and
-// written: the HBM reads no longer wait behind each tile's write phase.
+// Same tiles as stage_kernel (tile = 2^nU >= 1024 elements here), with
+//  * the gather of tile T+1 (cp.async, source order, into the second shared
+//    buffer) in flight while tile T is split and written, so the HBM reads
+//    no longer wait behind each tile's write phase;
+//  * all per-element tables in registers (a thread's slots are the same in
+//    every tile);
+//  * 4 consecutive tile elements per thread in the write phase: the low 5
+//    tile bits are the low 5 destination bits, so they land on 4 contiguous
+//    destination slots (16-B stores).
+// Shared layout: 2 pad elements per 32 keep each 4-group 16-B aligned.
+constexpr int kAsyncPad = 2;
 template <bool kExpand, int EPT>
 __global__ void __launch_bounds__(256)
 stage_async_kernel(const float2* __restrict__ src, StageTables tb, int logK,
                    const unsigned int* __restrict__ maxbits, __half2* __restrict__ hi,
                    __half2* __restrict__ lo) {
-  extern __shared__ float2 tile[];  // two padded buffers
+  static_assert(EPT % 4 == 0, "4 elements per write group");
+  constexpr int G = EPT / 4;  // write groups per thread
+  extern __shared__ float4 tile4[];  // two padded buffers (float2 units below)
+  float2* tile = reinterpret_cast<float2*>(tile4);
   __shared__ uint32_t ls[4][256];
   __shared__ uint32_t ld[4][256];
   for (int i = threadIdx.x; i < 1024; i += blockDim.x) {
     ls[i >> 8][i & 255] = tb.tile_src->t[i >> 8][i & 255];
     ld[i >> 8][i & 255] = tb.tile_dst->t[i >> 8][i & 255];
   }
-  const int tsize = 1 << tb.nU;
-  const int bstride = tsize + (tsize >> 5) + 1;
-  uint32_t tt[EPT], so[EPT];
+  const int tsize = 1 << tb.nU;  // == 256 * EPT
+  const int bstride = tsize + kAsyncPad * (tsize >> 5);
+  uint32_t tt[EPT], so[EPT], dq[G];
 #pragma unroll
   for (int j = 0; j < EPT; ++j) {
     const int i = threadIdx.x + 256 * j;
-    tt[j] = i < tsize ? __ldg(tb.rd_t + i) : 0u;
-    so[j] = i < tsize ? __ldg(tb.rd_src + i) : 0u;
+    const uint32_t t = __ldg(tb.rd_t + i);
+    tt[j] = t + kAsyncPad * (t >> 5);
+    so[j] = __ldg(tb.rd_src + i);
   }
+#pragma unroll
+  for (int g = 0; g < G; ++g) dq[g] = __ldg(tb.t_dst + 4 * (threadIdx.x + 256 * g));
   const float s = scale_from_bits(*maxbits);
   __syncthreads();
   auto gather = [&](int64_t T, int buf) {
     const float2* sb = src + lut_map(ls, (uint32_t)T);
     float2* tb_ = tile + buf * bstride;
 #pragma unroll
-    for (int j = 0; j < EPT; ++j)
-      if (threadIdx.x + 256 * j < tsize) cp_async8(tb_ + tt[j] + (tt[j] >> 5), sb + so[j]);
+    for (int j = 0; j < EPT; ++j) cp_async8(tb_ + tt[j], sb + so[j]);
   };
   int buf = 0;
   if ((int64_t)blockIdx.x < tb.n_tiles) gather(blockIdx.x, 0);
@@ -383,24 +396,32 @@ stage_async_kernel(const float2* __restrict__ src, StageTables tb, int logK,
     const float2* tl = tile + buf * bstride;
     const uint32_t dbase = lut_map(ld, (uint32_t)T);
 #pragma unroll
-    for (int j = 0; j < EPT; ++j) {
-      const int t = threadIdx.x + 256 * j;
-      if (t >= tsize) break;
-      const float2 x = tl[t + (t >> 5)];
-      const uint32_t d = dbase + __ldg(tb.t_dst + t);
+    for (int g = 0; g < G; ++g) {
+      const int t0 = 4 * (threadIdx.x + 256 * g);
+      const float4* p = reinterpret_cast<const float4*>(tl + t0 + kAsyncPad * (t0 >> 5));
+      const float4 x01 = p[0], x23 = p[1];
+      const float re[4] = {x01.x, x01.z, x23.x, x23.z};
+      const float im[4] = {x01.y, x01.w, x23.y, x23.w};
+      const uint32_t d = dbase + dq[g];
       if (!kExpand) {
-        __half2 h, o;
-        split2(x.x * s, x.y * s, h, o);
-        hi[d] = h;
-        lo[d] = o;
+        __half2 h[4], o[4];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) split2(re[e] * s, im[e] * s, h[e], o[e]);
+        *reinterpret_cast<uint4*>(hi + d) = *reinterpret_cast<const uint4*>(h);
+        *reinterpret_cast<uint4*>(lo + d) = *reinterpret_cast<const uint4*>(o);
       } else {
         const uint64_t r0 = (uint64_t)d + (((uint64_t)d >> logK) << logK);
         const uint64_t r1 = r0 + (1ull << logK);
-        __half2 h0, o0, h1, o1;
-        split2(x.x * s, -x.y * s, h0, o0);
-        split2(x.y * s, x.x * s, h1, o1);
-        hi[r0] = h0; lo[r0] = o0;
-        hi[r1] = h1; lo[r1] = o1;
+        __half2 h0[4], o0[4], h1[4], o1[4];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          split2(re[e] * s, -im[e] * s, h0[e], o0[e]);
+          split2(im[e] * s, re[e] * s, h1[e], o1[e]);
+        }
+        *reinterpret_cast<uint4*>(hi + r0) = *reinterpret_cast<const uint4*>(h0);
+        *reinterpret_cast<uint4*>(lo + r0) = *reinterpret_cast<const uint4*>(o0);
+        *reinterpret_cast<uint4*>(hi + r1) = *reinterpret_cast<const uint4*>(h1);
+        *reinterpret_cast<uint4*>(lo + r1) = *reinterpret_cast<const uint4*>(o1);
       }
     }
     __syncthreads();  // buffer `buf` is refilled by the next iteration's gather
@@ -582,20 +603,26 @@ void launch_stage(const float2* src, const StageTables& tb, int64_t K, bool expa
   auto go = [&](auto kexp, auto kept) {
     constexpr bool kE = decltype(kexp)::value;
     constexpr int kP = decltype(kept)::value;
-    auto kern = stage_async_kernel<kE, kP>;
-    const size_t smem2 = 2 * smem;
-    int per_sm = 0;
-    if (async) {
-      if (smem2 > 48 * 1024)
-        TNB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem2));
-      TNB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 256, smem2));
+    bool done = false;
+    if constexpr (kP >= 4) {
+      auto kern = stage_async_kernel<kE, kP>;
+      const size_t tsz = (size_t)1 << tb.nU;
+      const size_t smem2 = 2 * 8 * (tsz + kAsyncPad * (tsz >> 5));
+      int per_sm = 0;
+      if (async) {
+        if (smem2 > 48 * 1024)
+          TNB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem2));
+        TNB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 256, smem2));
+      }
+      // persistent grid of resident blocks, each looping (and prefetching) over tiles
+      const int64_t g2 = (int64_t)kSms * per_sm;
+      if (per_sm > 0 && tb.n_tiles > 2 * g2 && tsz == (size_t)256 * kP) {
+        kern<<<(unsigned)g2, 256, smem2, s>>>(src, tb, logK, maxbits, reinterpret_cast<__half2*>(hi),
+                                             reinterpret_cast<__half2*>(lo));
+        done = true;
+      }
     }
-    // persistent grid of resident blocks, each looping (and prefetching) over tiles
-    const int64_t g2 = (int64_t)kSms * per_sm;
-    if (per_sm > 0 && tb.n_tiles > 2 * g2) {
-      kern<<<(unsigned)g2, 256, smem2, s>>>(src, tb, logK, maxbits, reinterpret_cast<__half2*>(hi),
-                                           reinterpret_cast<__half2*>(lo));
-    } else {
+    if (!done) {
       stage_kernel<kE, kP><<<(unsigned)g, 256, smem, s>>>(
           src, tb, K, logK, maxbits, reinterpret_cast<__half2*>(hi), reinterpret_cast<__half2*>(lo));
     }
