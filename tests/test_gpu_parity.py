@@ -36,7 +36,11 @@ def _cgemm(lib, M, N, K, use_tc, seed=0):
 
 @pytest.mark.parametrize("M,N,K", [(128, 128, 64), (256, 128, 128), (1024, 512, 256),
                                    (4096, 256, 1024), (128, 4096, 512), (512, 64, 8192),
-                                   (8192, 2048, 64), (64, 64, 65536)])
+                                   (8192, 2048, 64), (64, 64, 65536),
+                                   # K-blocked layout boundaries: 2K = 16, 32 (one partial /
+                                   # exact K block, row-major) and 64 (first blocked size);
+                                   # N = 8 (16 expanded columns of a 256-wide tile)
+                                   (256, 8, 8), (128, 16, 16), (512, 256, 32), (2048, 8, 4096)])
 def test_cgemm_tensor_core_vs_fp64(gpu, M, N, K):
     Cm, ref, A, B = _cgemm(gpu, M, N, K, True)
     err = rel_l2(Cm, ref)
