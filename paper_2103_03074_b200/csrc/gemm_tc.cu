@@ -204,14 +204,103 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&r)[16]) {
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
 
-__device__ __forceinline__ float scale_of(unsigned int bits) {
-  const float m = __uint_as_float(bits);
-  if (!(m > 0.f)) return 1.f;
-  int e;
-  frexpf(m, &e);
-  int p = 15 - e;
-  p = p > 126 ? 126 : (p < -126 ? -126 : p);
-  return ldexpf(1.f, p);
+__device__ __forceinline__ uint32_t lut_lookup(const ByteLut* l, uint32_t j) {
+  return __ldg(&l->t[0][j & 255]) | __ldg(&l->t[1][(j >> 8) & 255]) |
+         __ldg(&l->t[2][(j >> 16) & 255]) | __ldg(&l->t[3][j >> 24]);
+}
+
+__device__ __forceinline__ void split2f(float a, float b, __half2& hi, __half2& lo) {
+  hi = __floats2half2_rn(a, b);
+  const float2 h = __half22float2(hi);
+  lo = __floats2half2_rn(a - h.x, b - h.y);
+}
+
+// Fused staging store of one thread's 32 complex results (acc = interleaved
+// re/im, already multiplied by alpha) into the consumer's operand layout:
+// MODE 1 = rows operand (hi/lo of x s), MODE 2 = cols operand (rows 2n and
+// 2n+1 of the 2x2 real expansion: (re, -im) and (im, re)), exactly what
+// stage_kernel writes for a staged operand.
+template <int MODE>
+__device__ __forceinline__ void store_slot(const FuseOut& fo, uint32_t a, const float* x, float so) {
+  // 4 consecutive complex (destination bits 0,1) -> 16-B hi/lo stores
+  if constexpr (MODE == 1) {
+    __half2 h[4], o[4];
+#pragma unroll
+    for (int e = 0; e < 4; ++e) split2f(x[2 * e] * so, x[2 * e + 1] * so, h[e], o[e]);
+    *reinterpret_cast<uint4*>(fo.hi + a) = *reinterpret_cast<const uint4*>(h);
+    *reinterpret_cast<uint4*>(fo.lo + a) = *reinterpret_cast<const uint4*>(o);
+  } else {
+    __half2 h0[4], o0[4], h1[4], o1[4];
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const float re = x[2 * e] * so, im = x[2 * e + 1] * so;
+      split2f(re, -im, h0[e], o0[e]);
+      split2f(im, re, h1[e], o1[e]);
+    }
+    const uint32_t a1 = a + (1u << fo.L);
+    *reinterpret_cast<uint4*>(fo.hi + a) = *reinterpret_cast<const uint4*>(h0);
+    *reinterpret_cast<uint4*>(fo.lo + a) = *reinterpret_cast<const uint4*>(o0);
+    *reinterpret_cast<uint4*>(fo.hi + a1) = *reinterpret_cast<const uint4*>(h1);
+    *reinterpret_cast<uint4*>(fo.lo + a1) = *reinterpret_cast<const uint4*>(o1);
+  }
+}
+
+// Fused staging store of one thread's 32 complex results (acc = interleaved
+// re/im, already multiplied by alpha) into the consumer's operand layout:
+// MODE 1 = rows operand (hi/lo of x s), MODE 2 = cols operand (rows 2n and
+// 2n+1 of the 2x2 real expansion: (re, -im) and (im, re)), exactly what
+// stage_kernel writes for a staged operand.  `tile` = destination of the
+// warp's (row0, col0) corner.  `fast` is warp-uniform.
+template <int MODE>
+__device__ __forceinline__ void fused_store(const FuseOut& fo, uint32_t tile, float* acc, float so,
+                                            int nvalid, int lane) {
+  if (fo.fast && nvalid == EPI_COLS / 2) {
+    // butterfly exchanges: slot q = complex 4q..4q+3 = floats 8q..8q+7
+#pragma unroll
+    for (int j = 0; j < 3; ++j) {
+      const int m = fo.xlane[j];
+      if (m == 0) continue;
+      const bool hi = (lane & m) != 0;
+#pragma unroll
+      for (int q0 = 0; q0 < 8; ++q0) {
+        if (q0 & (1 << j)) continue;
+        const int q1 = q0 | (1 << j);
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+          const float send = hi ? acc[8 * q0 + e] : acc[8 * q1 + e];
+          const float recv = __shfl_xor_sync(0xffffffffu, send, m);
+          if (hi) acc[8 * q0 + e] = recv; else acc[8 * q1 + e] = recv;
+        }
+      }
+    }
+    uint32_t a = tile;
+#pragma unroll
+    for (int b = 0; b < 5; ++b)
+      if ((lane >> b) & 1) a |= fo.lane_w[b];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) store_slot<MODE>(fo, a | fo.slot_w[q], acc + 8 * q, so);
+  } else {
+    const uint32_t base = tile | lut_lookup(fo.lut_m, (uint32_t)lane);
+#pragma unroll
+    for (int j = 0; j < EPI_COLS / 2; ++j) {
+      if (j >= nvalid) break;
+      const uint32_t a = base | fo.dlow[j];
+      const float re = acc[2 * j] * so, im = acc[2 * j + 1] * so;
+      if constexpr (MODE == 1) {
+        __half2 h, o;
+        split2f(re, im, h, o);
+        fo.hi[a] = h;
+        fo.lo[a] = o;
+      } else {
+        __half2 h0, o0, h1, o1;
+        split2f(re, -im, h0, o0);
+        split2f(im, re, h1, o1);
+        const uint32_t a1 = a + (1u << fo.L);
+        fo.hi[a] = h0; fo.lo[a] = o0;
+        fo.hi[a1] = h1; fo.lo[a1] = o1;
+      }
+    }
+  }
 }
 
 struct WorkCoord {
@@ -246,9 +335,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 gemm_f16x3_kernel(const __grid_constant__ CUtensorMap tm_ahi, const __grid_constant__ CUtensorMap tm_alo,
                   const __grid_constant__ CUtensorMap tm_bhi, const __grid_constant__ CUtensorMap tm_blo,
                   float* __restrict__ C, int M, int Np, int Kp, int splits, int k_per_split,
-                  int chunk_kb, int group_m, const unsigned int* __restrict__ max_rows,
-                  const unsigned int* __restrict__ max_cols, unsigned int* __restrict__ max_out,
-                  unsigned int* __restrict__ progress, int pace_slack) {
+                  int chunk_kb, int group_m, const ScaleSrc scale_rows, const ScaleSrc scale_cols,
+                  unsigned int* __restrict__ max_out, unsigned int* __restrict__ progress,
+                  int pace_slack, const __grid_constant__ FuseOut fo) {
   using CF = Cfg<CG>;
   constexpr int STAGES = CF::STAGES;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -392,7 +481,9 @@ gemm_f16x3_kernel(const __grid_constant__ CUtensorMap tm_ahi, const __grid_const
     // ===== promotion + epilogue: warp -> TMEM lane quadrant (warp % 4), column group =====
     const int q = warp & 3;
     const int grp = (warp - 4) >> 2;
-    const float alpha = splits == 1 ? 1.f / (scale_of(*max_rows) * scale_of(*max_cols)) : 1.f;
+    const float alpha =
+        splits == 1 ? 1.f / (scale_from_src(scale_rows) * scale_from_src(scale_cols)) : 1.f;
+    const float so = fo.mode != 0 ? scale_from_src(fo.scale) : 1.f;  // fused: consumer's scale
     float vmax = 0.f;  // max |C| of this thread's outputs (scale slot of the result tensor)
     int gchunk = 0;
     for (int w = unit; w < total; w += n_units) {
@@ -426,7 +517,15 @@ gemm_f16x3_kernel(const __grid_constant__ CUtensorMap tm_ahi, const __grid_const
         acc[j] *= alpha;
         vmax = fmaxf(vmax, fabsf(acc[j]));  // out-of-range rows/cols are TMA zero-fill
       }
-      if (row0 + 32 <= M && col0 + EPI_COLS <= Np) {
+      if (fo.mode != 0) {
+        // fused staging: write the consumer's fp16 operand directly
+        const int nvalid = min(EPI_COLS / 2, (Np - col0) >> 1);
+        if (nvalid > 0) {  // warp-uniform; every row of a 32-row group exists (M >= 128, 2^k)
+          const uint32_t tile = lut_lookup(fo.lut_m, (uint32_t)row0) | lut_lookup(fo.lut_n, (uint32_t)(col0 >> 1));
+          if (fo.mode == 1) fused_store<1>(fo, tile, acc, so, nvalid, lane);
+          else fused_store<2>(fo, tile, acc, so, nvalid, lane);
+        }
+      } else if (row0 + 32 <= M && col0 + EPI_COLS <= Np) {
         // full 32-row x 64-column block: transpose float4 chunks inside each
         // 8-lane group (3 xor-butterfly stages) so that every store writes
         // 4 rows x 128 contiguous bytes instead of 32 rows x 16 bytes
@@ -544,6 +643,8 @@ int choose_cg(int64_t M) {
 }
 
 int choose_splits(int64_t M, int64_t Np, int64_t Kp, int num_sms) {
+  static const int no_split = env_int("TNB_NO_SPLITK", 0);
+  if (no_split) return 1;
   const int cg = choose_cg(M);
   const int64_t units = num_sms / cg;
   const int64_t tiles = ((M + BM * cg - 1) / (BM * cg)) * ((Np + BN - 1) / BN);
@@ -565,6 +666,10 @@ bool tc_available(int device) {
   return prop.major == 10 && prop.minor == 0;
 }
 
+int tc_splits(int64_t M, int64_t Np, int64_t Kp, int num_sms) {
+  return choose_splits(M, Np, Kp, num_sms);
+}
+
 int64_t tc_workspace_elems(int64_t M, int64_t Np, int64_t Kp, int num_sms) {
   const int s = choose_splits(M, Np, Kp, num_sms);
   return s > 1 ? (int64_t)s * M * Np : 0;
@@ -572,8 +677,8 @@ int64_t tc_workspace_elems(int64_t M, int64_t Np, int64_t Kp, int num_sms) {
 
 void tc_plan_gemm(TcGemmPlan* p, const __half* Ahi, const __half* Alo, const __half* Bhi,
                   const __half* Blo, int64_t M, int64_t Np, int64_t Kp, float* C, float* workspace,
-                  int64_t workspace_elems, const unsigned int* max_rows,
-                  const unsigned int* max_cols, unsigned int* max_out, int num_sms) {
+                  int64_t workspace_elems, const ScaleSrc& scale_rows,
+                  const ScaleSrc& scale_cols, unsigned int* max_out, int num_sms) {
   if (M > (1ll << 31) - 1 || Np > (1ll << 31) - 1 || Kp > (1ll << 31) - 1)
     throw Error(TNB_ERR_SHAPE, "tensor-core GEMM dimension too large");
   p->M = M; p->Np = Np; p->Kp = Kp;
@@ -591,8 +696,8 @@ void tc_plan_gemm(TcGemmPlan* p, const __half* Ahi, const __half* Alo, const __h
   } else {
     p->C = C;
   }
-  p->max_rows = max_rows;
-  p->max_cols = max_cols;
+  p->scale_rows = scale_rows;
+  p->scale_cols = scale_cols;
   p->max_out = max_out;
   p->chunk_kb = env_int("TNB_CHUNK_KB", kDefaultChunkKb);
   if (p->chunk_kb <= 0) p->chunk_kb = 1 << 30;  // no promotion: whole K in TMEM
@@ -627,8 +732,8 @@ void launch_cg(const TcGemmPlan* p, cudaStream_t s) {
     TNB_CUDA(cudaMemsetAsync(p->progress, 0, sizeof(unsigned int) * (p->grid / CG), s));
   TNB_CUDA(cudaLaunchKernelEx(&cfg, kern, maps[0], maps[1], maps[2], maps[3], p->C, (int)p->M,
                               (int)p->Np, (int)p->Kp, p->splits, (int)p->k_per_split, p->chunk_kb,
-                              p->group_m, p->max_rows, p->max_cols, p->max_out, p->progress,
-                              p->pace_slack));
+                              p->group_m, p->scale_rows, p->scale_cols, p->max_out, p->progress,
+                              p->pace_slack, p->fuse));
 }
 
 void tc_launch_gemm(const TcGemmPlan* p, cudaStream_t s) {

@@ -429,10 +429,9 @@ stage_async_kernel(const float2* __restrict__ src, StageTables tb, int logK,
 }
 
 __global__ void splitk_reduce_kernel(const float* __restrict__ ws, int splits, int64_t elems,
-                                     float* __restrict__ C, const unsigned int* __restrict__ max_rows,
-                                     const unsigned int* __restrict__ max_cols,
-                                     unsigned int* __restrict__ max_out) {
-  const float alpha = 1.f / (scale_from_bits(*max_rows) * scale_from_bits(*max_cols));
+                                     float* __restrict__ C, const ScaleSrc scale_rows,
+                                     const ScaleSrc scale_cols, unsigned int* __restrict__ max_out) {
+  const float alpha = 1.f / (scale_from_src(scale_rows) * scale_from_src(scale_cols));
   float m = 0.f;
   for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < elems;
        j += (int64_t)gridDim.x * blockDim.x) {
@@ -640,10 +639,10 @@ void launch_stage(const float2* src, const StageTables& tb, int64_t K, bool expa
 }
 
 void launch_splitk_reduce(const float* ws, int splits, int64_t elems, float* C,
-                          const unsigned int* max_rows, const unsigned int* max_cols,
+                          const ScaleSrc& scale_rows, const ScaleSrc& scale_cols,
                           unsigned int* max_out, cudaStream_t s) {
-  splitk_reduce_kernel<<<grid_for(elems, 256), 256, 0, s>>>(ws, splits, elems, C, max_rows, max_cols,
-                                                            max_out);
+  splitk_reduce_kernel<<<grid_for(elems, 256), 256, 0, s>>>(ws, splits, elems, C, scale_rows,
+                                                            scale_cols, max_out);
   check_launch("splitk_reduce");
 }
 

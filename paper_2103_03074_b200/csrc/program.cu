@@ -20,6 +20,8 @@
 #include "tnb_internal.h"
 
 #include <algorithm>
+#include <cstdio>
+#include <cstdlib>
 #include <cmath>
 #include <cstring>
 #include <map>
@@ -29,10 +31,20 @@
 
 namespace tnb {
 
+static int env_int(const char* name, int dflt) {
+  const char* e = getenv(name);
+  return e ? atoi(e) : dflt;
+}
+
 namespace {
 
 constexpr int64_t kAlign = 1024;
 inline int64_t align_up(int64_t x, int64_t a) { return (x + a - 1) / a * a; }
+inline int ilog2(int64_t x) {
+  int l = 0;
+  while (((int64_t)1 << l) < x) ++l;
+  return l;
+}
 
 struct Arena {
   // first-fit allocator over a virtual offset space
@@ -95,6 +107,7 @@ struct TensorRec {
   int leaf_pos = -1;
   int def_step = -1;   // step producing it (-1: leaf)
   int last_use = -1;   // last consuming step (n_steps: the root)
+  int fuse_role = 0;   // 1/2: stored as its consumer's staged rows/cols operand (fp16 hi/lo)
 };
 
 enum StepKind { KIND_SIMT = 0, KIND_TC = 1 };
@@ -112,8 +125,18 @@ struct StepRec {
   int st_rows = -1, st_cols = -1;           // TC: indices into Program::stages
   double mults = 0;
   int64_t scratch_off = 0, scratch_bytes = 0;  // TC: staging region in the arena (bytes)
+  bool fuse_rows = false, fuse_cols = false;   // TC: operand written by its producer's epilogue
+  int fuse_consumer = -1;                      // TC: step whose operand this step's epilogue writes
   TcGemmPlan tc;
 };
+
+// bytes of a tensor's storage: complex elements, or the consumer's fp16
+// hi/lo planes when its producer's epilogue writes it in staged form
+inline int64_t tensor_bytes(const TensorRec& t, int64_t esize) {
+  if (t.fuse_role == 1) return 8 * t.elems;
+  if (t.fuse_role == 2) return 16 * t.elems;
+  return esize * t.elems;
+}
 
 }  // namespace
 
@@ -153,6 +176,8 @@ struct Program {
   std::vector<StageTables> stages;  // device views of the TC staging tables
   uint32_t* d_stage_u32 = nullptr;
   ByteLut* d_stage_luts = nullptr;
+  ByteLut* d_fuse_luts = nullptr;   // fused-staging destination maps (2 per fused edge)
+  int n_fused = 0;
   void* d_acc = nullptr;          // (n_sliced + 2) accumulator slots of out_elems
   int n_acc_slots = 0;
   bool invariant_valid = false;
@@ -171,7 +196,7 @@ struct Program {
   ~Program() {
     if (device >= 0) cudaSetDevice(device);
     void* ptrs[] = {d_leaf_pool, d_slice_pool, d_persist, d_arena, d_luts,
-                    d_sl_descs, d_keep, d_tmax, d_acc, d_stage_u32, d_stage_luts, d_progress};
+                    d_sl_descs, d_keep, d_tmax, d_acc, d_stage_u32, d_stage_luts, d_progress, d_fuse_luts};
     for (void* p : ptrs)
       if (p) cudaFree(p);
     for (auto e : ev_pool) cudaEventDestroy(e);
@@ -316,6 +341,117 @@ Program* program_create(const tnb_program_desc* d) {
   P->leaf_pool_elems = leaf_off;
   P->slice_pool_elems = slice_off;
 
+  // ---- pre-pass over index sets: kernel kind and operand roles of every
+  // step, the fused-staging edges (a tensor-core step whose result feeds a
+  // tensor-core step writes it in the consumer's staged fp16 layout from its
+  // epilogue), and the canonical index orders of every tensor-core step.
+  // Orders are planned consumer-first (reverse step order): a consumer puts
+  // contracted indices that sit on its producer's lowest result columns on
+  // its lowest K bits, and the producer then orders its free indices so that
+  // the consumer's lowest destination bits (low K bits, then the consumer's
+  // lowest free bits) are its thread-local columns / lane-local rows -- the
+  // epilogue's scattered stores then form contiguous runs.  Lists below are
+  // lowest-first (canonical bit 0 first).
+  auto tc_eligible = [&](int na, int nb, int nab) {
+    return use_tc && nab >= 3 && na + nb + nab >= 27 && std::max(na, nb) >= 7 && std::min(na, nb) >= 3;
+  };
+  std::vector<std::vector<int64_t>> ord_k(d->n_steps), ord_rows(d->n_steps), ord_cols(d->n_steps);
+  std::vector<int> fuse_role_pre;                           // tensor -> 1/2 when fused
+  std::vector<int> fuse_consumer_pre;                       // tensor -> consuming step
+  {
+    static const int fuse_env = [] {
+      const char* e = getenv("TNB_FUSE");
+      return e ? atoi(e) : 1;
+    }();
+    const int nt = d->n_leaves + d->n_steps;
+    std::vector<std::vector<int64_t>> sets(nt);
+    std::vector<int> def(nt, -1);
+    for (int i = 0; i < d->n_leaves; ++i) sets[i] = P->tensors[i].axes;
+    std::unordered_map<int64_t, int> ids;
+    for (int i = 0; i < d->n_leaves; ++i) ids[d->leaf_ids[i]] = i;
+    struct Pre { int a = -1, b = -1; bool tc = false, rows_is_a = true; std::vector<int64_t> shared, rows, cols; };
+    std::vector<Pre> pre(d->n_steps);
+    for (int i = 0; i < d->n_steps; ++i) {
+      auto ia = ids.find(d->steps[3 * i]), ib = ids.find(d->steps[3 * i + 1]);
+      if (ia == ids.end() || ib == ids.end() || d->steps[3 * i] == d->steps[3 * i + 1])
+        throw Error(TNB_ERR_SHAPE, "step " + std::to_string(i) + " references a missing operand");
+      Pre& q = pre[i];
+      q.a = ia->second;
+      q.b = ib->second;
+      ids.erase(ia);
+      ids.erase(ids.find(d->steps[3 * i + 1]));
+      const auto& A = sets[q.a];
+      const auto& B = sets[q.b];
+      std::vector<int64_t> afree, bfree;
+      for (int64_t x : A) (std::find(B.begin(), B.end(), x) != B.end() ? q.shared : afree).push_back(x);
+      for (int64_t x : B) if (std::find(A.begin(), A.end(), x) == A.end()) bfree.push_back(x);
+      const int na = (int)afree.size(), nb = (int)bfree.size(), nab = (int)q.shared.size();
+      q.tc = tc_eligible(na, nb, nab);
+      q.rows_is_a = na >= nb;
+      q.rows = q.rows_is_a ? afree : bfree;
+      q.cols = q.rows_is_a ? bfree : afree;
+      ord_k[i].assign(q.shared.rbegin(), q.shared.rend());
+      ord_rows[i].assign(q.rows.rbegin(), q.rows.rend());
+      ord_cols[i].assign(q.cols.rbegin(), q.cols.rend());
+      const int out = d->n_leaves + i;
+      sets[out] = afree;
+      sets[out].insert(sets[out].end(), bfree.begin(), bfree.end());
+      def[out] = i;
+      if (ids.count(d->steps[3 * i + 2])) throw Error(TNB_ERR_SHAPE, "step output id reused");
+      ids[d->steps[3 * i + 2]] = out;
+    }
+    fuse_role_pre.assign(nt, 0);
+    fuse_consumer_pre.assign(nt, -1);
+    auto unsplit_tc = [&](int s) {
+      const Pre& q = pre[s];
+      if (!q.tc) return false;
+      const int64_t M = (int64_t)1 << q.rows.size(), N = (int64_t)1 << q.cols.size();
+      return tc_splits(M, 2 * N, 2 * ((int64_t)1 << q.shared.size()), P->num_sms) == 1;
+    };
+    auto has = [](const std::vector<int64_t>& v, int64_t x) { return std::find(v.begin(), v.end(), x) != v.end(); };
+    // `priority` first (in order, where present), then the rest in current order
+    auto reorder = [&](std::vector<int64_t>& list, const std::vector<int64_t>& priority) {
+      std::vector<int64_t> out;
+      for (int64_t x : priority) if (has(list, x) && !has(out, x)) out.push_back(x);
+      for (int64_t x : list) if (!has(out, x)) out.push_back(x);
+      list.swap(out);
+    };
+    for (int c = d->n_steps - 1; fuse_env && c >= 0; --c) {
+      const Pre& q = pre[c];
+      if (!q.tc) continue;
+      const int rows_t = q.rows_is_a ? q.a : q.b, cols_t = q.rows_is_a ? q.b : q.a;
+      const int ops[2] = {rows_t, cols_t};
+      int primary = -1;
+      for (int r = 0; r < 2; ++r) {
+        const int t = ops[r];
+        if (def[t] < 0 || !unsplit_tc(def[t])) continue;
+        fuse_role_pre[t] = r + 1;
+        fuse_consumer_pre[t] = c;
+        if (primary < 0) primary = t;
+      }
+      if (primary < 0) continue;
+      // low K bits: contracted indices on the primary producer's result
+      // columns first (n bits 0,1 -> 16-B vectors), then on its rows
+      const Pre& pp = pre[def[primary]];
+      std::vector<int64_t> kpri;
+      for (int64_t x : ord_k[c]) if (has(pp.cols, x)) kpri.push_back(x);
+      for (int64_t x : ord_k[c]) if (has(pp.rows, x)) kpri.push_back(x);
+      reorder(ord_k[c], kpri);
+      const size_t L = std::min<size_t>(ord_k[c].size(), (size_t)kKBlockLog);
+      for (int r = 0; r < 2; ++r) {
+        const int t = ops[r];
+        if (!fuse_role_pre[t]) continue;
+        // destination bits of the consumer's operand, lowest first: low K
+        // bits, then the consumer's free bits on that side (its result order)
+        std::vector<int64_t> pri(ord_k[c].begin(), ord_k[c].begin() + L);
+        const auto& side = r == 0 ? ord_rows[c] : ord_cols[c];
+        pri.insert(pri.end(), side.begin(), side.end());
+        reorder(ord_cols[def[t]], pri);
+        reorder(ord_rows[def[t]], pri);
+      }
+    }
+  }
+
   // ---- steps: axis bookkeeping (engine.py:125-134)
   for (int i = 0; i < d->n_steps; ++i) {
     const int64_t lhs = d->steps[3 * i], rhs = d->steps[3 * i + 1], outid = d->steps[3 * i + 2];
@@ -356,6 +492,17 @@ Program* program_create(const tnb_program_desc* d) {
       // expand the smaller operand (B' doubles its size); rows = the other one
       const bool rows_is_a = ((int64_t)1 << (na + nab)) >= ((int64_t)1 << (nb + nab));
       s.kind = KIND_TC;
+      // canonical orders planned by the pre-pass (lists are lowest-first;
+      // the canonical bit 0 is the LAST axis of these lists)
+      auto as_axes = [&](const std::vector<int64_t>& low_first, const std::vector<int64_t>& cur) {
+        if (low_first.size() != cur.size()) throw Error(TNB_ERR_SHAPE, "order planning mismatch");
+        return std::vector<int64_t>(low_first.rbegin(), low_first.rend());
+      };
+      shared = as_axes(ord_k[i], shared);
+      (rows_is_a ? afree : bfree) = as_axes(ord_rows[i], rows_is_a ? afree : bfree);
+      (rows_is_a ? bfree : afree) = as_axes(ord_cols[i], rows_is_a ? bfree : afree);
+      s.fuse_rows = fuse_role_pre[rows_is_a ? s.a : s.b] != 0;
+      s.fuse_cols = fuse_role_pre[rows_is_a ? s.b : s.a] != 0;
       if (rows_is_a) {
         s.rows_t = s.a; s.cols_t = s.b;
         o.axes = afree; o.axes.insert(o.axes.end(), bfree.begin(), bfree.end());
@@ -380,6 +527,8 @@ Program* program_create(const tnb_program_desc* d) {
     P->tensors[s.a].last_use = i;
     P->tensors[s.b].last_use = i;
     s.out = (int)P->tensors.size();
+    o.fuse_role = fuse_role_pre[s.out];
+    s.fuse_consumer = fuse_consumer_pre[s.out];
     s.hoisted = !o.variant && !(d->flags & TNB_FLAG_NO_HOIST);
     P->tensors.push_back(o);
     if (id2t.count(outid)) throw Error(TNB_ERR_SHAPE, "step output id reused");
@@ -420,31 +569,33 @@ Program* program_create(const tnb_program_desc* d) {
   for (int i = 0; i < n_steps; ++i) {
     StepRec& s = P->steps[i];
     TensorRec& o = P->tensors[s.out];
+    const int64_t ob = tensor_bytes(o, (int64_t)P->esize);  // fused: the consumer's fp16 planes
     if (s.hoisted || !o.variant || o.cached) {
       o.pool = POOL_PERSIST;
       o.off = persist_off;
-      persist_off += align_up(o.elems, 128);
-      if (o.cached) P->reuse_bytes += o.elems * (int64_t)P->esize;
+      persist_off += align_up(ob / (int64_t)P->esize, 128);
+      if (o.cached) P->reuse_bytes += ob;
     } else {
       o.pool = POOL_ARENA;
-      o.off = arena.alloc(o.elems * (int64_t)P->esize) / (int64_t)P->esize;
+      o.off = arena.alloc(ob) / (int64_t)P->esize;
     }
     if (s.kind == KIND_TC) {
       // operand staging (+ split-K workspace) lives in the arena for the
-      // duration of this step only: it shares memory with dead tensors
+      // duration of this step only: it shares memory with dead tensors.
+      // Fused operands are already staged (their producer wrote them).
       const int64_t Kp = 2 * s.K, Np = 2 * s.N;
-      int64_t need = 2 * s.M * Kp * 2 + 2 * Np * Kp * 2;  // hi+lo for both operands (fp16)
+      int64_t need = (s.fuse_rows ? 0 : 2 * s.M * Kp * 2) + (s.fuse_cols ? 0 : 2 * Np * Kp * 2);
       need = align_up(need, kAlign) + tc_workspace_elems(s.M, Np, Kp, P->num_sms) * 4;
-      s.scratch_off = arena.alloc(need);
       s.scratch_bytes = need;
+      if (need > 0) s.scratch_off = arena.alloc(need);
       scratch_bytes = std::max(scratch_bytes, need);
     }
     // variant operands whose last use is this step are released after it
     for (int t : free_after[i]) {
       TensorRec& r = P->tensors[t];
-      if (r.pool == POOL_ARENA) arena.release(r.off * (int64_t)P->esize, r.elems * (int64_t)P->esize);
+      if (r.pool == POOL_ARENA) arena.release(r.off * (int64_t)P->esize, tensor_bytes(r, (int64_t)P->esize));
     }
-    if (s.kind == KIND_TC) arena.release(s.scratch_off, s.scratch_bytes);
+    if (s.kind == KIND_TC && s.scratch_bytes > 0) arena.release(s.scratch_off, s.scratch_bytes);
   }
   P->persist_elems = persist_off;
   P->arena_bytes = arena.top;
@@ -490,12 +641,16 @@ Program* program_create(const tnb_program_desc* d) {
     std::vector<StageHost> hosts;
     for (auto& s : P->steps) {
       if (s.kind != KIND_TC) continue;
-      hosts.emplace_back();
-      build_stage_tables(s.canon_rows, s.K, &hosts.back());
-      s.st_rows = (int)hosts.size() - 1;
-      hosts.emplace_back();
-      build_stage_tables(s.canon_cols, s.K, &hosts.back());
-      s.st_cols = (int)hosts.size() - 1;
+      if (!s.fuse_rows) {
+        hosts.emplace_back();
+        build_stage_tables(s.canon_rows, s.K, &hosts.back());
+        s.st_rows = (int)hosts.size() - 1;
+      }
+      if (!s.fuse_cols) {
+        hosts.emplace_back();
+        build_stage_tables(s.canon_cols, s.K, &hosts.back());
+        s.st_cols = (int)hosts.size() - 1;
+      }
     }
     size_t n32 = 0;
     for (auto& h : hosts) n32 += 3 * h.rd_t.size();
@@ -531,20 +686,134 @@ Program* program_create(const tnb_program_desc* d) {
 
   // ---- tensor-core plans (fixed addresses -> TMA descriptors built once)
   dmalloc((void**)&P->d_progress, (int64_t)P->num_sms * 4);
-  for (auto& s : P->steps) {
+  // fp16 split scale of a tensor-core operand: its own max when staged, the
+  // producer's a-priori bound 2 K max|A| max|B| when the producer's epilogue
+  // wrote it (fused); producer and consumer evaluate the same ScaleSrc
+  auto operand_scale = [&](int t) {
+    ScaleSrc sc;
+    const TensorRec& r = P->tensors[t];
+    if (r.fuse_role != 0) {
+      const StepRec& p = P->steps[r.def_step];
+      sc.a = P->d_tmax + P->slot[p.rows_t];
+      sc.b = P->d_tmax + P->slot[p.cols_t];
+      sc.f = (float)(2.0 * (double)p.K);
+    } else {
+      sc.a = P->d_tmax + P->slot[t];
+    }
+    return sc;
+  };
+  std::vector<ByteLut> fuse_luts;
+  std::vector<int> fuse_lut_step;
+  for (int i = 0; i < n_steps; ++i) {
+    StepRec& s = P->steps[i];
     if (s.kind != KIND_TC) continue;
     const int64_t Kp = 2 * s.K, Np = 2 * s.N;
     char* base = (char*)P->d_arena + s.scratch_off;
-    __half* ahi = (__half*)base;
+    int64_t used = 0;
+    __half* ahi = s.fuse_rows ? (__half*)P->tensor_ptr(s.rows_t) : (__half*)base;
+    if (!s.fuse_rows) used += 2 * s.M * Kp * 2;
     __half* alo = ahi + s.M * Kp;
-    __half* bhi = alo + s.M * Kp;
+    __half* bhi = s.fuse_cols ? (__half*)P->tensor_ptr(s.cols_t) : (__half*)(base + used);
+    if (!s.fuse_cols) used += 2 * Np * Kp * 2;
     __half* blo = bhi + Np * Kp;
-    float* ws = (float*)(base + align_up(2 * s.M * Kp * 2 + 2 * Np * Kp * 2, kAlign));
+    float* ws = (float*)(base + align_up(used, kAlign));
     const int64_t ws_elems = tc_workspace_elems(s.M, Np, Kp, P->num_sms);
     tc_plan_gemm(&s.tc, ahi, alo, bhi, blo, s.M, Np, Kp, (float*)P->tensor_ptr(s.out), ws, ws_elems,
-                 P->d_tmax + P->slot[s.rows_t], P->d_tmax + P->slot[s.cols_t],
-                 P->d_tmax + P->slot[s.out], P->num_sms);
+                 operand_scale(s.rows_t), operand_scale(s.cols_t), P->d_tmax + P->slot[s.out],
+                 P->num_sms);
     s.tc.progress = P->d_progress;
+    const TensorRec& o = P->tensors[s.out];
+    if (o.fuse_role == 0) continue;
+    if (s.tc.splits != 1) throw Error(TNB_ERR_SHAPE, "fused staging planned for a split-K step");
+    // destination map of the consumer's operand layout (stage_kernel's):
+    // canonical (row r, k) -> half2 index (k >> L, r, k & (2^L-1)) in
+    // [K/2^L][rows][2^L], a zero bit inserted at L for the expanded cols
+    const StepRec& c = P->steps[s.fuse_consumer];
+    const bool as_rows = o.fuse_role == 1;
+    const std::vector<int>& canon = as_rows ? c.canon_rows : c.canon_cols;
+    const int nk = ilog2(c.K), nr = ilog2(as_rows ? c.M : c.N);
+    const int L = std::min(nk, kKBlockLog);
+    const int nbits = (int)o.axes.size();
+    if (nbits != nk + nr || (int)canon.size() != nbits) throw Error(TNB_ERR_SHAPE, "fused staging: rank mismatch");
+    std::vector<int> dbit(nbits);
+    for (int p = 0; p < nbits; ++p) {
+      int db = p < L ? p : (p < nk ? p + nr : p - nk + L);
+      if (!as_rows && db >= L) db += 1;
+      dbit[canon[p]] = db;
+    }
+    const int ln = ilog2(s.N);  // complex result columns = the low source bits
+    std::vector<int> nvec(dbit.begin(), dbit.begin() + ln), mvec(dbit.begin() + ln, dbit.end());
+    FuseOut& f = s.tc.fuse;
+    f.mode = as_rows ? 1 : 2;
+    f.L = L;
+    // fast path: vector bits n0,n1 -> destination bits 0,1; the lanes take
+    // the 5 thread-local source bits (slot bits n2..n4, lane bits m0..m4)
+    // with the lowest destination bits, swapped in by butterfly exchanges
+    f.fast = 0;
+    static const int fast_env = env_int("TNB_FUSE_FAST", 1);
+    if (fast_env && ln >= 5 && (int)mvec.size() >= 5 && nvec[0] == 0 && nvec[1] == 1) {
+      std::vector<std::pair<int, int>> loc;  // (destination bit, local bit: 0-2 slot, 3-7 lane)
+      for (int j = 0; j < 3; ++j) loc.push_back({nvec[2 + j], j});
+      for (int b = 0; b < 5; ++b) loc.push_back({mvec[b], 3 + b});
+      std::sort(loc.begin(), loc.end());
+      std::vector<char> on_lane(8, 0);
+      for (int x = 0; x < 5; ++x) on_lane[loc[x].second] = 1;
+      int dslot[3], dlane[5];
+      for (int j = 0; j < 3; ++j) dslot[j] = nvec[2 + j];
+      for (int b = 0; b < 5; ++b) dlane[b] = mvec[b];
+      int b = 0;
+      for (int j = 0; j < 3; ++j) {
+        f.xlane[j] = 0;
+        if (!on_lane[j]) continue;              // slot bit stays in the registers
+        while (on_lane[3 + b]) ++b;             // a lane bit that must leave the lanes
+        f.xlane[j] = 1 << b;
+        std::swap(dslot[j], dlane[b]);
+        ++b;
+      }
+      for (int bb = 0; bb < 5; ++bb) f.lane_w[bb] = 1u << dlane[bb];
+      for (int q = 0; q < 8; ++q) {
+        uint32_t v = 0;
+        for (int j = 0; j < 3; ++j)
+          if ((q >> j) & 1) v |= 1u << dslot[j];
+        f.slot_w[q] = v;
+      }
+      f.fast = 1;
+    }
+    for (int j = 0; j < 32; ++j) {
+      uint32_t v = 0;
+      for (int p = 0; p < std::min(5, ln); ++p)
+        if ((j >> p) & 1) v |= 1u << nvec[p];
+      f.dlow[j] = v;
+    }
+    if (getenv("TNB_DEBUG_FUSE")) {
+      fprintf(stderr, "TNB_FUSE step %d -> %d role %d out 2^%d fast %d nvec[0..4]", i, s.fuse_consumer,
+              o.fuse_role, nbits, f.fast);
+      for (int p = 0; p < std::min(5, ln); ++p) fprintf(stderr, " %d", nvec[p]);
+      fprintf(stderr, " mvec[0..4]");
+      for (int p = 0; p < std::min<int>(5, (int)mvec.size()); ++p) fprintf(stderr, " %d", mvec[p]);
+      fprintf(stderr, " lane_w");
+      for (int b = 0; b < 5; ++b) fprintf(stderr, " %d", f.fast ? ilog2(f.lane_w[b]) : -1);
+      fprintf(stderr, "\n");
+    }
+    f.hi = (__half2*)P->tensor_ptr(s.out);
+    f.lo = f.hi + (as_rows ? c.M * c.K : 2 * c.N * c.K);
+    f.scale = operand_scale(s.out);
+    fuse_luts.emplace_back();
+    build_lut(mvec, &fuse_luts.back());
+    fuse_luts.emplace_back();
+    build_lut(nvec, &fuse_luts.back());
+    fuse_lut_step.push_back(i);
+  }
+  P->n_fused = (int)fuse_lut_step.size();
+  if (!fuse_luts.empty()) {
+    dmalloc((void**)&P->d_fuse_luts, (int64_t)fuse_luts.size() * sizeof(ByteLut));
+    TNB_CUDA(cudaMemcpy(P->d_fuse_luts, fuse_luts.data(), fuse_luts.size() * sizeof(ByteLut),
+                        cudaMemcpyHostToDevice));
+    for (size_t e = 0; e < fuse_lut_step.size(); ++e) {
+      FuseOut& f = P->steps[fuse_lut_step[e]].tc.fuse;
+      f.lut_m = P->d_fuse_luts + 2 * e;
+      f.lut_n = P->d_fuse_luts + 2 * e + 1;
+    }
   }
 
   // ---- upload leaf values
@@ -588,7 +857,7 @@ void program_info(const Program* P, tnb_program_info* info) {
   int k = P->n_sl_descs ? 1 : 0;
   for (auto& s : P->steps) {
     if (s.hoisted) continue;
-    k += s.kind == KIND_TC ? (3 + (s.tc.splits > 1 ? 1 : 0)) : 1;
+    k += s.kind == KIND_TC ? (1 + !s.fuse_rows + !s.fuse_cols + (s.tc.splits > 1 ? 1 : 0)) : 1;
   }
   info->kernels_per_slice = k + 1;
   info->reuse_bytes = P->reuse_bytes;
@@ -748,26 +1017,34 @@ void exec_step(Program* P, StepRec& s) {
     const int64_t Kp = 2 * s.K, Np = 2 * s.N;
     const float2* rows = (const float2*)P->tensor_ptr(s.rows_t);
     const float2* cols = (const float2*)P->tensor_ptr(s.cols_t);
+    // staging destinations: the step's scratch, rows planes first (same
+    // layout as the plan's TMA maps; fused operands are not staged here)
     char* base = (char*)P->d_arena + s.scratch_off;
     __half* ahi = (__half*)base;
     __half* alo = ahi + s.M * Kp;
-    __half* bhi = alo + s.M * Kp;
+    __half* bhi = (__half*)(base + (s.fuse_rows ? 0 : 2 * s.M * Kp * 2));
     __half* blo = bhi + Np * Kp;
-    cudaEvent_t e = C.mark();
-    launch_stage(rows, P->stages[s.st_rows], s.K, false, P->d_tmax + P->slot[s.rows_t], ahi, alo, P->stream);
-    launch_stage(cols, P->stages[s.st_cols], s.K, true, P->d_tmax + P->slot[s.cols_t], bhi, blo, P->stream);
-    C.close(1, e);
+    cudaEvent_t e = nullptr;
+    if (!s.fuse_rows || !s.fuse_cols) e = C.mark();
+    if (!s.fuse_rows) {
+      launch_stage(rows, P->stages[s.st_rows], s.K, false, P->d_tmax + P->slot[s.rows_t], ahi, alo, P->stream);
+      C.launches++;
+    }
+    if (!s.fuse_cols) {
+      launch_stage(cols, P->stages[s.st_cols], s.K, true, P->d_tmax + P->slot[s.cols_t], bhi, blo, P->stream);
+      C.launches++;
+    }
+    if (!s.fuse_rows || !s.fuse_cols) C.close(1, e);
     e = C.mark();
     tc_launch_gemm(&s.tc, P->stream);
     C.close(0, e);
-    C.launches += 3;
+    C.launches += 1;
     C.gemm_launches++;
     C.gemm_flops += 8.0 * s.mults;
     if (s.tc.splits > 1) {
       e = C.mark();
       launch_splitk_reduce(s.tc.C, s.tc.splits, s.M * Np, (float*)P->tensor_ptr(s.out),
-                           s.tc.max_rows, s.tc.max_cols, s.tc.max_out,
-                           P->stream);
+                           s.tc.scale_rows, s.tc.scale_cols, s.tc.max_out, P->stream);
       C.close(1, e);
       C.launches++;
     }
@@ -875,6 +1152,19 @@ void run_range_t(Program* P, uint64_t a, uint64_t b, int mode, void* out, bool o
   }
   cudaEvent_t t_end = ctx.mark();
   TNB_CUDA(cudaStreamSynchronize(st));
+  if (std::is_same<T, float2>::value && getenv("TNB_DEBUG_MAX")) {
+    // diagnostic: per-step output max vs the a-priori bound 2 K max|A| max|B|
+    std::vector<float> mx(P->slot.size() ? *std::max_element(P->slot.begin(), P->slot.end()) + 1 : 0);
+    TNB_CUDA(cudaMemcpy(mx.data(), P->d_tmax, mx.size() * 4, cudaMemcpyDeviceToHost));
+    for (size_t i = 0; i < P->steps.size(); ++i) {
+      const StepRec& s = P->steps[i];
+      const float ma = mx[P->slot[s.a]], mb = mx[P->slot[s.b]], mc = mx[P->slot[s.out]];
+      const double bound = 2.0 * (double)s.K * ma * mb;
+      fprintf(stderr, "TNB_MAX step %zu kind %d M %lld N %lld K %lld maxA %.3e maxB %.3e maxC %.3e log2(bound/maxC) %.2f\n",
+              i, s.kind, (long long)s.M, (long long)s.N, (long long)s.K, ma, mb, mc,
+              mc > 0 ? std::log2(bound / mc) : -1.0);
+    }
+  }
   tnb_timing tm{};
   if (P->timing) {
     float ms = 0;

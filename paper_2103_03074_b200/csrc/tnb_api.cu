@@ -223,12 +223,15 @@ int tnb_cgemm(int32_t device, int64_t M, int64_t N, int64_t K, const void* A, co
       launch_stage((const float2*)pa, tb[0], K, false, mx, ahi, alo, st);
       launch_stage((const float2*)pb, tb[1], K, true, mx + 1, bhi, blo, st);
       TcGemmPlan plan;
-      tc_plan_gemm(&plan, ahi, alo, bhi, blo, M, Np, Kp, (float*)pc, wsp, ws, mx, mx + 1, mx + 2, sms);
+      ScaleSrc sa, sb;
+      sa.a = mx;
+      sb.a = mx + 1;
+      tc_plan_gemm(&plan, ahi, alo, bhi, blo, M, Np, Kp, (float*)pc, wsp, ws, sa, sb, mx + 2, sms);
       DevBuf progress((size_t)sms * 4);
       plan.progress = (unsigned int*)progress.p;
       tc_launch_gemm(&plan, st);
       if (plan.splits > 1)
-        launch_splitk_reduce(plan.C, plan.splits, M * Np, (float*)pc, mx, mx + 1, mx + 2, st);
+        launch_splitk_reduce(plan.C, plan.splits, M * Np, (float*)pc, sa, sb, mx + 2, st);
       TNB_CUDA(cudaStreamSynchronize(st));
     }
     if (!on_device) TNB_CUDA(cudaMemcpyAsync(C, pc, ec, cudaMemcpyDeviceToHost, st));

@@ -50,6 +50,45 @@ struct ByteLut {
 void build_lut(const std::vector<int>& src_bit, ByteLut* out);
 
 // ---------------------------------------------------------------------------
+// fp16 split scale of a staged operand: s = 2^(15-e) where the bound
+// v = f * max(a) [* max(b)] = frac * 2^e (frac in [0.5, 1)), so v*s lands in
+// [2^14, 2^15).  Staged operands use their own exact max (b = null, f = 1);
+// operands written by the producer's epilogue (fused staging) use the a-priori
+// bound |x| <= 2 K max|A| max|B| of the producing step (its operands' maxes),
+// known before the producer runs.
+struct ScaleSrc {
+  const unsigned int* a = nullptr;
+  const unsigned int* b = nullptr;
+  float f = 1.f;  // power of two
+};
+
+#ifdef __CUDACC__
+__device__ __forceinline__ float scale_from_src(const ScaleSrc& s) {
+  const float ma = __uint_as_float(*s.a);
+  if (!(ma > 0.f)) return 1.f;
+  int e;
+  float fr = frexpf(ma, &e);  // ma = fr * 2^e
+  if (s.b != nullptr) {
+    const float mb = __uint_as_float(*s.b);
+    if (!(mb > 0.f)) return 1.f;
+    int eb, ef, ep;
+    const float fb = frexpf(mb, &eb);
+    frexpf(s.f, &ef);            // f = 2^(ef-1)
+    fr = frexpf(fr * fb, &ep);   // product of the fractions in [0.25, 1)
+    e = e + eb + (ef - 1) + ep;
+  } else if (s.f != 1.f) {
+    int ef;
+    frexpf(s.f, &ef);
+    e += ef - 1;
+  }
+  int p = 15 - e;
+  p = p > 126 ? 126 : (p < -126 ? -126 : p);
+  return ldexpf(1.f, p);
+}
+#endif
+
+
+// ---------------------------------------------------------------------------
 // Kernel launchers (kernels.cu).  All take a stream; pointers are device.
 struct SlicedLeafDesc {      // one sliced leaf to prepare per mask
   uint64_t src_off;          // element offset of the full leaf in the leaf pool
@@ -116,8 +155,35 @@ void build_stage_tables(const std::vector<int>& canon_to_src, int64_t K, StageHo
 void launch_stage(const float2* src, const StageTables& tb, int64_t K, bool expand,
                   const unsigned int* maxbits, __half* hi, __half* lo, cudaStream_t s);
 void launch_splitk_reduce(const float* ws, int splits, int64_t elems, float* C,
-                          const unsigned int* max_rows, const unsigned int* max_cols,
+                          const ScaleSrc& scale_rows, const ScaleSrc& scale_cols,
                           unsigned int* max_out, cudaStream_t s);
+
+// Fused staging: the producer GEMM's epilogue writes its result straight into
+// the consumer GEMM's operand layout (K-blocked fp16 hi/lo planes; role 1 =
+// the consumer's rows operand, role 2 = its 2x2-expanded cols operand).  The
+// destination half2 index of result element (m, n) is lut_m(m) | lut_n(n)
+// (a bit permutation); dlow[j] = lut_n(j) for the 32 columns of one thread.
+//
+// Fast path (`fast`): one thread holds row m (lane = m bits 0-4) and 32
+// complex columns (n bits 0-4 = vector element e (2 bits) | slot q (3 bits)).
+// When n bits 0,1 are destination bits 0,1, up to three butterfly exchanges
+// (slot bit j <-> lane bit log2(xlane[j])) move the source bits whose
+// destination bits are lowest onto the lanes, so each warp store writes
+// contiguous runs; the address is then tile base | lane part | slot_w[q].
+struct FuseOut {
+  int mode = 0;                  // 0: plain fp32 C; 1: rows operand; 2: cols operand
+  int L = 0;                     // cols: rows 2n / 2n+1 are 2^L half2 apart
+  int fast = 0;                  // exchange + 16-B store path usable
+  int xlane[3] = {0, 0, 0};      // lane xor mask exchanged with slot bit j (0: none)
+  uint32_t lane_w[5] = {};       // destination weight of lane bit b (after exchanges)
+  uint32_t slot_w[8] = {};       // destination offset of slot q (after exchanges)
+  __half2* hi = nullptr;
+  __half2* lo = nullptr;
+  const ByteLut* lut_m = nullptr;
+  const ByteLut* lut_n = nullptr;
+  uint32_t dlow[32] = {};
+  ScaleSrc scale;                // scale of the written operand
+};
 
 // ---------------------------------------------------------------------------
 // tcgen05 GEMM (gemm_tc.cu):  C[M][Np] (fp32) = alpha * sum over the three
@@ -134,17 +200,19 @@ struct TcGemmPlan {
   int grid = 0;
   alignas(64) unsigned char tmap[4][128];  // CUtensorMap x4: Ahi, Alo, Bhi, Blo
   float* C = nullptr;            // output (splits == 1) or workspace [splits][M][Np]
-  const unsigned int* max_rows = nullptr;  // device: max bits of the rows operand
-  const unsigned int* max_cols = nullptr;  // device: max bits of the cols operand
+  ScaleSrc scale_rows;           // fp16 split scale of the rows operand
+  ScaleSrc scale_cols;           // ... and of the cols operand
   unsigned int* max_out = nullptr;         // device: max bits of the result (atomicMax)
+  FuseOut fuse;                  // epilogue output format (splits == 1 only)
 };
 
 bool tc_available(int device);
 void tc_plan_gemm(TcGemmPlan* p, const __half* Ahi, const __half* Alo, const __half* Bhi,
                   const __half* Blo, int64_t M, int64_t Np, int64_t Kp, float* C,
-                  float* workspace, int64_t workspace_elems, const unsigned int* max_rows,
-                  const unsigned int* max_cols, unsigned int* max_out, int num_sms);
+                  float* workspace, int64_t workspace_elems, const ScaleSrc& scale_rows,
+                  const ScaleSrc& scale_cols, unsigned int* max_out, int num_sms);
 void tc_launch_gemm(const TcGemmPlan* p, cudaStream_t s);
 int64_t tc_workspace_elems(int64_t M, int64_t Np, int64_t Kp, int num_sms);
+int tc_splits(int64_t M, int64_t Np, int64_t Kp, int num_sms);
 
 }  // namespace tnb
