@@ -324,7 +324,9 @@ def run_ours(args):
             "bound": "tensor", "kernel": "gemm_f16x3 (tcgen05)",
             "achieved": achieved, "peak": sustained, "unit": "TFLOP/s",
             "frac": achieved / sustained,
-            "peak_kind": f"{src} bf16 dense sustained (MEASURED_PEAKS.json)",
+            "peak_kind": (f"{src} bf16 dense sustained " +
+                          ("(MEASURED_PEAKS.json)" if src == "measured"
+                           else "(B200_PROFILING.md fallback: MEASURED_PEAKS.json absent)")),
             "achieved_is": "algorithmic complex FLOPs (8 per complex multiply-add) per GEMM launch / event time",
             "tensor_tflops_executed": 3.0 * achieved,
             "tensor_frac": 3.0 * achieved / sustained,

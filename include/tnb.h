@@ -63,6 +63,9 @@ typedef enum { TNB_FIXED = 0, TNB_FREE = 1 } tnb_mode;          /* engine.py:293
 #define TNB_FLAG_REUSE_SLICES    0x4u  /* reuse results whose mask bits did not
                                           change between consecutive slices
                                           (bit-identical; skips recomputation)  */
+#define TNB_FLAG_NO_FUSE         0x8u  /* stage every tensor-core operand with the
+                                          permute/split kernel instead of writing
+                                          it from the producer GEMM's epilogue   */
 
 typedef struct tnb_program tnb_program;
 
@@ -97,6 +100,9 @@ typedef struct {
   int32_t n_steps_hoisted;      /* slice-invariant steps computed once              */
   int32_t kernels_per_slice;    /* launches per slice                               */
   int64_t reuse_bytes;          /* TNB_FLAG_REUSE_SLICES: dedicated cached buffers  */
+  int32_t n_steps_fused;        /* tensor-core steps whose result is written by the
+                                   GEMM epilogue as the consumer's staged operand    */
+  int32_t n_steps_fused_fast;   /* ... of which on the coalesced exchange path      */
 } tnb_program_info;
 
 typedef struct {

@@ -21,6 +21,7 @@ TNB_FIXED, TNB_FREE = 0, 1
 TNB_FLAG_NO_TENSOR_CORES = 0x1
 TNB_FLAG_NO_HOIST = 0x2
 TNB_FLAG_REUSE_SLICES = 0x4
+TNB_FLAG_NO_FUSE = 0x8
 
 i32, i64, u32, u64, f64 = C.c_int32, C.c_int64, C.c_uint32, C.c_uint64, C.c_double
 P = C.c_void_p
@@ -43,6 +44,7 @@ class ProgramInfo(C.Structure):
         ("arena_bytes", i64), ("persistent_bytes", i64), ("scratch_bytes", i64),
         ("n_steps_tc", i32), ("n_steps_simt", i32), ("n_steps_hoisted", i32),
         ("kernels_per_slice", i32), ("reuse_bytes", i64),
+        ("n_steps_fused", i32), ("n_steps_fused_fast", i32),
     ]
 
 

@@ -337,7 +337,7 @@ gemm_f16x3_kernel(const __grid_constant__ CUtensorMap tm_ahi, const __grid_const
                   float* __restrict__ C, int M, int Np, int Kp, int splits, int k_per_split,
                   int chunk_kb, int group_m, const ScaleSrc scale_rows, const ScaleSrc scale_cols,
                   unsigned int* __restrict__ max_out, unsigned int* __restrict__ progress,
-                  int pace_slack, const __grid_constant__ FuseOut fo) {
+                  int pace_slack, const __grid_constant__ FuseOut fo, int exp_skip) {
   using CF = Cfg<CG>;
   constexpr int STAGES = CF::STAGES;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -422,13 +422,19 @@ gemm_f16x3_kernel(const __grid_constant__ CUtensorMap tm_ahi, const __grid_const
         if (lane == 0) {
           mbar_wait_sleep(&empty_bar[stage], phase ^ 1);
           uint8_t* st = smem + stage * CF::STAGE_BYTES;
-          if (leader) mbar_arrive_expect_tx(&full_bar[stage], CG * CF::STAGE_BYTES);
+          // exp_skip (diagnostic only, wrong results): 1 = skip B loads, 2 = skip A loads
+          const uint32_t bytes = exp_skip == 1 ? 2 * A_TILE : exp_skip == 2 ? 2 * CF::B_TILE : CF::STAGE_BYTES;
+          if (leader) mbar_arrive_expect_tx(&full_bar[stage], CG * bytes);
           else mbar_arrive_remote(&full_bar[stage], 0);
           const int kbk = k / BK;
-          tma_load_tile<CG>(st, &tm_ahi, &full_bar[stage], m0, kbk);
-          tma_load_tile<CG>(st + A_TILE, &tm_alo, &full_bar[stage], m0, kbk);
-          tma_load_tile<CG>(st + 2 * A_TILE, &tm_bhi, &full_bar[stage], n0, kbk);
-          tma_load_tile<CG>(st + 2 * A_TILE + CF::B_TILE, &tm_blo, &full_bar[stage], n0, kbk);
+          if (exp_skip != 2) {
+            tma_load_tile<CG>(st, &tm_ahi, &full_bar[stage], m0, kbk);
+            tma_load_tile<CG>(st + A_TILE, &tm_alo, &full_bar[stage], m0, kbk);
+          }
+          if (exp_skip != 1) {
+            tma_load_tile<CG>(st + 2 * A_TILE, &tm_bhi, &full_bar[stage], n0, kbk);
+            tma_load_tile<CG>(st + 2 * A_TILE + CF::B_TILE, &tm_blo, &full_bar[stage], n0, kbk);
+          }
         }
         __syncwarp();
         if (++stage == STAGES) { stage = 0; phase ^= 1; }
@@ -733,7 +739,7 @@ void launch_cg(const TcGemmPlan* p, cudaStream_t s) {
   TNB_CUDA(cudaLaunchKernelEx(&cfg, kern, maps[0], maps[1], maps[2], maps[3], p->C, (int)p->M,
                               (int)p->Np, (int)p->Kp, p->splits, (int)p->k_per_split, p->chunk_kb,
                               p->group_m, p->scale_rows, p->scale_cols, p->max_out, p->progress,
-                              p->pace_slack, p->fuse));
+                              p->pace_slack, p->fuse, env_int("TNB_EXP_SKIP", 0)));
 }
 
 void tc_launch_gemm(const TcGemmPlan* p, cudaStream_t s) {

@@ -416,7 +416,8 @@ Program* program_create(const tnb_program_desc* d) {
       for (int64_t x : list) if (!has(out, x)) out.push_back(x);
       list.swap(out);
     };
-    for (int c = d->n_steps - 1; fuse_env && c >= 0; --c) {
+    const bool fuse = fuse_env && !(d->flags & TNB_FLAG_NO_FUSE);
+    for (int c = d->n_steps - 1; fuse && c >= 0; --c) {
       const Pre& q = pre[c];
       if (!q.tc) continue;
       const int rows_t = q.rows_is_a ? q.a : q.b, cols_t = q.rows_is_a ? q.b : q.a;
@@ -861,6 +862,13 @@ void program_info(const Program* P, tnb_program_info* info) {
   }
   info->kernels_per_slice = k + 1;
   info->reuse_bytes = P->reuse_bytes;
+  info->n_steps_fused = 0;
+  info->n_steps_fused_fast = 0;
+  for (auto& s : P->steps)
+    if (s.kind == KIND_TC && s.tc.fuse.mode != 0) {
+      info->n_steps_fused++;
+      info->n_steps_fused_fast += s.tc.fuse.fast ? 1 : 0;
+    }
 }
 
 void program_set_leaf(Program* P, int leaf_pos, const double* data) {

@@ -1,0 +1,33 @@
+"""What-if: time the top C4 GEMM shape with A or B tile loads skipped
+(TNB_EXP_SKIP; wrong results, timing only) to see how much the L2->SM
+operand traffic costs under the power cap."""
+import os, sys, subprocess, json
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+if len(sys.argv) > 1:
+    import numpy as np, torch
+    from paper_2103_03074_b200 import _lib
+    lib = _lib.load()
+    M, N, K = 1 << 15, 1 << 12, 1 << 15
+    A = torch.randn(M, K, dtype=torch.complex64, device="cuda")
+    B = torch.randn(K, N, dtype=torch.complex64, device="cuda")
+    C = torch.empty(M, N, dtype=torch.complex64, device="cuda")
+    for _ in range(2):
+        _lib.check(lib.tnb_cgemm(0, M, N, K, A.data_ptr(), B.data_ptr(), C.data_ptr(), 1, 1))
+    torch.cuda.synchronize()
+    import time
+    ts = []
+    for _ in range(3):
+        t = time.perf_counter()
+        _lib.check(lib.tnb_cgemm(0, M, N, K, A.data_ptr(), B.data_ptr(), C.data_ptr(), 1, 1))
+        torch.cuda.synchronize()
+        ts.append(time.perf_counter() - t)
+    print(json.dumps({"skip": os.environ.get("TNB_EXP_SKIP", "0"), "s": min(ts)}))
+else:
+    for sk in ["0", "1", "2", "0"]:
+        env = dict(os.environ, TNB_EXP_SKIP=sk)
+        smi = subprocess.Popen(["nvidia-smi", "--query-gpu=clocks.sm,power.draw", "--format=csv,noheader", "-lms", "200"],
+                               stdout=subprocess.PIPE, text=True)
+        out = subprocess.run([sys.executable, __file__, "run"], env=env, capture_output=True, text=True)
+        smi.terminate()
+        samples = smi.communicate()[0].strip().splitlines()
+        print(out.stdout.strip(), out.stderr.strip()[-300:], "clocks/power samples (last 8):", samples[-8:])

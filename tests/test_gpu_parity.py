@@ -249,3 +249,38 @@ def test_cross_slice_reuse_bit_identical(gpu, workloads, name, rng_):
     # continuing with the next range reuses across calls, still bit-identical
     a, b = rng_
     assert np.array_equal(reuse.run_range(b, 2 * b - a), base.run_range(b, 2 * b - a))
+
+
+@pytest.mark.parametrize("name", ["m12", "c2", "c3"])
+def test_fused_staging_vs_staged(gpu, workloads, name):
+    """Operands written by the producer GEMM's epilogue (default) and operands
+    staged by the permute/split kernel (TNB_FLAG_NO_FUSE) both match the
+    reference golden head slice; the fused program launches fewer kernels."""
+    from paper_2103_03074_b200 import _lib, engine as E
+
+    w = workloads(name)
+    g = golden(name)
+    stride = int(g["stride"])
+    ref = g["head_single_0_1_sub"]
+    fused = E.head_program(w.tn, w.tree, w.sliced, "single", flags=0)
+    staged = E.head_program(w.tn, w.tree, w.sliced, "single", flags=_lib.TNB_FLAG_NO_FUSE)
+    assert fused.info.n_steps_fused > 0 and staged.info.n_steps_fused == 0
+    assert fused.info.kernels_per_slice < staged.info.kernels_per_slice
+    hf = fused.run_range(0, 1)
+    hs = staged.run_range(0, 1)
+    ef, es = rel_l2(hf[::stride], ref), rel_l2(hs[::stride], ref)
+    assert ef < SINGLE_TOL and es < SINGLE_TOL, (ef, es)
+    # the bound-based fp16 scale keeps fp32-level accuracy
+    assert ef < 10 * max(es, 1e-6), (ef, es)
+    assert rel_l2(hf, hs) < SINGLE_TOL
+
+
+def test_fused_staging_c4_plan(gpu, workloads):
+    """C4: every tensor-core -> tensor-core edge is fused, most on the
+    coalesced exchange path; no split-K producer is fused."""
+    from paper_2103_03074_b200 import engine as E
+
+    w = workloads("c4")
+    prog = E.head_program(w.tn, w.tree, w.sliced, "single")
+    assert prog.info.n_steps_fused >= 15
+    assert prog.info.n_steps_fused_fast >= prog.info.n_steps_fused - 3
