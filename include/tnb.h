@@ -161,6 +161,34 @@ int tnb_cgemm(int32_t device, int64_t M, int64_t N, int64_t K,
 int tnb_add_tree(int32_t device, int32_t precision, int64_t elems, int32_t n,
                  const void* const* vecs, void* out);
 
+/* ---- On-device output-distribution analytics (tncut analytics.py) on a
+   probability vector in device memory (`probs`, fp64).  Host results.
+   Sums are deterministic (fixed reduction tree); counts/min/max exact. */
+
+/* probs[i] = |amps[i]|^2 in fp64; amps complex64 (TNB_SINGLE) or complex128,
+   the engine's AmplitudeTable.probabilities (engine.py:79-81). */
+int tnb_probabilities(int32_t device, int32_t precision, const void* amps, int64_t n, double* probs);
+/* out4 = {sum, min, max, min over p > 0 (+inf if none)}: the reductions of
+   xeb (analytics.py:46-58), marginal_and_conditional (:159-177) and the
+   log-scale histogram range (:104-107). */
+int tnb_prob_reduce(int32_t device, const double* probs, int64_t n, double* out4_host);
+/* counts of x = scale * p per bin [edges[i], edges[i+1]) (last bin closed),
+   np.histogram semantics of histogram() (analytics.py:90-121). */
+int tnb_prob_histogram(int32_t device, const double* probs, int64_t n, double scale,
+                       const double* edges_host, int32_t bins, int64_t* counts_host);
+/* in-place radix sort (ascending, or descending if `descending`). */
+int tnb_prob_sort(int32_t device, double* probs, int64_t n, int32_t descending);
+/* sortedness check of postselect_curve (analytics.py:136-137). */
+int tnb_prob_is_sorted_desc(int32_t device, const double* probs, int64_t n, int32_t* sorted_host);
+/* sums_host[j] = probs[0] + ... + probs[ks[j]-1] (the cumsum of
+   postselect_curve, analytics.py:138-142). */
+int tnb_prob_prefix_sums(int32_t device, const double* probs, int64_t n, const int64_t* ks_host,
+                         int32_t nk, double* sums_host);
+/* KS distance of scale * p (sorted ascending) against Exp(1)
+   (ks_to_porter_thomas, analytics.py:70-79). */
+int tnb_prob_ks(int32_t device, const double* probs_sorted_asc, int64_t n, double scale,
+                double* out_host);
+
 #ifdef __cplusplus
 }
 #endif

@@ -29,6 +29,7 @@ from .errors import (  # noqa: F401
     ShapeMismatch,
     TncutError,
 )
+from . import analytics  # noqa: F401  (on-device analytics.py drop-in)
 from .io import read_head_vector, write_amplitude_tsv, write_head_vector  # noqa: F401
 from .provenance import normalize_s1, provenance_hash  # noqa: F401
 from .workloads import load_workload  # noqa: F401

@@ -72,6 +72,13 @@ EXPORTS = {
     "tnb_program_get_timing": (i32, [P, C.POINTER(Timing)]),
     "tnb_cgemm": (i32, [i32, i64, i64, i64, P, P, P, i32, i32]),
     "tnb_add_tree": (i32, [i32, i32, i64, i32, C.POINTER(P), P]),
+    "tnb_probabilities": (i32, [i32, i32, P, i64, P]),
+    "tnb_prob_reduce": (i32, [i32, P, i64, C.POINTER(f64)]),
+    "tnb_prob_histogram": (i32, [i32, P, i64, f64, C.POINTER(f64), i32, C.POINTER(i64)]),
+    "tnb_prob_sort": (i32, [i32, P, i64, i32]),
+    "tnb_prob_is_sorted_desc": (i32, [i32, P, i64, C.POINTER(i32)]),
+    "tnb_prob_prefix_sums": (i32, [i32, P, i64, C.POINTER(i64), i32, C.POINTER(f64)]),
+    "tnb_prob_ks": (i32, [i32, P, i64, f64, C.POINTER(f64)]),
 }
 
 _lib = None

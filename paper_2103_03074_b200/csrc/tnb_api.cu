@@ -20,6 +20,14 @@ void program_set_leaf_c64(Program* P, int leaf_pos, const float* data);
 void program_run_range(Program* P, uint64_t a, uint64_t b, int mode, void* out, int out_dev);
 void program_set_timing(Program* P, int on);
 void program_get_timing(const Program* P, tnb_timing* t);
+// analytics.cu
+void prob_from_amps(int precision, const void* amps, int64_t n, double* p);
+void prob_reduce(const double* p, int64_t n, double* out4);
+void prob_histogram(const double* p, int64_t n, double scale, const double* edges, int bins, int64_t* counts);
+void prob_sort(double* p, int64_t n, int descending);
+int prob_check_desc(const double* p, int64_t n);
+void prob_prefix_at(const double* p, int64_t n, const int64_t* ks, int nk, double* sums);
+double prob_ks(const double* p_sorted_asc, int64_t n, double scale);
 
 namespace {
 thread_local std::string g_err;
@@ -278,6 +286,67 @@ int tnb_add_tree(int32_t device, int32_t precision, int64_t elems, int32_t n,
     }
     TNB_CUDA(cudaMemcpyAsync(out, res, (size_t)elems * es, cudaMemcpyDeviceToDevice, st));
     TNB_CUDA(cudaStreamSynchronize(st));
+  });
+}
+
+
+// ---- on-device analytics (analytics.py); all pointers are device pointers
+// on `device` unless named *_host
+int tnb_probabilities(int32_t device, int32_t precision, const void* amps, int64_t n, double* probs) {
+  return guarded([&] {
+    if (!amps || !probs || n < 0) throw Error(TNB_ERR_ARG, "bad probabilities arguments");
+    TNB_CUDA(cudaSetDevice(device));
+    if (n) prob_from_amps(precision, amps, n, probs);
+  });
+}
+
+int tnb_prob_reduce(int32_t device, const double* probs, int64_t n, double* out4_host) {
+  return guarded([&] {
+    if (!probs || !out4_host || n <= 0) throw Error(TNB_ERR_ARG, "bad reduce arguments");
+    TNB_CUDA(cudaSetDevice(device));
+    prob_reduce(probs, n, out4_host);
+  });
+}
+
+int tnb_prob_histogram(int32_t device, const double* probs, int64_t n, double scale,
+                       const double* edges_host, int32_t bins, int64_t* counts_host) {
+  return guarded([&] {
+    if (!probs || !edges_host || !counts_host || n <= 0) throw Error(TNB_ERR_ARG, "bad histogram arguments");
+    TNB_CUDA(cudaSetDevice(device));
+    prob_histogram(probs, n, scale, edges_host, bins, counts_host);
+  });
+}
+
+int tnb_prob_sort(int32_t device, double* probs, int64_t n, int32_t descending) {
+  return guarded([&] {
+    if (!probs || n < 0) throw Error(TNB_ERR_ARG, "bad sort arguments");
+    TNB_CUDA(cudaSetDevice(device));
+    if (n > 1) prob_sort(probs, n, descending);
+  });
+}
+
+int tnb_prob_is_sorted_desc(int32_t device, const double* probs, int64_t n, int32_t* sorted_host) {
+  return guarded([&] {
+    if (!probs || !sorted_host || n < 0) throw Error(TNB_ERR_ARG, "bad sortedness arguments");
+    TNB_CUDA(cudaSetDevice(device));
+    *sorted_host = n > 1 ? !prob_check_desc(probs, n) : 1;
+  });
+}
+
+int tnb_prob_prefix_sums(int32_t device, const double* probs, int64_t n, const int64_t* ks_host,
+                         int32_t nk, double* sums_host) {
+  return guarded([&] {
+    if (!probs || !ks_host || !sums_host || n <= 0 || nk <= 0) throw Error(TNB_ERR_ARG, "bad prefix arguments");
+    TNB_CUDA(cudaSetDevice(device));
+    prob_prefix_at(probs, n, ks_host, nk, sums_host);
+  });
+}
+
+int tnb_prob_ks(int32_t device, const double* probs_sorted_asc, int64_t n, double scale, double* out_host) {
+  return guarded([&] {
+    if (!probs_sorted_asc || !out_host || n <= 0) throw Error(TNB_ERR_ARG, "bad ks arguments");
+    TNB_CUDA(cudaSetDevice(device));
+    *out_host = prob_ks(probs_sorted_asc, n, scale);
   });
 }
 

@@ -216,6 +216,25 @@ def clear_cache() -> None:
         _cache.clear()
 
 
+_split_cache: dict = {}
+
+
+def _split(tn, tree):
+    """planner.split memoised per (network, tree) object pair: the split only
+    depends on the topology, and repeated calls on the same objects (slice
+    ranges, tail after head) are common.  The cache holds references to both
+    objects, so an id is never reused while its entry lives."""
+    key = (id(tn), id(tree), len(tree.steps))
+    hit = _split_cache.get(key)
+    if hit is not None and hit[0] is tn and hit[1] is tree:
+        return hit[2]
+    res = split(tn, tree)
+    if len(_split_cache) >= 16:
+        _split_cache.pop(next(iter(_split_cache)))
+    _split_cache[key] = (tn, tree, res)
+    return res
+
+
 def _steps_tuples(steps):
     return [(s.lhs, s.rhs, s.out) for s in steps]
 
@@ -229,7 +248,7 @@ def _leaf_entries(tn, leaf_ids):
 
 def head_program(tn, tree, sliced_indices, precision="single", device=None, flags=None):
     """The compiled head program (for benchmarks / timing introspection)."""
-    head_leaves, head_steps, _, _, cut = split(tn, tree)
+    head_leaves, head_steps, _, _, cut = _split(tn, tree)
     return get_program(_leaf_entries(tn, head_leaves), _steps_tuples(head_steps),
                        list(sliced_indices), sorted(cut), precision, device, flags)
 
@@ -240,7 +259,7 @@ def compute_head_vector(tn, tree, sliced_indices, s1, slice_range=None, precisio
     s1 = normalize_s1(tn, s1)
     tn = tn.repin(s1)
     sliced_indices = list(sliced_indices)
-    head_leaves, head_steps, _, _, cut = split(tn, tree)
+    head_leaves, head_steps, _, _, cut = _split(tn, tree)
     head_set = set(head_leaves)
     for ix in sliced_indices:
         eps = tn.index_endpoints.get(ix, ())
@@ -287,7 +306,7 @@ def _degenerate_sum(count, dtype, mode):
 
 def tail_plan(tn, tree, cut, head_id=None):
     """Leaves + greedy steps of the head-absorbed tail network."""
-    _, _, tail_leaves, _, _ = split(tn, tree)
+    _, _, tail_leaves, _, _ = _split(tn, tree)
     hid = (max(tn.nodes) + 1) if head_id is None else head_id
     sets = {nid: frozenset(tn.nodes[nid].indices) for nid in tail_leaves}
     sets[hid] = frozenset(cut)
@@ -319,7 +338,7 @@ def tail_amplitudes_unchecked(tn, tree, head: HeadVector, space_cap=None, precis
 
 
 def _tail(tn, tree, head, space_cap, precision, stats, device):
-    _, _, tail_leaves, tail_steps, cut = split(tn, tree)
+    _, _, tail_leaves, tail_steps, cut = _split(tn, tree)
     if sorted(cut) != list(head.cut_order):
         raise ProvenanceMismatch("cut indices differ from the head vector's")
     dtype = DTYPES[precision]
