@@ -337,7 +337,7 @@ gemm_f16x3_kernel(const __grid_constant__ CUtensorMap tm_ahi, const __grid_const
                   float* __restrict__ C, int M, int Np, int Kp, int splits, int k_per_split,
                   int chunk_kb, int group_m, const ScaleSrc scale_rows, const ScaleSrc scale_cols,
                   unsigned int* __restrict__ max_out, unsigned int* __restrict__ progress,
-                  int pace_slack, const __grid_constant__ FuseOut fo, int exp_skip) {
+                  int pace_slack, const __grid_constant__ FuseOut fo, int exp_skip, int epi_spin) {
   using CF = Cfg<CG>;
   constexpr int STAGES = CF::STAGES;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -420,14 +420,17 @@ gemm_f16x3_kernel(const __grid_constant__ CUtensorMap tm_ahi, const __grid_const
           }
         }
         if (lane == 0) {
-          mbar_wait_sleep(&empty_bar[stage], phase ^ 1);
+          if (epi_spin & 4) mbar_wait(&empty_bar[stage], phase ^ 1);
+          else mbar_wait_sleep(&empty_bar[stage], phase ^ 1);
           uint8_t* st = smem + stage * CF::STAGE_BYTES;
           // exp_skip (diagnostic only, wrong results): 1 = skip B loads, 2 = skip A loads
-          const uint32_t bytes = exp_skip == 1 ? 2 * A_TILE : exp_skip == 2 ? 2 * CF::B_TILE : CF::STAGE_BYTES;
+          const int kbk = k / BK;
+          // 3 = skip A on odd K blocks (half the A traffic: the bound of sharing A)
+          const bool skip_a = exp_skip == 2 || (exp_skip == 3 && (kbk & 1));
+          const uint32_t bytes = exp_skip == 1 ? 2 * A_TILE : skip_a ? 2 * CF::B_TILE : CF::STAGE_BYTES;
           if (leader) mbar_arrive_expect_tx(&full_bar[stage], CG * bytes);
           else mbar_arrive_remote(&full_bar[stage], 0);
-          const int kbk = k / BK;
-          if (exp_skip != 2) {
+          if (!skip_a) {
             tma_load_tile<CG>(st, &tm_ahi, &full_bar[stage], m0, kbk);
             tma_load_tile<CG>(st + A_TILE, &tm_alo, &full_bar[stage], m0, kbk);
           }
@@ -453,12 +456,14 @@ gemm_f16x3_kernel(const __grid_constant__ CUtensorMap tm_ahi, const __grid_const
         const int nkb = (min(Kp, k_begin + k_per_split) - k_begin + BK - 1) / BK;
         for (int c0 = 0; c0 < nkb; c0 += chunk_kb, ++gchunk) {
           const int buf = gchunk & 1;
-          mbar_wait_sleep(&pempty_bar[buf], ((gchunk >> 1) & 1) ^ 1);
+          if (epi_spin & 2) mbar_wait(&pempty_bar[buf], ((gchunk >> 1) & 1) ^ 1);
+          else mbar_wait_sleep(&pempty_bar[buf], ((gchunk >> 1) & 1) ^ 1);
           tc_fence_after();
           const uint32_t tmem_c = tmem_base + buf * BN;
           const int c1 = min(nkb, c0 + chunk_kb);
           for (int kb = c0; kb < c1; ++kb) {
-            mbar_wait_sleep(&full_bar[stage], phase);
+            if (epi_spin & 2) mbar_wait(&full_bar[stage], phase);
+            else mbar_wait_sleep(&full_bar[stage], phase);
             tc_fence_after();
             if (lane == 0) {
               uint8_t* st = smem + stage * CF::STAGE_BYTES;
@@ -501,7 +506,8 @@ gemm_f16x3_kernel(const __grid_constant__ CUtensorMap tm_ahi, const __grid_const
       for (int j = 0; j < EPI_COLS; ++j) acc[j] = 0.f;
       for (int c0 = 0; c0 < nkb; c0 += chunk_kb, ++gchunk) {
         const int buf = gchunk & 1;
-        mbar_wait_sleep(&pfull_bar[buf], (gchunk >> 1) & 1);
+        if (epi_spin & 1) mbar_wait(&pfull_bar[buf], (gchunk >> 1) & 1);
+        else mbar_wait_sleep(&pfull_bar[buf], (gchunk >> 1) & 1);
         tc_fence_after();
         const uint32_t taddr = tmem_base + ((uint32_t)(q * 32) << 16) + buf * BN + grp * EPI_COLS;
 #pragma unroll
@@ -518,18 +524,25 @@ gemm_f16x3_kernel(const __grid_constant__ CUtensorMap tm_ahi, const __grid_const
       const int row0 = wc.mb * BM * CG + (int)rank * BM + q * 32;
       const int row = row0 + lane;
       const int col0 = wc.nb * BN + grp * EPI_COLS;
+      {
+        // max |C| of the tile (alpha > 0 is a power of two: max|x alpha| = alpha max|x|)
+        float tm = 0.f;
 #pragma unroll
-      for (int j = 0; j < EPI_COLS; ++j) {
-        acc[j] *= alpha;
-        vmax = fmaxf(vmax, fabsf(acc[j]));  // out-of-range rows/cols are TMA zero-fill
+        for (int j = 0; j < EPI_COLS; ++j) tm = fmaxf(tm, fabsf(acc[j]));  // out-of-range rows/cols are TMA zero-fill
+        vmax = fmaxf(vmax, tm * alpha);
+      }
+      if (fo.mode == 0) {
+#pragma unroll
+        for (int j = 0; j < EPI_COLS; ++j) acc[j] *= alpha;
       }
       if (fo.mode != 0) {
         // fused staging: write the consumer's fp16 operand directly
         const int nvalid = min(EPI_COLS / 2, (Np - col0) >> 1);
         if (nvalid > 0) {  // warp-uniform; every row of a 32-row group exists (M >= 128, 2^k)
           const uint32_t tile = lut_lookup(fo.lut_m, (uint32_t)row0) | lut_lookup(fo.lut_n, (uint32_t)(col0 >> 1));
-          if (fo.mode == 1) fused_store<1>(fo, tile, acc, so, nvalid, lane);
-          else fused_store<2>(fo, tile, acc, so, nvalid, lane);
+          // (x alpha) so == x (alpha so) exactly: both are powers of two
+          if (fo.mode == 1) fused_store<1>(fo, tile, acc, alpha * so, nvalid, lane);
+          else fused_store<2>(fo, tile, acc, alpha * so, nvalid, lane);
         }
       } else if (row0 + 32 <= M && col0 + EPI_COLS <= Np) {
         // full 32-row x 64-column block: transpose float4 chunks inside each
@@ -709,7 +722,13 @@ void tc_plan_gemm(TcGemmPlan* p, const __half* Ahi, const __half* Alo, const __h
   if (p->chunk_kb <= 0) p->chunk_kb = 1 << 30;  // no promotion: whole K in TMEM
   p->group_m = env_int("TNB_GROUP_M", GROUP_M);
   if (p->group_m <= 0) p->group_m = 1 << 30;
-  p->pace_slack = env_int("TNB_PACE", kDefaultPaceSlack);
+  // soft pacing keeps long-K tiles inside the L2 window (top C4 GEMM: 75 vs
+  // 343 GB DRAM without it); tiles of few K blocks turn over fast enough for
+  // the raster alone, and there the lockstep costs 6-8% of the cycles
+  static const int pace_min_kb = env_int("TNB_PACE_MIN_KB", 64);
+  p->pace_slack = kblocks / p->splits >= pace_min_kb ? env_int("TNB_PACE", kDefaultPaceSlack) : 0;
+  static const int spin = env_int("TNB_EPI_SPIN", -1);
+  p->epi_spin = spin >= 0 ? spin : 0;
   const int b_rows = BN / p->cta_group;
   make_map(p->tmap[0], Ahi, M, Kp, BM);
   make_map(p->tmap[1], Alo, M, Kp, BM);
@@ -739,7 +758,7 @@ void launch_cg(const TcGemmPlan* p, cudaStream_t s) {
   TNB_CUDA(cudaLaunchKernelEx(&cfg, kern, maps[0], maps[1], maps[2], maps[3], p->C, (int)p->M,
                               (int)p->Np, (int)p->Kp, p->splits, (int)p->k_per_split, p->chunk_kb,
                               p->group_m, p->scale_rows, p->scale_cols, p->max_out, p->progress,
-                              p->pace_slack, p->fuse, env_int("TNB_EXP_SKIP", 0)));
+                              p->pace_slack, p->fuse, env_int("TNB_EXP_SKIP", 0), p->epi_spin));
 }
 
 void tc_launch_gemm(const TcGemmPlan* p, cudaStream_t s) {

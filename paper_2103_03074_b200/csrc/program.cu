@@ -431,12 +431,19 @@ Program* program_create(const tnb_program_desc* d) {
         if (primary < 0) primary = t;
       }
       if (primary < 0) continue;
-      // low K bits: contracted indices on the primary producer's result
-      // columns first (n bits 0,1 -> 16-B vectors), then on its rows
+      // low K bits: k0,k1 on the primary producer's result columns (n bits
+      // 0,1 -> 16-B vectors), k2,k3 on its rows (lane bits: no exchange
+      // needed to put destination bits 2,3 on the lanes); fall back to the
+      // other side when one side has too few contracted indices
       const Pre& pp = pre[def[primary]];
-      std::vector<int64_t> kpri;
-      for (int64_t x : ord_k[c]) if (has(pp.cols, x)) kpri.push_back(x);
-      for (int64_t x : ord_k[c]) if (has(pp.rows, x)) kpri.push_back(x);
+      std::vector<int64_t> kc, kr, kpri;
+      for (int64_t x : ord_k[c]) (has(pp.cols, x) ? kc : kr).push_back(x);
+      size_t ic = 0, ir = 0;
+      for (int slot = 0; slot < 4 && (ic < kc.size() || ir < kr.size()); ++slot) {
+        const bool want_col = slot < 2;
+        if ((want_col && ic < kc.size()) || ir >= kr.size()) kpri.push_back(kc[ic++]);
+        else kpri.push_back(kr[ir++]);
+      }
       reorder(ord_k[c], kpri);
       const size_t L = std::min<size_t>(ord_k[c].size(), (size_t)kKBlockLog);
       for (int r = 0; r < 2; ++r) {
@@ -794,6 +801,7 @@ Program* program_create(const tnb_program_desc* d) {
       for (int p = 0; p < std::min<int>(5, (int)mvec.size()); ++p) fprintf(stderr, " %d", mvec[p]);
       fprintf(stderr, " lane_w");
       for (int b = 0; b < 5; ++b) fprintf(stderr, " %d", f.fast ? ilog2(f.lane_w[b]) : -1);
+      fprintf(stderr, " exchanges %d", (f.xlane[0] != 0) + (f.xlane[1] != 0) + (f.xlane[2] != 0));
       fprintf(stderr, "\n");
     }
     f.hi = (__half2*)P->tensor_ptr(s.out);

@@ -304,13 +304,24 @@ def _degenerate_sum(count, dtype, mode):
     return np.array([float(count)], dtype=dtype)
 
 
+_tail_plan_cache: dict = {}
+
+
 def tail_plan(tn, tree, cut, head_id=None):
-    """Leaves + greedy steps of the head-absorbed tail network."""
+    """Leaves + greedy steps of the head-absorbed tail network (memoised per
+    (network, tree, cut) like ``_split``: the order depends on the topology only)."""
     _, _, tail_leaves, _, _ = _split(tn, tree)
     hid = (max(tn.nodes) + 1) if head_id is None else head_id
+    key = (id(tn), id(tree), tuple(cut), hid)
+    hit = _tail_plan_cache.get(key)
+    if hit is not None and hit[0] is tn and hit[1] is tree:
+        return tail_leaves, hid, hit[2]
     sets = {nid: frozenset(tn.nodes[nid].indices) for nid in tail_leaves}
     sets[hid] = frozenset(cut)
     steps = greedy_steps(sets, hid + 1)
+    if len(_tail_plan_cache) >= 16:
+        _tail_plan_cache.pop(next(iter(_tail_plan_cache)))
+    _tail_plan_cache[key] = (tn, tree, steps)
     return tail_leaves, hid, steps
 
 
