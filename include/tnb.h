@@ -144,7 +144,9 @@ int tnb_program_set_leaf_device(tnb_program* p, int32_t leaf_pos, const void* de
    program's device.  Synchronous. */
 int tnb_program_run_range(tnb_program* p, uint64_t a, uint64_t b, int32_t mode,
                           void* out, int32_t out_on_device);
-/* Enable (1) / disable (0) CUDA-event timing of kernel classes. */
+/* CUDA-event timing of the next run_range calls: 0 off, 1 every kernel class
+   (gemm/convert/simt/other), 2 GEMM launches + the range total only (no
+   event records around the small kernels). */
 int tnb_program_set_timing(tnb_program* p, int32_t enabled);
 int tnb_program_get_timing(const tnb_program* p, tnb_timing* t);
 

@@ -185,7 +185,7 @@ struct Program {
   int64_t reuse_bytes = 0;          // dedicated buffers of cross-slice cached tensors
 
   // timing
-  bool timing = false;
+  int timing = 0;                   // 0 off, 1 all kernel classes, 2 GEMM + total
   tnb_timing last{};
   std::vector<cudaEvent_t> ev_pool;
 
@@ -1000,15 +1000,19 @@ struct RunCtx {
     }
     return P->ev_pool[ev_next++];
   }
-  cudaEvent_t mark() {
-    if (!P->timing) return nullptr;
+  // timing 1: every kernel class; timing 2: GEMM launches + the range total
+  // only (no event records around the hundreds of tiny kernels, whose issue
+  // cost would otherwise show up in the measured time)
+  bool records(int cls) const { return P->timing == 1 || (P->timing == 2 && cls <= 0); }
+  cudaEvent_t mark(int cls = -1) {
+    if (!records(cls)) return nullptr;
     cudaEvent_t e = get();
     TNB_CUDA(cudaEventRecord(e, P->stream));
     return e;
   }
   void close(int cls, cudaEvent_t a) {
-    if (!P->timing) return;
-    cudaEvent_t b = mark();
+    if (!a || !records(cls)) return;
+    cudaEvent_t b = mark(cls);
     recs.push_back({cls, a, b});
   }
 };
@@ -1019,7 +1023,7 @@ template <typename T>
 void exec_step(Program* P, StepRec& s) {
   RunCtx& C = *g_ctx;
   if (s.kind == KIND_SIMT) {
-    cudaEvent_t e = C.mark();
+    cudaEvent_t e = C.mark(2);
     launch_contract_simt<T>((const T*)P->tensor_ptr(s.a), (const T*)P->tensor_ptr(s.b),
                             (T*)P->tensor_ptr(s.out), s.M, s.N, s.K, P->d_luts + s.lut_a,
                             P->d_luts + s.lut_b,
@@ -1041,7 +1045,7 @@ void exec_step(Program* P, StepRec& s) {
     __half* bhi = (__half*)(base + (s.fuse_rows ? 0 : 2 * s.M * Kp * 2));
     __half* blo = bhi + Np * Kp;
     cudaEvent_t e = nullptr;
-    if (!s.fuse_rows || !s.fuse_cols) e = C.mark();
+    if (!s.fuse_rows || !s.fuse_cols) e = C.mark(1);
     if (!s.fuse_rows) {
       launch_stage(rows, P->stages[s.st_rows], s.K, false, P->d_tmax + P->slot[s.rows_t], ahi, alo, P->stream);
       C.launches++;
@@ -1051,14 +1055,14 @@ void exec_step(Program* P, StepRec& s) {
       C.launches++;
     }
     if (!s.fuse_rows || !s.fuse_cols) C.close(1, e);
-    e = C.mark();
+    e = C.mark(0);
     tc_launch_gemm(&s.tc, P->stream);
     C.close(0, e);
     C.launches += 1;
     C.gemm_launches++;
     C.gemm_flops += 8.0 * s.mults;
     if (s.tc.splits > 1) {
-      e = C.mark();
+      e = C.mark(1);
       launch_splitk_reduce(s.tc.C, s.tc.splits, s.M * Np, (float*)P->tensor_ptr(s.out),
                            s.tc.scale_rows, s.tc.scale_cols, s.tc.max_out, P->stream);
       C.close(1, e);
@@ -1082,7 +1086,7 @@ void run_range_t(Program* P, uint64_t a, uint64_t b, int mode, void* out, bool o
   auto slot = [&](int i) { return slots + (size_t)i * slot_stride; };
   T* total_slot = slot(P->n_sliced + 1);
   T* perm_slot = slot(P->n_sliced + 2);
-  cudaEvent_t t_start = ctx.mark();
+  cudaEvent_t t_start = ctx.mark(-1);
 
   // hoisted slice-invariant steps (once per leaf-data version)
   if (!P->invariant_valid) {
@@ -1100,7 +1104,7 @@ void run_range_t(Program* P, uint64_t a, uint64_t b, int mode, void* out, bool o
   uint64_t count = 0;
   const T* root_ptr = (const T*)P->tensor_ptr(P->root);
   for (uint64_t mask = a; mask < b; ++mask) {
-    cudaEvent_t e = ctx.mark();
+    cudaEvent_t e = ctx.mark(3);
     launch_prepare_leaves<T>((const T*)P->d_leaf_pool, (T*)P->d_slice_pool, P->d_sl_descs,
                              P->n_sl_descs, P->d_keep, mask, st);
     if (P->n_sl_descs) ctx.launches++;
@@ -1124,7 +1128,7 @@ void run_range_t(Program* P, uint64_t a, uint64_t b, int mode, void* out, bool o
         s.last_key = key;
       }
     }
-    e = ctx.mark();
+    e = ctx.mark(3);
     if (mode == TNB_FIXED) {
       // binary-counter increment: the new chunk merges with the levels
       // 0..merges-1 (x = prev + x, lowest level first) -> level `merges`
@@ -1142,7 +1146,7 @@ void run_range_t(Program* P, uint64_t a, uint64_t b, int mode, void* out, bool o
     ctx.close(3, e);
     ++count;
   }
-  cudaEvent_t e = ctx.mark();
+  cudaEvent_t e = ctx.mark(3);
   const T* result = total_slot;
   if (mode == TNB_FIXED) {
     // total = stack[0] (highest level) + stack[1] + ... (engine.py:218-221)
@@ -1166,7 +1170,7 @@ void run_range_t(Program* P, uint64_t a, uint64_t b, int mode, void* out, bool o
   } else {
     TNB_CUDA(cudaMemcpyAsync(out, result, (size_t)E * sizeof(T), cudaMemcpyDeviceToHost, st));
   }
-  cudaEvent_t t_end = ctx.mark();
+  cudaEvent_t t_end = ctx.mark(-1);
   TNB_CUDA(cudaStreamSynchronize(st));
   if (std::is_same<T, float2>::value && getenv("TNB_DEBUG_MAX")) {
     // diagnostic: per-step output max vs the a-priori bound 2 K max|A| max|B|
@@ -1215,7 +1219,7 @@ void program_run_range(Program* P, uint64_t a, uint64_t b, int mode, void* out, 
   else run_range_t<double2>(P, a, b, mode, out, out_dev != 0);
 }
 
-void program_set_timing(Program* P, int on) { P->timing = on != 0; }
+void program_set_timing(Program* P, int on) { P->timing = on < 0 ? 0 : (on > 2 ? 1 : on); }
 void program_get_timing(const Program* P, tnb_timing* t) { *t = P->last; }
 
 }  // namespace tnb

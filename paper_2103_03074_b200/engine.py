@@ -160,8 +160,10 @@ class Program:
                 self.handle, a, b, _MODES[mode], C.c_void_p(out), 1))
             return None
 
-    def set_timing(self, on: bool) -> None:
-        _lib.check(self.lib.tnb_program_set_timing(self.handle, 1 if on else 0))
+    def set_timing(self, on) -> None:
+        """False/0 off, True/1 every kernel class, 2 GEMM launches + total only."""
+        mode = (1 if on else 0) if isinstance(on, bool) else int(on)
+        _lib.check(self.lib.tnb_program_set_timing(self.handle, mode))
 
     def timing(self) -> dict:
         t = _lib.Timing()
