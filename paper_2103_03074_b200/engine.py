@@ -152,7 +152,7 @@ class Program:
         """Host result (numpy) unless ``out`` is a device pointer (int)."""
         with self.lock:
             if out is None:
-                res = np.empty(self.info.out_elems, dtype=self.dtype)
+                res = _host_array(self.info.out_elems, self.dtype)
                 _lib.check(self.lib.tnb_program_run_range(
                     self.handle, a, b, _MODES[mode], res.ctypes.data_as(C.c_void_p), 0))
                 return res
@@ -169,6 +169,26 @@ class Program:
         t = _lib.Timing()
         _lib.check(self.lib.tnb_program_get_timing(self.handle, C.byref(t)))
         return {f: getattr(t, f) for f, _ in _lib.Timing._fields_}
+
+
+_PIN_MIN_BYTES = 1 << 20
+
+
+def _host_array(n: int, dtype) -> np.ndarray:
+    """Result buffer for a device->host copy: page-locked (pinned) host memory
+    for large results -- the copy then runs at full PCIe/C2C speed instead of
+    through the driver's pageable staging -- exposed as a plain numpy array
+    (the torch tensor owning the pinned block is kept alive as its base)."""
+    nbytes = int(n) * np.dtype(dtype).itemsize
+    if nbytes >= _PIN_MIN_BYTES:
+        try:
+            import torch
+
+            tdt = torch.complex64 if np.dtype(dtype) == np.complex64 else torch.complex128
+            return torch.empty(int(n), dtype=tdt, pin_memory=True).numpy()
+        except Exception:  # pinning is an optimisation only
+            pass
+    return np.empty(int(n), dtype=dtype)
 
 
 _cache: dict = {}
