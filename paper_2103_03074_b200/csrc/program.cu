@@ -352,8 +352,13 @@ Program* program_create(const tnb_program_desc* d) {
   // lowest free bits) are its thread-local columns / lane-local rows -- the
   // epilogue's scattered stores then form contiguous runs.  Lists below are
   // lowest-first (canonical bit 0 first).
+  // tensor-core eligibility: big enough to fill 128x256 tiles and amortise
+  // staging.  TNB_TC_MIN_RANK (read per program; tests lower it so small
+  // random networks exercise the tensor-core and fused-staging paths)
+  const int tc_min_rank = env_int("TNB_TC_MIN_RANK", 27);
   auto tc_eligible = [&](int na, int nb, int nab) {
-    return use_tc && nab >= 3 && na + nb + nab >= 27 && std::max(na, nb) >= 7 && std::min(na, nb) >= 3;
+    return use_tc && nab >= 3 && na + nb + nab >= tc_min_rank && std::max(na, nb) >= 7 &&
+           std::min(na, nb) >= 3;
   };
   std::vector<std::vector<int64_t>> ord_k(d->n_steps), ord_rows(d->n_steps), ord_cols(d->n_steps);
   std::vector<int> fuse_role_pre;                           // tensor -> 1/2 when fused
@@ -493,9 +498,7 @@ Program* program_create(const tnb_program_desc* d) {
     s.M = (int64_t)1 << na;
     s.N = (int64_t)1 << nb;
     s.K = (int64_t)1 << nab;
-    // tensor-core eligibility: big enough to fill 128x256 tiles and amortise staging
-    bool tc = use_tc && nab >= 3 && na + nb + nab >= 27 && std::max(na, nb) >= 7 &&
-              std::min(na, nb) >= 3;
+    const bool tc = tc_eligible(na, nb, nab);
     if (tc) {
       // expand the smaller operand (B' doubles its size); rows = the other one
       const bool rows_is_a = ((int64_t)1 << (na + nab)) >= ((int64_t)1 << (nb + nab));
