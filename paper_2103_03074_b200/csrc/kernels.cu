@@ -147,18 +147,76 @@ contract_simt_kernel(const T* __restrict__ A, const T* __restrict__ B, T* __rest
 // thread produces 4 consecutive output columns of one row with two 16-byte
 // (float2) or four 16-byte (double2) stores, so the kernel runs at HBM write
 // speed instead of the 32x32-tile kernel's padded K loop.
+__device__ __forceinline__ void split2(float a, float b, __half2& hi, __half2& lo);
+
+// fused output of the small-K kernel: C[m][n0..n0+3] as the tensor-core
+// consumer's staged operand (see FuseOut / gemm_tc.cu fused_store)
+__device__ __forceinline__ void smallk_fused_store(const FuseOut& fo, const uint32_t (*fm)[256],
+                                                   const uint32_t (*fn)[256], int64_t m, int64_t n0,
+                                                   const float* re, const float* im, float so) {
+  const uint32_t base = lut_map(fm, (uint32_t)m) | lut_map(fn, (uint32_t)n0);
+  if (fo.vec) {  // n bits 0,1 are destination bits 0,1: 16-B stores
+    if (fo.mode == 1) {
+      __half2 h[4], o[4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) split2(re[j] * so, im[j] * so, h[j], o[j]);
+      *reinterpret_cast<uint4*>(fo.hi + base) = *reinterpret_cast<const uint4*>(h);
+      *reinterpret_cast<uint4*>(fo.lo + base) = *reinterpret_cast<const uint4*>(o);
+    } else {
+      __half2 h0[4], o0[4], h1[4], o1[4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        split2(re[j] * so, -im[j] * so, h0[j], o0[j]);
+        split2(im[j] * so, re[j] * so, h1[j], o1[j]);
+      }
+      const uint32_t b1 = base + (1u << fo.L);
+      *reinterpret_cast<uint4*>(fo.hi + base) = *reinterpret_cast<const uint4*>(h0);
+      *reinterpret_cast<uint4*>(fo.lo + base) = *reinterpret_cast<const uint4*>(o0);
+      *reinterpret_cast<uint4*>(fo.hi + b1) = *reinterpret_cast<const uint4*>(h1);
+      *reinterpret_cast<uint4*>(fo.lo + b1) = *reinterpret_cast<const uint4*>(o1);
+    }
+    return;
+  }
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const uint32_t a = base | fo.dlow[j];
+    if (fo.mode == 1) {
+      __half2 h, o;
+      split2(re[j] * so, im[j] * so, h, o);
+      fo.hi[a] = h;
+      fo.lo[a] = o;
+    } else {
+      __half2 h0, o0, h1, o1;
+      split2(re[j] * so, -im[j] * so, h0, o0);
+      split2(im[j] * so, re[j] * so, h1, o1);
+      const uint32_t a1 = a + (1u << fo.L);
+      fo.hi[a] = h0; fo.lo[a] = o0;
+      fo.hi[a1] = h1; fo.lo[a1] = o1;
+    }
+  }
+}
+
 template <typename T>
 __global__ void __launch_bounds__(256)
 contract_smallk_kernel(const T* __restrict__ A, const T* __restrict__ B, T* __restrict__ C,
                        int64_t M, int64_t N, int K, const ByteLut* __restrict__ gla,
-                       const ByteLut* __restrict__ glb, unsigned int* __restrict__ max_out) {
+                       const ByteLut* __restrict__ glb, unsigned int* __restrict__ max_out,
+                       const __grid_constant__ FuseOut fo) {
   using S = typename Scalar<T>::type;
   __shared__ uint32_t la[4][256];
   __shared__ uint32_t lb[4][256];
+  __shared__ uint32_t fm[4][256];
+  __shared__ uint32_t fn[4][256];
+  const bool fused = std::is_same<T, float2>::value && fo.mode != 0;
   for (int i = threadIdx.x; i < 1024; i += 256) {
     la[i >> 8][i & 255] = gla->t[i >> 8][i & 255];
     lb[i >> 8][i & 255] = glb->t[i >> 8][i & 255];
+    if (fused) {
+      fm[i >> 8][i & 255] = fo.lut_m->t[i >> 8][i & 255];
+      fn[i >> 8][i & 255] = fo.lut_n->t[i >> 8][i & 255];
+    }
   }
+  const float so = fused ? scale_from_src(fo.scale) : 1.f;
   __syncthreads();
   const int64_t nq = N >> 2;
   const int64_t total = M * nq;
@@ -176,12 +234,19 @@ contract_smallk_kernel(const T* __restrict__ A, const T* __restrict__ B, T* __re
         im[j] += a.x * b.y + a.y * b.x;
       }
     }
+#pragma unroll
+    for (int j = 0; j < 4; ++j) vmax = fmaxf(vmax, (float)fmax(fabs(re[j]), fabs(im[j])));
+    if constexpr (std::is_same<T, float2>::value) {
+      if (fused) {
+        smallk_fused_store(fo, fm, fn, m, n0, re, im, so);
+        continue;
+      }
+    }
     T* dst = C + m * N + n0;
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
       T v; v.x = re[j]; v.y = im[j];
       dst[j] = v;
-      vmax = fmaxf(vmax, (float)fmax(fabs(v.x), fabs(v.y)));
     }
   }
   if (max_out) block_max_atomic(vmax, max_out);
@@ -478,14 +543,16 @@ void launch_prepare_leaves(const T* leaf_pool, T* slice_pool, const SlicedLeafDe
 template <typename T>
 void launch_contract_simt(const T* A, const T* B, T* C, int64_t M, int64_t N, int64_t K,
                           const ByteLut* lutA, const ByteLut* lutB, unsigned int* max_out,
-                          cudaStream_t s) {
-  if (K <= 8 && N >= 4 && M * N >= (1 << 16)) {
+                          const FuseOut* fuse, cudaStream_t s) {
+  if (simt_uses_smallk(M, N, K)) {
     // outer-product-like: stream the output
+    const FuseOut fo = fuse ? *fuse : FuseOut{};
     contract_smallk_kernel<T><<<grid_for(M * (N >> 2), 256), 256, 0, s>>>(A, B, C, M, N, (int)K, lutA,
-                                                                            lutB, max_out);
+                                                                            lutB, max_out, fo);
     check_launch("contract_smallk");
     return;
   }
+  if (fuse && fuse->mode != 0) throw Error(TNB_ERR_SHAPE, "fused output planned for a tiled SIMT step");
   const int64_t blocks = ((M + 31) / 32) * ((N + 31) / 32);
   if (blocks > 0x7fffffffll) throw Error(TNB_ERR_SHAPE, "SIMT contraction too large");
   contract_simt_kernel<T><<<(unsigned)blocks, 256, 0, s>>>(A, B, C, M, N, K, lutA, lutB, max_out);
@@ -651,7 +718,7 @@ void launch_splitk_reduce(const float* ws, int splits, int64_t elems, float* C,
                                          const uint32_t*, uint64_t, cudaStream_t);         \
   template void launch_contract_simt<T>(const T*, const T*, T*, int64_t, int64_t, int64_t, \
                                         const ByteLut*, const ByteLut*, unsigned int*,     \
-                                        cudaStream_t);                                     \
+                                        const FuseOut*, cudaStream_t);                     \
   template void launch_permute<T>(const T*, T*, int64_t, const ByteLut*, cudaStream_t);    \
   template void launch_counter_merge<T>(const T*, const T*, int64_t, int, T*, int64_t, cudaStream_t); \
   template void launch_add<T>(const T*, const T*, T*, int64_t, cudaStream_t);              \

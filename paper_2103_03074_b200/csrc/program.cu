@@ -126,7 +126,8 @@ struct StepRec {
   double mults = 0;
   int64_t scratch_off = 0, scratch_bytes = 0;  // TC: staging region in the arena (bytes)
   bool fuse_rows = false, fuse_cols = false;   // TC: operand written by its producer's epilogue
-  int fuse_consumer = -1;                      // TC: step whose operand this step's epilogue writes
+  int fuse_consumer = -1;                      // step whose operand this step's output is written as
+  FuseOut simt_fuse;                           // SIMT (small-K) producer: fused output map
   TcGemmPlan tc;
 };
 
@@ -361,6 +362,7 @@ Program* program_create(const tnb_program_desc* d) {
            std::min(na, nb) >= 3;
   };
   std::vector<std::vector<int64_t>> ord_k(d->n_steps), ord_rows(d->n_steps), ord_cols(d->n_steps);
+  std::vector<char> pre_rows_is_a(d->n_steps, 1);  // SIMT small-K producer: m/n roles swapped if 0
   std::vector<int> fuse_role_pre;                           // tensor -> 1/2 when fused
   std::vector<int> fuse_consumer_pre;                       // tensor -> consuming step
   {
@@ -374,7 +376,11 @@ Program* program_create(const tnb_program_desc* d) {
     for (int i = 0; i < d->n_leaves; ++i) sets[i] = P->tensors[i].axes;
     std::unordered_map<int64_t, int> ids;
     for (int i = 0; i < d->n_leaves; ++i) ids[d->leaf_ids[i]] = i;
-    struct Pre { int a = -1, b = -1; bool tc = false, rows_is_a = true; std::vector<int64_t> shared, rows, cols; };
+    // rows/cols: the GEMM's M/N sides (tensor-core steps: rows = larger
+    // operand's free indices; SIMT steps: rows = a's, cols = b's, the m/n of
+    // the SIMT kernels).  smallk: a SIMT step on the streaming small-K kernel
+    // (launch_contract_simt), whose result may also be written fused.
+    struct Pre { int a = -1, b = -1; bool tc = false, smallk = false, rows_is_a = true; std::vector<int64_t> shared, rows, cols; };
     std::vector<Pre> pre(d->n_steps);
     for (int i = 0; i < d->n_steps; ++i) {
       auto ia = ids.find(d->steps[3 * i]), ib = ids.find(d->steps[3 * i + 1]);
@@ -392,7 +398,8 @@ Program* program_create(const tnb_program_desc* d) {
       for (int64_t x : B) if (std::find(A.begin(), A.end(), x) == A.end()) bfree.push_back(x);
       const int na = (int)afree.size(), nb = (int)bfree.size(), nab = (int)q.shared.size();
       q.tc = tc_eligible(na, nb, nab);
-      q.rows_is_a = na >= nb;
+      q.rows_is_a = q.tc ? na >= nb : true;
+      q.smallk = use_tc && !q.tc && simt_uses_smallk((int64_t)1 << na, (int64_t)1 << nb, (int64_t)1 << nab);
       q.rows = q.rows_is_a ? afree : bfree;
       q.cols = q.rows_is_a ? bfree : afree;
       ord_k[i].assign(q.shared.rbegin(), q.shared.rend());
@@ -407,8 +414,9 @@ Program* program_create(const tnb_program_desc* d) {
     }
     fuse_role_pre.assign(nt, 0);
     fuse_consumer_pre.assign(nt, -1);
-    auto unsplit_tc = [&](int s) {
+    auto fusable_producer = [&](int s) {
       const Pre& q = pre[s];
+      if (q.smallk) return true;
       if (!q.tc) return false;
       const int64_t M = (int64_t)1 << q.rows.size(), N = (int64_t)1 << q.cols.size();
       return tc_splits(M, 2 * N, 2 * ((int64_t)1 << q.shared.size()), P->num_sms) == 1;
@@ -422,6 +430,11 @@ Program* program_create(const tnb_program_desc* d) {
       list.swap(out);
     };
     const bool fuse = fuse_env && !(d->flags & TNB_FLAG_NO_FUSE);
+    struct Commit {  // copy the per-step role decisions out of the pre-pass
+      std::vector<Pre>& pre;
+      std::vector<char>& out;
+      ~Commit() { for (size_t i = 0; i < pre.size(); ++i) out[i] = pre[i].rows_is_a ? 1 : 0; }
+    } commit{pre, pre_rows_is_a};
     for (int c = d->n_steps - 1; fuse && c >= 0; --c) {
       const Pre& q = pre[c];
       if (!q.tc) continue;
@@ -430,22 +443,44 @@ Program* program_create(const tnb_program_desc* d) {
       int primary = -1;
       for (int r = 0; r < 2; ++r) {
         const int t = ops[r];
-        if (def[t] < 0 || !unsplit_tc(def[t])) continue;
+        if (def[t] < 0 || !fusable_producer(def[t])) continue;
         fuse_role_pre[t] = r + 1;
         fuse_consumer_pre[t] = c;
         if (primary < 0) primary = t;
       }
       if (primary < 0) continue;
+      // a small-K producer computes C[m][n] over gathered layouts, so its
+      // m/n roles are free: put the side holding more of this consumer's
+      // contracted indices on the columns (its thread-/warp-local bits)
+      for (int t : ops) {
+        const int p = def[t] >= 0 ? def[t] : -1;
+        if (p < 0 || !fuse_role_pre[t] || !pre[p].smallk || pre[p].tc) continue;
+        auto cnt = [&](const std::vector<int64_t>& side) {
+          int n = 0;
+          for (int64_t x : side) n += has(q.shared, x) ? 1 : 0;
+          return n;
+        };
+        Pre& pq = pre[p];
+        if (cnt(pq.rows) > cnt(pq.cols) &&
+            simt_uses_smallk((int64_t)1 << pq.cols.size(), (int64_t)1 << pq.rows.size(),
+                             (int64_t)1 << pq.shared.size())) {
+          std::swap(pq.rows, pq.cols);
+          std::swap(ord_rows[p], ord_cols[p]);
+          pq.rows_is_a = false;  // SIMT: rows = b's free indices
+        }
+      }
       // low K bits: k0,k1 on the primary producer's result columns (n bits
       // 0,1 -> 16-B vectors), k2,k3 on its rows (lane bits: no exchange
       // needed to put destination bits 2,3 on the lanes); fall back to the
       // other side when one side has too few contracted indices
+      // (a small-K SIMT producer's thread-/warp-local bits are all columns:
+      // 4 per thread, 128 per warp, so every low K bit goes there first)
       const Pre& pp = pre[def[primary]];
       std::vector<int64_t> kc, kr, kpri;
       for (int64_t x : ord_k[c]) (has(pp.cols, x) ? kc : kr).push_back(x);
       size_t ic = 0, ir = 0;
       for (int slot = 0; slot < 4 && (ic < kc.size() || ir < kr.size()); ++slot) {
-        const bool want_col = slot < 2;
+        const bool want_col = slot < 2 || pp.smallk;
         if ((want_col && ic < kc.size()) || ir >= kr.size()) kpri.push_back(kc[ic++]);
         else kpri.push_back(kr[ir++]);
       }
@@ -459,8 +494,25 @@ Program* program_create(const tnb_program_desc* d) {
         std::vector<int64_t> pri(ord_k[c].begin(), ord_k[c].begin() + L);
         const auto& side = r == 0 ? ord_rows[c] : ord_cols[c];
         pri.insert(pri.end(), side.begin(), side.end());
-        reorder(ord_cols[def[t]], pri);
-        reorder(ord_rows[def[t]], pri);
+        const int p = def[t];
+        reorder(ord_cols[p], pri);
+        reorder(ord_rows[p], pri);
+        if (pre[p].smallk && !pre[p].tc) {
+          // a small-K producer's warp writes 32 lanes x 4 consecutive columns:
+          // fuse only if its lowest columns are the consumer's lowest
+          // destination bits (k0..k3, then -- rows operand -- the first row
+          // bit), so a warp store covers whole 128-B lines; small results
+          // are fused regardless (their staging launch costs more)
+          const auto& pc = ord_cols[p];
+          const size_t need = L;  // 64-B runs per 4 lanes
+          bool good = L == (size_t)kKBlockLog && pc.size() >= need + 2;
+          for (size_t x = 0; good && x < need; ++x) good = pc[x] == pri[x];
+          const size_t bits = pre[p].rows.size() + pre[p].cols.size();
+          if (!good && bits > 20) {
+            fuse_role_pre[t] = 0;
+            fuse_consumer_pre[t] = -1;
+          }
+        }
       }
     }
   }
@@ -529,9 +581,28 @@ Program* program_create(const tnb_program_desc* d) {
       }
     } else {
       s.kind = KIND_SIMT;
+      if (fuse_role_pre[(int)P->tensors.size()]) {
+        // fused small-K producer: planned free orders; rows = a's free
+        // indices unless the pre-pass swapped the kernel's m/n roles
+        const bool swapped = !pre_rows_is_a[i];
+        auto& mfree = swapped ? bfree : afree;
+        auto& nfree = swapped ? afree : bfree;
+        if (ord_rows[i].size() != mfree.size() || ord_cols[i].size() != nfree.size())
+          throw Error(TNB_ERR_SHAPE, "order planning mismatch");
+        mfree.assign(ord_rows[i].rbegin(), ord_rows[i].rend());
+        nfree.assign(ord_cols[i].rbegin(), ord_cols[i].rend());
+        if (swapped) {  // C[m over b][n over a] = B A
+          std::swap(s.a, s.b);
+          std::swap(afree, bfree);
+          s.M = (int64_t)1 << afree.size();
+          s.N = (int64_t)1 << bfree.size();
+        }
+      }
+      const TensorRec& SA = P->tensors[s.a];
+      const TensorRec& SB = P->tensors[s.b];
       o.axes = afree; o.axes.insert(o.axes.end(), bfree.begin(), bfree.end());
-      s.lut_a = add_lut(P.get(), canon_bits(A.axes, afree, shared));
-      s.lut_b = add_lut(P.get(), canon_bits(B.axes, bfree, shared));
+      s.lut_a = add_lut(P.get(), canon_bits(SA.axes, afree, shared));
+      s.lut_b = add_lut(P.get(), canon_bits(SB.axes, bfree, shared));
     }
     if (o.axes.size() > 32) throw Error(TNB_ERR_SHAPE, "intermediate rank above 32");
     o.elems = (int64_t)1 << o.axes.size();
@@ -705,8 +776,8 @@ Program* program_create(const tnb_program_desc* d) {
     const TensorRec& r = P->tensors[t];
     if (r.fuse_role != 0) {
       const StepRec& p = P->steps[r.def_step];
-      sc.a = P->d_tmax + P->slot[p.rows_t];
-      sc.b = P->d_tmax + P->slot[p.cols_t];
+      sc.a = P->d_tmax + P->slot[p.kind == KIND_TC ? p.rows_t : p.a];
+      sc.b = P->d_tmax + P->slot[p.kind == KIND_TC ? p.cols_t : p.b];
       sc.f = (float)(2.0 * (double)p.K);
     } else {
       sc.a = P->d_tmax + P->slot[t];
@@ -715,9 +786,72 @@ Program* program_create(const tnb_program_desc* d) {
   };
   std::vector<ByteLut> fuse_luts;
   std::vector<int> fuse_lut_step;
+  // destination map of a fused result in its consumer's operand layout
+  // (stage_kernel's): canonical (row r, k) -> half2 index (k >> L, r,
+  // k & (2^L-1)) in [K/2^L][rows][2^L], a zero bit inserted at L for the
+  // expanded cols operand.  Returns the destination bit of every result
+  // column bit (nvec) and row bit (mvec); fills everything but the kernel-
+  // specific store-path fields.
+  auto build_fuse_map = [&](int i, StepRec& s, FuseOut& f, std::vector<int>& nvec, std::vector<int>& mvec) {
+    const TensorRec& o = P->tensors[s.out];
+    const StepRec& c = P->steps[s.fuse_consumer];
+    const bool as_rows = o.fuse_role == 1;
+    const std::vector<int>& canon = as_rows ? c.canon_rows : c.canon_cols;
+    const int nk = ilog2(c.K), nr = ilog2(as_rows ? c.M : c.N);
+    const int L = std::min(nk, kKBlockLog);
+    const int nbits = (int)o.axes.size();
+    if (nbits != nk + nr || (int)canon.size() != nbits) throw Error(TNB_ERR_SHAPE, "fused staging: rank mismatch");
+    std::vector<int> dbit(nbits);
+    for (int p = 0; p < nbits; ++p) {
+      int db = p < L ? p : (p < nk ? p + nr : p - nk + L);
+      if (!as_rows && db >= L) db += 1;
+      dbit[canon[p]] = db;
+    }
+    const int ln = ilog2(s.N);  // result columns = the low source bits
+    nvec.assign(dbit.begin(), dbit.begin() + ln);
+    mvec.assign(dbit.begin() + ln, dbit.end());
+    f.mode = as_rows ? 1 : 2;
+    f.L = L;
+    for (int j = 0; j < 32; ++j) {
+      uint32_t v = 0;
+      for (int p = 0; p < std::min(5, ln); ++p)
+        if ((j >> p) & 1) v |= 1u << nvec[p];
+      f.dlow[j] = v;
+    }
+    f.hi = (__half2*)P->tensor_ptr(s.out);
+    f.lo = f.hi + (as_rows ? c.M * c.K : 2 * c.N * c.K);
+    f.scale = operand_scale(s.out);
+    fuse_luts.emplace_back();
+    build_lut(mvec, &fuse_luts.back());
+    fuse_luts.emplace_back();
+    build_lut(nvec, &fuse_luts.back());
+    fuse_lut_step.push_back(i);
+  };
+  auto debug_fuse = [&](int i, const StepRec& s, const FuseOut& f, const std::vector<int>& nvec,
+                        const std::vector<int>& mvec) {
+    if (!getenv("TNB_DEBUG_FUSE")) return;
+    fprintf(stderr, "TNB_FUSE step %d (%s) -> %d role %d out 2^%d fast %d vec %d nvec[0..4]", i,
+            s.kind == KIND_TC ? "tc" : "smallk", s.fuse_consumer, f.mode, (int)(nvec.size() + mvec.size()),
+            f.fast, f.vec);
+    for (size_t p = 0; p < std::min<size_t>(5, nvec.size()); ++p) fprintf(stderr, " %d", nvec[p]);
+    fprintf(stderr, " mvec[0..4]");
+    for (size_t p = 0; p < std::min<size_t>(5, mvec.size()); ++p) fprintf(stderr, " %d", mvec[p]);
+    fprintf(stderr, " lane_w");
+    for (int b = 0; b < 5; ++b) fprintf(stderr, " %d", f.fast ? ilog2(f.lane_w[b]) : -1);
+    fprintf(stderr, " exchanges %d\n", (f.xlane[0] != 0) + (f.xlane[1] != 0) + (f.xlane[2] != 0));
+  };
   for (int i = 0; i < n_steps; ++i) {
     StepRec& s = P->steps[i];
-    if (s.kind != KIND_TC) continue;
+    std::vector<int> nvec, mvec;
+    if (s.kind != KIND_TC) {
+      if (P->tensors[s.out].fuse_role == 0) continue;
+      // fused small-K SIMT producer: a thread owns 4 consecutive columns
+      if (!simt_uses_smallk(s.M, s.N, s.K)) throw Error(TNB_ERR_SHAPE, "fused output on a tiled SIMT step");
+      build_fuse_map(i, s, s.simt_fuse, nvec, mvec);
+      s.simt_fuse.vec = nvec.size() >= 2 && nvec[0] == 0 && nvec[1] == 1;
+      debug_fuse(i, s, s.simt_fuse, nvec, mvec);
+      continue;
+    }
     const int64_t Kp = 2 * s.K, Np = 2 * s.N;
     char* base = (char*)P->d_arena + s.scratch_off;
     int64_t used = 0;
@@ -733,30 +867,11 @@ Program* program_create(const tnb_program_desc* d) {
                  operand_scale(s.rows_t), operand_scale(s.cols_t), P->d_tmax + P->slot[s.out],
                  P->num_sms);
     s.tc.progress = P->d_progress;
-    const TensorRec& o = P->tensors[s.out];
-    if (o.fuse_role == 0) continue;
+    if (P->tensors[s.out].fuse_role == 0) continue;
     if (s.tc.splits != 1) throw Error(TNB_ERR_SHAPE, "fused staging planned for a split-K step");
-    // destination map of the consumer's operand layout (stage_kernel's):
-    // canonical (row r, k) -> half2 index (k >> L, r, k & (2^L-1)) in
-    // [K/2^L][rows][2^L], a zero bit inserted at L for the expanded cols
-    const StepRec& c = P->steps[s.fuse_consumer];
-    const bool as_rows = o.fuse_role == 1;
-    const std::vector<int>& canon = as_rows ? c.canon_rows : c.canon_cols;
-    const int nk = ilog2(c.K), nr = ilog2(as_rows ? c.M : c.N);
-    const int L = std::min(nk, kKBlockLog);
-    const int nbits = (int)o.axes.size();
-    if (nbits != nk + nr || (int)canon.size() != nbits) throw Error(TNB_ERR_SHAPE, "fused staging: rank mismatch");
-    std::vector<int> dbit(nbits);
-    for (int p = 0; p < nbits; ++p) {
-      int db = p < L ? p : (p < nk ? p + nr : p - nk + L);
-      if (!as_rows && db >= L) db += 1;
-      dbit[canon[p]] = db;
-    }
-    const int ln = ilog2(s.N);  // complex result columns = the low source bits
-    std::vector<int> nvec(dbit.begin(), dbit.begin() + ln), mvec(dbit.begin() + ln, dbit.end());
     FuseOut& f = s.tc.fuse;
-    f.mode = as_rows ? 1 : 2;
-    f.L = L;
+    build_fuse_map(i, s, f, nvec, mvec);
+    const int ln = (int)nvec.size();
     // fast path: vector bits n0,n1 -> destination bits 0,1; the lanes take
     // the 5 thread-local source bits (slot bits n2..n4, lane bits m0..m4)
     // with the lowest destination bits, swapped in by butterfly exchanges
@@ -790,31 +905,7 @@ Program* program_create(const tnb_program_desc* d) {
       }
       f.fast = 1;
     }
-    for (int j = 0; j < 32; ++j) {
-      uint32_t v = 0;
-      for (int p = 0; p < std::min(5, ln); ++p)
-        if ((j >> p) & 1) v |= 1u << nvec[p];
-      f.dlow[j] = v;
-    }
-    if (getenv("TNB_DEBUG_FUSE")) {
-      fprintf(stderr, "TNB_FUSE step %d -> %d role %d out 2^%d fast %d nvec[0..4]", i, s.fuse_consumer,
-              o.fuse_role, nbits, f.fast);
-      for (int p = 0; p < std::min(5, ln); ++p) fprintf(stderr, " %d", nvec[p]);
-      fprintf(stderr, " mvec[0..4]");
-      for (int p = 0; p < std::min<int>(5, (int)mvec.size()); ++p) fprintf(stderr, " %d", mvec[p]);
-      fprintf(stderr, " lane_w");
-      for (int b = 0; b < 5; ++b) fprintf(stderr, " %d", f.fast ? ilog2(f.lane_w[b]) : -1);
-      fprintf(stderr, " exchanges %d", (f.xlane[0] != 0) + (f.xlane[1] != 0) + (f.xlane[2] != 0));
-      fprintf(stderr, "\n");
-    }
-    f.hi = (__half2*)P->tensor_ptr(s.out);
-    f.lo = f.hi + (as_rows ? c.M * c.K : 2 * c.N * c.K);
-    f.scale = operand_scale(s.out);
-    fuse_luts.emplace_back();
-    build_lut(mvec, &fuse_luts.back());
-    fuse_luts.emplace_back();
-    build_lut(nvec, &fuse_luts.back());
-    fuse_lut_step.push_back(i);
+    debug_fuse(i, s, f, nvec, mvec);
   }
   P->n_fused = (int)fuse_lut_step.size();
   if (!fuse_luts.empty()) {
@@ -822,7 +913,8 @@ Program* program_create(const tnb_program_desc* d) {
     TNB_CUDA(cudaMemcpy(P->d_fuse_luts, fuse_luts.data(), fuse_luts.size() * sizeof(ByteLut),
                         cudaMemcpyHostToDevice));
     for (size_t e = 0; e < fuse_lut_step.size(); ++e) {
-      FuseOut& f = P->steps[fuse_lut_step[e]].tc.fuse;
+      StepRec& st = P->steps[fuse_lut_step[e]];
+      FuseOut& f = st.kind == KIND_TC ? st.tc.fuse : st.simt_fuse;
       f.lut_m = P->d_fuse_luts + 2 * e;
       f.lut_n = P->d_fuse_luts + 2 * e + 1;
     }
@@ -875,11 +967,12 @@ void program_info(const Program* P, tnb_program_info* info) {
   info->reuse_bytes = P->reuse_bytes;
   info->n_steps_fused = 0;
   info->n_steps_fused_fast = 0;
-  for (auto& s : P->steps)
-    if (s.kind == KIND_TC && s.tc.fuse.mode != 0) {
-      info->n_steps_fused++;
-      info->n_steps_fused_fast += s.tc.fuse.fast ? 1 : 0;
-    }
+  for (auto& s : P->steps) {
+    const FuseOut& f = s.kind == KIND_TC ? s.tc.fuse : s.simt_fuse;
+    if (f.mode == 0) continue;
+    info->n_steps_fused++;
+    info->n_steps_fused_fast += (f.fast || f.vec) ? 1 : 0;
+  }
 }
 
 void program_set_leaf(Program* P, int leaf_pos, const double* data) {
@@ -1031,7 +1124,7 @@ void exec_step(Program* P, StepRec& s) {
                             (T*)P->tensor_ptr(s.out), s.M, s.N, s.K, P->d_luts + s.lut_a,
                             P->d_luts + s.lut_b,
                             P->precision == TNB_SINGLE ? P->d_tmax + P->slot[s.out] : nullptr,
-                            P->stream);
+                            s.simt_fuse.mode ? &s.simt_fuse : nullptr, P->stream);
     C.close(2, e);
     C.launches++;
     return;

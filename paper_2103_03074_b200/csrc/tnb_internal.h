@@ -106,10 +106,17 @@ void launch_prepare_leaves(const T* leaf_pool, T* slice_pool, const SlicedLeafDe
                            int n_descs, const uint32_t* keep_tables, uint64_t mask,
                            cudaStream_t s);
 
+struct FuseOut;
+// C = A B over the gathered layouts; `fuse` (single precision, small-K kernel
+// only, may be null): write C as a tensor-core consumer's staged operand
 template <typename T>
 void launch_contract_simt(const T* A, const T* B, T* C, int64_t M, int64_t N, int64_t K,
                           const ByteLut* lutA, const ByteLut* lutB, unsigned int* max_out,
-                          cudaStream_t s);
+                          const FuseOut* fuse, cudaStream_t s);
+// whether launch_contract_simt takes the streaming small-K kernel
+inline bool simt_uses_smallk(int64_t M, int64_t N, int64_t K) {
+  return K <= 8 && N >= 4 && M * N >= (1 << 16);
+}
 
 template <typename T>
 void launch_permute(const T* in, T* out, int64_t elems, const ByteLut* lut, cudaStream_t s);
@@ -173,7 +180,8 @@ void launch_splitk_reduce(const float* ws, int splits, int64_t elems, float* C,
 struct FuseOut {
   int mode = 0;                  // 0: plain fp32 C; 1: rows operand; 2: cols operand
   int L = 0;                     // cols: rows 2n / 2n+1 are 2^L half2 apart
-  int fast = 0;                  // exchange + 16-B store path usable
+  int fast = 0;                  // GEMM epilogue: exchange + 16-B store path usable
+  int vec = 0;                   // small-K SIMT producer: n bits 0,1 -> destination bits 0,1
   int xlane[3] = {0, 0, 0};      // lane xor mask exchanged with slot bit j (0: none)
   uint32_t lane_w[5] = {};       // destination weight of lane bit b (after exchanges)
   uint32_t slot_w[8] = {};       // destination offset of slot q (after exchanges)
