@@ -225,11 +225,16 @@ contract_smallk_kernel(const T* __restrict__ A, const T* __restrict__ B, T* __re
        idx += (int64_t)gridDim.x * 256) {
     const int64_t m = idx / nq, n0 = (idx - m * nq) << 2;
     S re[4] = {0, 0, 0, 0}, im[4] = {0, 0, 0, 0};
+    // K is a power of two <= 8 and n0 a multiple of 4, so the canonical
+    // indices m*K + k and (n0 + j)*K + k split into disjoint bit fields: one
+    // full LUT lookup per row / column, then a byte-table OR per (j, k)
+    const uint32_t abase = lut_map(la, (uint32_t)(m * K));
+    const uint32_t bbase = lut_map(lb, (uint32_t)(n0 * K));
     for (int k = 0; k < K; ++k) {
-      const T a = A[lut_map(la, (uint32_t)(m * K + k))];
+      const T a = A[abase | la[0][k]];
 #pragma unroll
       for (int j = 0; j < 4; ++j) {
-        const T b = B[lut_map(lb, (uint32_t)((n0 + j) * K + k))];
+        const T b = B[bbase | lb[0][j * K + k]];
         re[j] += a.x * b.x - a.y * b.y;
         im[j] += a.x * b.y + a.y * b.x;
       }
