@@ -74,11 +74,13 @@ __global__ void prepare_leaves_kernel(const T* __restrict__ pool, T* __restrict_
 // ---------------------------------------------------------------------------
 // Gathered SIMT contraction: C[m*N+n] = sum_k A[lutA(m*K+k)] * B[lutB(n*K+k)].
 // 32x32 output tile per 256-thread block, 2x2 per thread, K chunks of 16.
+// `tile` = this block's tile index within the step.
 template <typename T>
-__global__ void __launch_bounds__(256)
-contract_simt_kernel(const T* __restrict__ A, const T* __restrict__ B, T* __restrict__ C,
-                     int64_t M, int64_t N, int64_t K, const ByteLut* __restrict__ gla,
-                     const ByteLut* __restrict__ glb, unsigned int* __restrict__ max_out) {
+__device__ __forceinline__ void simt_tile(const T* __restrict__ A, const T* __restrict__ B,
+                                          T* __restrict__ C, int64_t M, int64_t N, int64_t K,
+                                          const ByteLut* __restrict__ gla,
+                                          const ByteLut* __restrict__ glb,
+                                          unsigned int* __restrict__ max_out, int64_t tile) {
   using S = typename Scalar<T>::type;
   constexpr int BM = 32, BN = 32, BK = 16;
   __shared__ uint32_t la[4][256];
@@ -91,7 +93,7 @@ contract_simt_kernel(const T* __restrict__ A, const T* __restrict__ B, T* __rest
     lb[i >> 8][i & 255] = glb->t[i >> 8][i & 255];
   }
   const int64_t nbn = (N + BN - 1) / BN;
-  const int64_t m0 = ((int64_t)blockIdx.x / nbn) * BM, n0 = ((int64_t)blockIdx.x % nbn) * BN;
+  const int64_t m0 = (tile / nbn) * BM, n0 = (tile % nbn) * BN;
   const int tx = tid & 15, ty = tid >> 4;
   S acc_re[2][2] = {{0, 0}, {0, 0}}, acc_im[2][2] = {{0, 0}, {0, 0}};
   __syncthreads();
@@ -140,6 +142,30 @@ contract_simt_kernel(const T* __restrict__ A, const T* __restrict__ B, T* __rest
       }
     }
   if (max_out) block_max_atomic(vmax, max_out);
+}
+
+template <typename T>
+__global__ void __launch_bounds__(256)
+contract_simt_kernel(const T* __restrict__ A, const T* __restrict__ B, T* __restrict__ C,
+                     int64_t M, int64_t N, int64_t K, const ByteLut* __restrict__ gla,
+                     const ByteLut* __restrict__ glb, unsigned int* __restrict__ max_out) {
+  simt_tile<T>(A, B, C, M, N, K, gla, glb, max_out, blockIdx.x);
+}
+
+// Several independent small SIMT steps in one launch (one block per 32x32
+// tile of any of them): removes the per-step launch latency that dominates
+// the ~160 tiny contraction steps of a slice.
+template <typename T>
+__global__ void __launch_bounds__(256)
+contract_simt_batch_kernel(const SimtStepDesc* __restrict__ d, int n) {
+  int lo = 0, hi = n;  // last descriptor with block0 <= blockIdx.x
+  while (hi - lo > 1) {
+    const int mid = (lo + hi) >> 1;
+    if (d[mid].block0 <= (int64_t)blockIdx.x) lo = mid; else hi = mid;
+  }
+  const SimtStepDesc& s = d[lo];
+  simt_tile<T>((const T*)s.A, (const T*)s.B, (T*)s.C, s.M, s.N, s.K, s.lut_a, s.lut_b, s.max_out,
+               (int64_t)blockIdx.x - s.block0);
 }
 
 // ---------------------------------------------------------------------------
@@ -564,6 +590,15 @@ void launch_contract_simt(const T* A, const T* B, T* C, int64_t M, int64_t N, in
   check_launch("contract_simt");
 }
 
+int64_t simt_tiles(int64_t M, int64_t N) { return ((M + 31) / 32) * ((N + 31) / 32); }
+
+template <typename T>
+void launch_contract_simt_batch(const SimtStepDesc* descs, int n, int64_t blocks, cudaStream_t s) {
+  if (blocks > 0x7fffffffll) throw Error(TNB_ERR_SHAPE, "SIMT batch too large");
+  contract_simt_batch_kernel<T><<<(unsigned)blocks, 256, 0, s>>>(descs, n);
+  check_launch("contract_simt_batch");
+}
+
 template <typename T>
 void launch_permute(const T* in, T* out, int64_t elems, const ByteLut* lut, cudaStream_t s) {
   permute_kernel<T><<<grid_for(elems, 256), 256, 0, s>>>(in, out, elems, lut);
@@ -724,6 +759,7 @@ void launch_splitk_reduce(const float* ws, int splits, int64_t elems, float* C,
   template void launch_contract_simt<T>(const T*, const T*, T*, int64_t, int64_t, int64_t, \
                                         const ByteLut*, const ByteLut*, unsigned int*,     \
                                         const FuseOut*, cudaStream_t);                     \
+  template void launch_contract_simt_batch<T>(const SimtStepDesc*, int, int64_t, cudaStream_t); \
   template void launch_permute<T>(const T*, T*, int64_t, const ByteLut*, cudaStream_t);    \
   template void launch_counter_merge<T>(const T*, const T*, int64_t, int, T*, int64_t, cudaStream_t); \
   template void launch_add<T>(const T*, const T*, T*, int64_t, cudaStream_t);              \

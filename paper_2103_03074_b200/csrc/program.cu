@@ -128,6 +128,7 @@ struct StepRec {
   bool fuse_rows = false, fuse_cols = false;   // TC: operand written by its producer's epilogue
   int fuse_consumer = -1;                      // step whose operand this step's output is written as
   FuseOut simt_fuse;                           // SIMT (small-K) producer: fused output map
+  int batch = -1;                              // tiled SIMT step launched in Program::batches[batch]
   TcGemmPlan tc;
 };
 
@@ -178,6 +179,9 @@ struct Program {
   uint32_t* d_stage_u32 = nullptr;
   ByteLut* d_stage_luts = nullptr;
   ByteLut* d_fuse_luts = nullptr;   // fused-staging destination maps (2 per fused edge)
+  struct SimtBatch { int first_step, last_step, n; int64_t blocks; SimtStepDesc* d_descs; };
+  std::vector<SimtBatch> batches;   // independent consecutive tiled-SIMT steps, one launch each
+  SimtStepDesc* d_simt_descs = nullptr;
   int n_fused = 0;
   void* d_acc = nullptr;          // (n_sliced + 2) accumulator slots of out_elems
   int n_acc_slots = 0;
@@ -197,7 +201,7 @@ struct Program {
   ~Program() {
     if (device >= 0) cudaSetDevice(device);
     void* ptrs[] = {d_leaf_pool, d_slice_pool, d_persist, d_arena, d_luts,
-                    d_sl_descs, d_keep, d_tmax, d_acc, d_stage_u32, d_stage_luts, d_progress, d_fuse_luts};
+                    d_sl_descs, d_keep, d_tmax, d_acc, d_stage_u32, d_stage_luts, d_progress, d_fuse_luts, d_simt_descs};
     for (void* p : ptrs)
       if (p) cudaFree(p);
     for (auto e : ev_pool) cudaEventDestroy(e);
@@ -639,6 +643,44 @@ Program* program_create(const tnb_program_desc* d) {
     P->root_lut = add_lut(P.get(), canon_bits(R.axes, want, {}));
   }
 
+  // ---- SIMT batching: consecutive tiled-SIMT steps of one execution
+  // sequence (the hoisted pass, or the per-slice pass) that do not consume
+  // each other's results run as one launch.  Memory planning below keeps
+  // every operand of a batch live until its last member, so members never
+  // alias each other's inputs or outputs.
+  {
+    static const int batch_env = env_int("TNB_SIMT_BATCH", 1);
+    const bool batching = batch_env && !P->reuse;
+    for (int seq = 0; batching && seq < 2; ++seq) {
+      std::vector<int> cur;
+      auto close = [&] {
+        if (cur.size() >= 2) {
+          Program::SimtBatch b{cur.front(), cur.back(), (int)cur.size(), 0, nullptr};
+          for (int i : cur) P->steps[i].batch = (int)P->batches.size();
+          P->batches.push_back(b);
+        }
+        cur.clear();
+      };
+      for (int i = 0; i < n_steps; ++i) {
+        StepRec& s = P->steps[i];
+        if ((int)s.hoisted != seq) continue;  // seq 1: hoisted pass, seq 0: per slice
+        const bool cand = s.kind == KIND_SIMT && !simt_uses_smallk(s.M, s.N, s.K) &&
+                          P->tensors[s.out].fuse_role == 0;
+        if (!cand) { close(); continue; }
+        bool dep = false;
+        for (int m : cur)
+          if (P->steps[m].out == s.a || P->steps[m].out == s.b) dep = true;
+        if (dep || cur.size() >= 128) close();
+        cur.push_back(i);
+      }
+      close();
+    }
+  }
+  std::vector<int> batch_last(n_steps, -1);  // step -> global index of its batch's last member
+  for (auto& b : P->batches)
+    for (int i = b.first_step; i <= b.last_step; ++i)
+      if (P->steps[i].batch >= 0 && &P->batches[P->steps[i].batch] == &b) batch_last[i] = b.last_step;
+
   // ---- memory planning: persistent (hoisted) and arena (variant) tensors
   int64_t persist_off = 0;
   Arena arena;
@@ -648,6 +690,7 @@ Program* program_create(const tnb_program_desc* d) {
     if (r.def_step >= 0 && r.last_use >= 0 && r.last_use < n_steps) free_after[r.last_use].push_back(t);
   }
   int64_t scratch_bytes = 0;
+  std::vector<std::vector<int>> deferred(n_steps + 1);
   for (int i = 0; i < n_steps; ++i) {
     StepRec& s = P->steps[i];
     TensorRec& o = P->tensors[s.out];
@@ -673,7 +716,17 @@ Program* program_create(const tnb_program_desc* d) {
       scratch_bytes = std::max(scratch_bytes, need);
     }
     // variant operands whose last use is this step are released after it
-    for (int t : free_after[i]) {
+    // (after the batch's last member when the step runs in a SIMT batch)
+    const int rel_at = batch_last[i] >= 0 ? batch_last[i] : i;
+    if (rel_at != i) {
+      deferred[rel_at].insert(deferred[rel_at].end(), free_after[i].begin(), free_after[i].end());
+    } else {
+      for (int t : free_after[i]) {
+        TensorRec& r = P->tensors[t];
+        if (r.pool == POOL_ARENA) arena.release(r.off * (int64_t)P->esize, tensor_bytes(r, (int64_t)P->esize));
+      }
+    }
+    for (int t : deferred[i]) {
       TensorRec& r = P->tensors[t];
       if (r.pool == POOL_ARENA) arena.release(r.off * (int64_t)P->esize, tensor_bytes(r, (int64_t)P->esize));
     }
@@ -765,6 +818,36 @@ Program* program_create(const tnb_program_desc* d) {
   }
   P->n_acc_slots = P->n_sliced + 3;  // counter levels + total + permuted output
   dmalloc(&P->d_acc, (int64_t)P->n_acc_slots * align_up(P->out_elems, 128) * (int64_t)P->esize);
+
+  // ---- SIMT batch descriptors (fixed addresses)
+  if (!P->batches.empty()) {
+    std::vector<SimtStepDesc> descs;
+    for (auto& b : P->batches) {
+      int64_t blocks = 0;
+      const size_t first = descs.size();
+      for (int i = b.first_step; i <= b.last_step; ++i) {
+        const StepRec& s = P->steps[i];
+        if (s.batch != (int)(&b - P->batches.data())) continue;
+        SimtStepDesc d{};
+        d.A = P->tensor_ptr(s.a);
+        d.B = P->tensor_ptr(s.b);
+        d.C = P->tensor_ptr(s.out);
+        d.M = s.M; d.N = s.N; d.K = s.K;
+        d.lut_a = P->d_luts + s.lut_a;
+        d.lut_b = P->d_luts + s.lut_b;
+        d.max_out = P->precision == TNB_SINGLE ? P->d_tmax + P->slot[s.out] : nullptr;
+        d.block0 = blocks;
+        blocks += simt_tiles(s.M, s.N);
+        descs.push_back(d);
+      }
+      b.blocks = blocks;
+      b.d_descs = reinterpret_cast<SimtStepDesc*>(first);  // offset, rebased below
+    }
+    dmalloc((void**)&P->d_simt_descs, (int64_t)descs.size() * sizeof(SimtStepDesc));
+    TNB_CUDA(cudaMemcpy(P->d_simt_descs, descs.data(), descs.size() * sizeof(SimtStepDesc),
+                        cudaMemcpyHostToDevice));
+    for (auto& b : P->batches) b.d_descs = P->d_simt_descs + reinterpret_cast<size_t>(b.d_descs);
+  }
 
   // ---- tensor-core plans (fixed addresses -> TMA descriptors built once)
   dmalloc((void**)&P->d_progress, (int64_t)P->num_sms * 4);
@@ -959,8 +1042,10 @@ void program_info(const Program* P, tnb_program_info* info) {
   info->n_steps_simt = P->n_simt;
   info->n_steps_hoisted = P->n_hoisted;
   int k = P->n_sl_descs ? 1 : 0;
-  for (auto& s : P->steps) {
+  for (size_t i = 0; i < P->steps.size(); ++i) {
+    const StepRec& s = P->steps[i];
     if (s.hoisted) continue;
+    if (s.kind != KIND_TC && s.batch >= 0 && (int)i != P->batches[s.batch].first_step) continue;
     k += s.kind == KIND_TC ? (1 + !s.fuse_rows + !s.fuse_cols + (s.tc.splits > 1 ? 1 : 0)) : 1;
   }
   info->kernels_per_slice = k + 1;
@@ -1118,6 +1203,15 @@ thread_local RunCtx* g_ctx = nullptr;
 template <typename T>
 void exec_step(Program* P, StepRec& s) {
   RunCtx& C = *g_ctx;
+  if (s.kind == KIND_SIMT && s.batch >= 0) {
+    const Program::SimtBatch& b = P->batches[s.batch];
+    if (&s - P->steps.data() != b.first_step) return;  // launched with its batch
+    cudaEvent_t e = C.mark(2);
+    launch_contract_simt_batch<T>(b.d_descs, b.n, b.blocks, P->stream);
+    C.close(2, e);
+    C.launches++;
+    return;
+  }
   if (s.kind == KIND_SIMT) {
     cudaEvent_t e = C.mark(2);
     launch_contract_simt<T>((const T*)P->tensor_ptr(s.a), (const T*)P->tensor_ptr(s.b),

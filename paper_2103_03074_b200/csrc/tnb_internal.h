@@ -113,6 +113,20 @@ template <typename T>
 void launch_contract_simt(const T* A, const T* B, T* C, int64_t M, int64_t N, int64_t K,
                           const ByteLut* lutA, const ByteLut* lutB, unsigned int* max_out,
                           const FuseOut* fuse, cudaStream_t s);
+// one step of a batched SIMT launch (contract_simt_batch_kernel)
+struct SimtStepDesc {
+  const void* A;
+  const void* B;
+  void* C;
+  int64_t M, N, K;
+  const ByteLut* lut_a;
+  const ByteLut* lut_b;
+  unsigned int* max_out;
+  int64_t block0;             // first block of this step in the batch grid
+};
+int64_t simt_tiles(int64_t M, int64_t N);
+template <typename T>
+void launch_contract_simt_batch(const SimtStepDesc* descs, int n, int64_t blocks, cudaStream_t s);
 // whether launch_contract_simt takes the streaming small-K kernel
 inline bool simt_uses_smallk(int64_t M, int64_t N, int64_t K) {
   return K <= 8 && N >= 4 && M * N >= (1 << 16);

@@ -1,7 +1,10 @@
 """Summarise an ncu --metrics gpu__time_duration.sum launch list (CSV)."""
 import collections
 import csv
+import signal
 import sys
+
+signal.signal(signal.SIGPIPE, signal.SIG_DFL)  # quiet under `| head`
 
 rows = list(csv.reader(open(sys.argv[1])))
 hi = [i for i, r in enumerate(rows) if "Kernel Name" in r][0]
