@@ -16,6 +16,7 @@ S = 2
 
 
 def step(a):
+    # as bench.py's e2e leg: every call's leaves arrive from the host
     prog = E.head_program(w.tn, w.tree, w.sliced, "single")
     prog._leaf_data = [None] * prog.n_leaves
     hv = tnb.compute_head_vector(w.tn, w.tree, w.sliced, None, slice_range=(a, a + S),
@@ -33,4 +34,4 @@ for a in range(10 * S, 13 * S, S):
     step(a)
 pr.disable()
 print(f"3 steps: {(time.perf_counter() - t0) * 1e3:.1f} ms")
-pstats.Stats(pr).sort_stats("cumulative").print_stats(25)
+pstats.Stats(pr).sort_stats("tottime").print_stats(20)
