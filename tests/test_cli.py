@@ -1,0 +1,96 @@
+"""The reference CLI (tncut) driven through paper_2103_03074_b200.cli: the
+engine and analytics names inside tncut.cli / tncut.pipeline are rebound to
+this executor (CPU: binding only; GPU: a full `tncut run` + `reduce`
+round trip against the reference's own output)."""
+
+from __future__ import annotations
+
+import os
+import sys
+
+import numpy as np
+import pytest
+
+from conftest import GOLDEN, ROOT
+
+REF_INSTALL = os.path.join(ROOT, "baseline", "_ref")  # pip --target install of the reference
+
+
+def _tncut():
+    """tncut from /root/reference (build container) or baseline/_ref (GPU box)."""
+    for path in ("/root/reference/pkg/src", REF_INSTALL):
+        if os.path.isdir(os.path.join(path, "tncut")) and path not in sys.path:
+            sys.path.insert(0, path)
+    os.environ.setdefault("NUMBA_CACHE_DIR", "/tmp/numba_cache")
+    try:
+        import tncut  # noqa: F401
+    except Exception:
+        pytest.skip("reference package not importable")
+
+
+def test_bind_rebinds_engine_and_analytics_names():
+    _tncut()
+    import tncut.cli as cli
+    import tncut.pipeline as pipeline
+
+    from paper_2103_03074_b200 import analytics, cli as ours, engine
+
+    prev = ours.bind()
+    try:
+        assert cli.compute_head_vector is engine.compute_head_vector
+        assert cli.compute_tail_amplitudes is engine.compute_tail_amplitudes
+        assert cli.reduce_partials is engine.reduce_partials
+        assert pipeline.compute_head_vector is engine.compute_head_vector
+        assert cli.xeb is analytics.xeb
+    finally:
+        ours.unbind(prev)
+    assert cli.compute_head_vector is not engine.compute_head_vector
+
+
+@pytest.mark.gpu
+def test_tncut_run_and_reduce_on_the_executor(gpu, tmp_path):
+    """`tncut run` (full range and two partials + `tncut reduce`) on the C1
+    plan through the executor; amplitudes match the reference's own run."""
+    _tncut()
+    import tncut.cli as cli
+
+    from paper_2103_03074_b200 import cli as ours
+
+    circ = os.path.join(GOLDEN, "c1", "circuit.qsim")
+    order = os.path.join(GOLDEN, "c1", "order.json")
+
+    def table(path):
+        rows = [l.split("\t") for l in open(path)
+                if l.strip() and not l.startswith("#") and not l.startswith("bitstring")]
+        return {r[0]: complex(float(r[1]), float(r[2])) for r in rows if len(r) >= 3}
+
+    # the reference itself (unbound)
+    ref_out = tmp_path / "ref.tsv"
+    with pytest.raises(SystemExit) as e:
+        cli.main(args=["run", circ, order, "--precision", "double", "-o", str(ref_out)])
+    assert e.value.code in (0, None)
+    ref = table(ref_out)
+
+    for precision, tol in (("double", 1e-10), ("single", 1e-4)):
+        out = tmp_path / f"ours_{precision}.tsv"
+        assert ours.main(["run", circ, order, "--precision", precision, "-o", str(out)]) == 0
+        got = table(out)
+        assert got.keys() == ref.keys()
+        a = np.array([got[k] for k in ref]); b = np.array([ref[k] for k in ref])
+        assert np.linalg.norm(a - b) / np.linalg.norm(b) < tol, precision
+
+    # partial ranges written by the executor, reduced by the reference's `reduce`
+    import json
+    n_e = len(json.load(open(order)).get("slices", []))
+    if n_e >= 1:
+        half = 1 << (n_e - 1)
+        parts = []
+        for a, b in ((0, half), (half, 2 * half)):
+            p = tmp_path / f"part_{a}.hv"
+            assert ours.main(["run", circ, order, "--slices", f"{a}..{b}", "-o", str(p)]) == 0
+            parts.append(str(p))
+        red = tmp_path / "reduced.tsv"
+        assert ours.main(["reduce", *parts, "--circuit", circ, "--order", order, "-o", str(red)]) == 0
+        got = table(red)
+        a = np.array([got[k] for k in ref]); b = np.array([ref[k] for k in ref])
+        assert np.linalg.norm(a - b) / np.linalg.norm(b) < 1e-10
