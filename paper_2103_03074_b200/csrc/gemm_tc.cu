@@ -427,14 +427,15 @@ gemm_f16x3_kernel(const __grid_constant__ CUtensorMap tm_ahi, const __grid_const
           const int kbk = k / BK;
           // 3 = skip A on odd K blocks (half the A traffic: the bound of sharing A)
           const bool skip_a = exp_skip == 2 || (exp_skip == 3 && (kbk & 1));
-          const uint32_t bytes = exp_skip == 1 ? 2 * A_TILE : skip_a ? 2 * CF::B_TILE : CF::STAGE_BYTES;
+          const bool skip_b = exp_skip == 1 || (exp_skip == 4 && (kbk & 1));  // 4: half the B traffic
+          const uint32_t bytes = (skip_a ? 0 : 2 * A_TILE) + (skip_b ? 0 : 2 * CF::B_TILE);
           if (leader) mbar_arrive_expect_tx(&full_bar[stage], CG * bytes);
           else mbar_arrive_remote(&full_bar[stage], 0);
           if (!skip_a) {
             tma_load_tile<CG>(st, &tm_ahi, &full_bar[stage], m0, kbk);
             tma_load_tile<CG>(st + A_TILE, &tm_alo, &full_bar[stage], m0, kbk);
           }
-          if (exp_skip != 1) {
+          if (!skip_b) {
             tma_load_tile<CG>(st + 2 * A_TILE, &tm_bhi, &full_bar[stage], n0, kbk);
             tma_load_tile<CG>(st + 2 * A_TILE + CF::B_TILE, &tm_blo, &full_bar[stage], n0, kbk);
           }
@@ -705,7 +706,8 @@ void tc_plan_gemm(TcGemmPlan* p, const __half* Ahi, const __half* Alo, const __h
   p->splits = choose_splits(M, Np, Kp, num_sms);
   const int64_t kblocks = (Kp + BK - 1) / BK;
   p->k_per_split = ((kblocks + p->splits - 1) / p->splits) * BK;
-  const int64_t units = num_sms / p->cta_group;
+  static const int max_sms = env_int("TNB_GEMM_MAX_SMS", 0);  // diagnostic: cap the persistent grid
+  const int64_t units = (max_sms > 0 && max_sms < num_sms ? max_sms : num_sms) / p->cta_group;
   const int64_t work = ((M + BM * p->cta_group - 1) / (BM * p->cta_group)) * ((Np + BN - 1) / BN) * p->splits;
   p->grid = (int)((work < units ? work : units) * p->cta_group);
   if (p->splits > 1) {
