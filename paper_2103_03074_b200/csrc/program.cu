@@ -481,12 +481,30 @@ Program* program_create(const tnb_program_desc* d) {
       // 4 per thread, 128 per warp, so every low K bit goes there first)
       const Pre& pp = pre[def[primary]];
       std::vector<int64_t> kc, kr, kpri;
-      for (int64_t x : ord_k[c]) (has(pp.cols, x) ? kc : kr).push_back(x);
-      size_t ic = 0, ir = 0;
-      for (int slot = 0; slot < 4 && (ic < kc.size() || ir < kr.size()); ++slot) {
-        const bool want_col = slot < 2 || pp.smallk;
-        if ((want_col && ic < kc.size()) || ir >= kr.size()) kpri.push_back(kc[ic++]);
-        else kpri.push_back(kr[ir++]);
+      // joint choice when the other operand comes from a large small-K
+      // producer: k0,k1 on both producers' columns, k2,k3 on the small-K
+      // producer's columns (its fused stores need all four there)
+      const int sec = (primary == rows_t && fuse_role_pre[cols_t]) ? cols_t : -1;
+      if (sec >= 0 && pre[def[sec]].smallk && !pre[def[sec]].tc &&
+          pre[def[sec]].rows.size() + pre[def[sec]].cols.size() > 20) {
+        const Pre& ps = pre[def[sec]];
+        std::vector<int64_t> both, sonly;
+        for (int64_t x : ord_k[c])
+          if (has(ps.cols, x)) (has(pp.cols, x) ? both : sonly).push_back(x);
+        if (both.size() >= 2 && both.size() + sonly.size() >= (size_t)kKBlockLog) {
+          kpri = {both[0], both[1]};
+          for (int64_t x : sonly) if (kpri.size() < (size_t)kKBlockLog) kpri.push_back(x);
+          for (size_t x = 2; x < both.size() && kpri.size() < (size_t)kKBlockLog; ++x) kpri.push_back(both[x]);
+        }
+      }
+      if (kpri.empty()) {
+        for (int64_t x : ord_k[c]) (has(pp.cols, x) ? kc : kr).push_back(x);
+        size_t ic = 0, ir = 0;
+        for (int slot = 0; slot < 4 && (ic < kc.size() || ir < kr.size()); ++slot) {
+          const bool want_col = slot < 2 || pp.smallk;
+          if ((want_col && ic < kc.size()) || ir >= kr.size()) kpri.push_back(kc[ic++]);
+          else kpri.push_back(kr[ir++]);
+        }
       }
       reorder(ord_k[c], kpri);
       const size_t L = std::min<size_t>(ord_k[c].size(), (size_t)kKBlockLog);
