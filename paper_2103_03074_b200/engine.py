@@ -103,6 +103,7 @@ class Program:
         info = _lib.ProgramInfo()
         _lib.check(lib.tnb_program_get_info(self.handle, C.byref(info)))
         self.info = info
+        _warm_pinned(info.out_elems, self.dtype)
 
     def __del__(self):
         h = getattr(self, "handle", None)
@@ -189,6 +190,17 @@ def _host_array(n: int, dtype) -> np.ndarray:
         except Exception:  # pinning is an optimisation only
             pass
     return np.empty(int(n), dtype=dtype)
+
+
+def _warm_pinned(n: int, dtype, blocks: int = 3) -> None:
+    """Page-lock a few result-sized blocks once (program creation) and hand
+    them to torch's pinned-memory cache, so the per-call result buffers of
+    ``_host_array`` are cache hits instead of ~10 ms cudaHostAlloc calls (a
+    new result is requested while the caller still holds the previous one)."""
+    if int(n) * np.dtype(dtype).itemsize < _PIN_MIN_BYTES:
+        return
+    held = [_host_array(n, dtype) for _ in range(blocks)]
+    del held
 
 
 _cache: dict = {}
