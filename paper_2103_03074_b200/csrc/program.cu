@@ -182,6 +182,14 @@ struct Program {
   struct SimtBatch { int first_step, last_step, n; int64_t blocks; SimtStepDesc* d_descs; };
   std::vector<SimtBatch> batches;   // independent consecutive tiled-SIMT steps, one launch each
   SimtStepDesc* d_simt_descs = nullptr;
+  // per-slice launch plan as CUDA-graph segments: the runs of small kernels
+  // between GEMMs are captured once and replayed per mask; GEMMs stay direct
+  // launches (their CUDA-event timing feeds the roofline figures)
+  struct Segment { cudaGraphExec_t exec = nullptr; int kernels = 0; };
+  struct PlanItem { int seg = -1, step = -1; };
+  std::vector<Segment> segs;
+  std::vector<PlanItem> items;
+  bool segs_built = false;
   int n_fused = 0;
   void* d_acc = nullptr;          // (n_sliced + 2) accumulator slots of out_elems
   int n_acc_slots = 0;
@@ -205,6 +213,7 @@ struct Program {
     for (void* p : ptrs)
       if (p) cudaFree(p);
     for (auto e : ev_pool) cudaEventDestroy(e);
+    for (auto& g : segs) if (g.exec) cudaGraphExecDestroy(g.exec);
     if (stream) cudaStreamDestroy(stream);
   }
 
@@ -244,8 +253,15 @@ int add_lut(Program* P, const std::vector<int>& src_bit) {
   return (int)P->luts.size() - 1;
 }
 
+// parts of a step's launches: SIMT kernels / operand staging (kPre), the
+// tensor-core GEMM (kGemm), the split-K reduce (kPost)
+enum StepPart { kPre = 1, kGemm = 2, kPost = 4, kAll = 7 };
+
 template <typename T>
-void exec_step(Program* P, StepRec& s);
+void exec_step(Program* P, StepRec& s, int parts = kAll);
+
+template <typename T>
+void build_segments(Program* P);
 
 template <typename T>
 void run_range_t(Program* P, uint64_t a, uint64_t b, int mode, void* out, bool out_dev);
@@ -1219,8 +1235,9 @@ struct RunCtx {
 thread_local RunCtx* g_ctx = nullptr;
 
 template <typename T>
-void exec_step(Program* P, StepRec& s) {
+void exec_step(Program* P, StepRec& s, int parts) {
   RunCtx& C = *g_ctx;
+  if (s.kind == KIND_SIMT && !(parts & kPre)) return;
   if (s.kind == KIND_SIMT && s.batch >= 0) {
     const Program::SimtBatch& b = P->batches[s.batch];
     if (&s - P->steps.data() != b.first_step) return;  // launched with its batch
@@ -1253,23 +1270,27 @@ void exec_step(Program* P, StepRec& s) {
     __half* bhi = (__half*)(base + (s.fuse_rows ? 0 : 2 * s.M * Kp * 2));
     __half* blo = bhi + Np * Kp;
     cudaEvent_t e = nullptr;
-    if (!s.fuse_rows || !s.fuse_cols) e = C.mark(1);
-    if (!s.fuse_rows) {
-      launch_stage(rows, P->stages[s.st_rows], s.K, false, P->d_tmax + P->slot[s.rows_t], ahi, alo, P->stream);
-      C.launches++;
+    if ((parts & kPre) && (!s.fuse_rows || !s.fuse_cols)) {
+      e = C.mark(1);
+      if (!s.fuse_rows) {
+        launch_stage(rows, P->stages[s.st_rows], s.K, false, P->d_tmax + P->slot[s.rows_t], ahi, alo, P->stream);
+        C.launches++;
+      }
+      if (!s.fuse_cols) {
+        launch_stage(cols, P->stages[s.st_cols], s.K, true, P->d_tmax + P->slot[s.cols_t], bhi, blo, P->stream);
+        C.launches++;
+      }
+      C.close(1, e);
     }
-    if (!s.fuse_cols) {
-      launch_stage(cols, P->stages[s.st_cols], s.K, true, P->d_tmax + P->slot[s.cols_t], bhi, blo, P->stream);
-      C.launches++;
+    if (parts & kGemm) {
+      e = C.mark(0);
+      tc_launch_gemm(&s.tc, P->stream);
+      C.close(0, e);
+      C.launches += 1;
+      C.gemm_launches++;
+      C.gemm_flops += 8.0 * s.mults;
     }
-    if (!s.fuse_rows || !s.fuse_cols) C.close(1, e);
-    e = C.mark(0);
-    tc_launch_gemm(&s.tc, P->stream);
-    C.close(0, e);
-    C.launches += 1;
-    C.gemm_launches++;
-    C.gemm_flops += 8.0 * s.mults;
-    if (s.tc.splits > 1) {
+    if ((parts & kPost) && s.tc.splits > 1) {
       e = C.mark(1);
       launch_splitk_reduce(s.tc.C, s.tc.splits, s.M * Np, (float*)P->tensor_ptr(s.out),
                            s.tc.scale_rows, s.tc.scale_cols, s.tc.max_out, P->stream);
@@ -1279,6 +1300,55 @@ void exec_step(Program* P, StepRec& s) {
   } else {
     throw Error(TNB_ERR_ARG, "tensor-core path requires single precision");
   }
+}
+
+// Capture the per-slice launch sequence (everything but the GEMMs) into
+// graph segments: [max-slot reset, SIMT/staging kernels ...] GEMM [split-K
+// reduce, SIMT/staging ...] GEMM ...  Capturing records without executing.
+template <typename T>
+void build_segments(Program* P) {
+  RunCtx& C = *g_ctx;
+  cudaStream_t st = P->stream;
+  const int64_t launches0 = C.launches;
+  int64_t seg_start = C.launches;
+  auto begin = [&] {
+    TNB_CUDA(cudaStreamBeginCapture(st, cudaStreamCaptureModeRelaxed));
+    seg_start = C.launches;
+  };
+  auto end = [&] {
+    cudaGraph_t g = nullptr;
+    TNB_CUDA(cudaStreamEndCapture(st, &g));
+    size_t nodes = 0;
+    TNB_CUDA(cudaGraphGetNodes(g, nullptr, &nodes));
+    if (nodes > 0) {
+      Program::Segment seg;
+      TNB_CUDA(cudaGraphInstantiate(&seg.exec, g, 0));
+      seg.kernels = (int)(C.launches - seg_start);
+      P->items.push_back({(int)P->segs.size(), -1});
+      P->segs.push_back(seg);
+    }
+    TNB_CUDA(cudaGraphDestroy(g));
+  };
+  P->items.clear();
+  begin();
+  if (P->var_slot_count)
+    TNB_CUDA(cudaMemsetAsync(P->d_tmax + P->var_slot_begin, 0, (size_t)P->var_slot_count * 4, st));
+  for (size_t i = 0; i < P->steps.size(); ++i) {
+    StepRec& s = P->steps[i];
+    if (s.hoisted) continue;
+    if (s.kind != KIND_TC) {
+      exec_step<T>(P, s, kPre);
+      continue;
+    }
+    exec_step<T>(P, s, kPre);
+    end();
+    P->items.push_back({-1, (int)i});
+    begin();
+    exec_step<T>(P, s, kPost);
+  }
+  end();
+  C.launches = launches0;  // nothing ran: the replays count their kernels
+  P->segs_built = true;
 }
 
 template <typename T>
@@ -1294,6 +1364,11 @@ void run_range_t(Program* P, uint64_t a, uint64_t b, int mode, void* out, bool o
   auto slot = [&](int i) { return slots + (size_t)i * slot_stride; };
   T* total_slot = slot(P->n_sliced + 1);
   T* perm_slot = slot(P->n_sliced + 2);
+  // CUDA-graph segments for the per-slice launches (not with per-class
+  // timing, whose events would be baked into the graphs, nor reuse mode,
+  // which skips steps per mask)
+  static const int graphs_env = env_int("TNB_GRAPHS", 1);
+  const bool use_graphs = graphs_env && P->timing != 1 && !P->reuse;
   cudaEvent_t t_start = ctx.mark(-1);
 
   // hoisted slice-invariant steps (once per leaf-data version)
@@ -1317,7 +1392,17 @@ void run_range_t(Program* P, uint64_t a, uint64_t b, int mode, void* out, bool o
                              P->n_sl_descs, P->d_keep, mask, st);
     if (P->n_sl_descs) ctx.launches++;
     ctx.close(3, e);
-    if (!P->reuse) {
+    if (!P->reuse && use_graphs) {
+      if (!P->segs_built) build_segments<T>(P);
+      for (const auto& it : P->items) {
+        if (it.seg >= 0) {
+          TNB_CUDA(cudaGraphLaunch(P->segs[it.seg].exec, st));
+          ctx.launches += P->segs[it.seg].kernels;
+        } else {
+          exec_step<T>(P, P->steps[it.step], kGemm);
+        }
+      }
+    } else if (!P->reuse) {
       if (P->var_slot_count)
         TNB_CUDA(cudaMemsetAsync(P->d_tmax + P->var_slot_begin, 0, (size_t)P->var_slot_count * 4, st));
       for (auto& s : P->steps)
