@@ -271,120 +271,308 @@ void run_range_t(Program* P, uint64_t a, uint64_t b, int mode, void* out, bool o
 void upload_leaf_max(Program* P, int leaf_pos, const double* data);
 
 // ---------------------------------------------------------------------------
-Program* program_create(const tnb_program_desc* d) {
-  if (!d) throw Error(TNB_ERR_ARG, "null descriptor");
-  if (d->precision != TNB_SINGLE && d->precision != TNB_DOUBLE)
-    throw Error(TNB_ERR_ARG, "precision must be TNB_SINGLE or TNB_DOUBLE");
-  if (d->n_leaves <= 0) throw Error(TNB_ERR_SHAPE, "program needs at least one leaf");
-  if (d->n_sliced < 0 || d->n_sliced > 64) throw Error(TNB_ERR_ARG, "n_sliced must be in [0, 64]");
-  int ndev = 0;
-  TNB_CUDA(cudaGetDeviceCount(&ndev));
-  if (d->device < 0 || d->device >= ndev) throw Error(TNB_ERR_NODEV, "device ordinal out of range");
-
-  std::unique_ptr<Program> P(new Program());
-  P->device = d->device;
-  P->precision = d->precision;
-  P->flags = d->flags;
-  P->esize = d->precision == TNB_SINGLE ? 8 : 16;
-  P->n_sliced = d->n_sliced;
-  P->reuse = (d->flags & TNB_FLAG_REUSE_SLICES) != 0;
-  TNB_CUDA(cudaSetDevice(P->device));
-  TNB_CUDA(cudaDeviceGetAttribute(&P->num_sms, cudaDevAttrMultiProcessorCount, P->device));
-  TNB_CUDA(cudaStreamCreateWithFlags(&P->stream, cudaStreamNonBlocking));
-  const bool use_tc = d->precision == TNB_SINGLE && !(d->flags & TNB_FLAG_NO_TENSOR_CORES) &&
-                      tc_available(P->device);
-
-  // sliced index -> mask bit (engine.py:276-279: bit n_e-1-pos pins sliced[pos])
-  std::unordered_map<int64_t, int> slice_bit;
-  for (int i = 0; i < d->n_sliced; ++i) {
-    if (slice_bit.count(d->sliced[i])) throw Error(TNB_ERR_ARG, "duplicate sliced index");
-    slice_bit[d->sliced[i]] = d->n_sliced - 1 - i;
-  }
-
-  // ---- leaves
-  std::unordered_map<int64_t, int> id2t;
-  std::vector<SlicedLeafDesc> sl_descs;
-  std::vector<uint32_t> keep;
-  int64_t leaf_off = 0, slice_off = 0, idx_off = 0;
-  P->leaf_ranks.assign(d->leaf_ranks, d->leaf_ranks + d->n_leaves);
-  for (int i = 0; i < d->n_leaves; ++i) {
-    const int r = d->leaf_ranks[i];
-    if (r < 0 || r > 32) throw Error(TNB_ERR_SHAPE, "leaf rank out of range");
-    TensorRec t;
-    t.leaf_pos = i;
-    std::vector<int64_t> full(d->leaf_indices + idx_off, d->leaf_indices + idx_off + r);
-    idx_off += r;
-    std::vector<std::pair<int, uint32_t>> sl;  // (mask bit, stride)
-    std::vector<int> keep_src;
-    for (int ax = 0; ax < r; ++ax) {
-      auto it = slice_bit.find(full[ax]);
-      if (it != slice_bit.end()) {
-        sl.push_back({it->second, 1u << (r - 1 - ax)});
-        t.dep |= 1ull << it->second;
-      } else {
-        t.axes.push_back(full[ax]);
-        keep_src.push_back(r - 1 - ax);
+// SIMT batching (program_create): fills P->batches and StepRec::batch.
+void plan_simt_batches(Program* P) {
+  const int n_steps = (int)P->steps.size();
+  // SIMT batching: consecutive tiled-SIMT steps of one execution
+  // sequence (the hoisted pass, or the per-slice pass) that do not consume
+  // each other's results run as one launch.  Memory planning below keeps
+  // every operand of a batch live until its last member, so members never
+  // alias each other's inputs or outputs.
+  {
+    static const int batch_env = env_int("TNB_SIMT_BATCH", 1);
+    const bool batching = batch_env && !P->reuse;
+    for (int seq = 0; batching && seq < 2; ++seq) {
+      std::vector<int> cur;
+      auto close = [&] {
+        if (cur.size() >= 2) {
+          Program::SimtBatch b{cur.front(), cur.back(), (int)cur.size(), 0, nullptr};
+          for (int i : cur) P->steps[i].batch = (int)P->batches.size();
+          P->batches.push_back(b);
+        }
+        cur.clear();
+      };
+      for (int i = 0; i < n_steps; ++i) {
+        StepRec& s = P->steps[i];
+        if ((int)s.hoisted != seq) continue;  // seq 1: hoisted pass, seq 0: per slice
+        const bool cand = s.kind == KIND_SIMT && !simt_uses_smallk(s.M, s.N, s.K) &&
+                          P->tensors[s.out].fuse_role == 0;
+        if (!cand) { close(); continue; }
+        bool dep = false;
+        for (int m : cur)
+          if (P->steps[m].out == s.a || P->steps[m].out == s.b) dep = true;
+        if (dep || cur.size() >= 128) close();
+        cur.push_back(i);
       }
+      close();
     }
-    P->leaf_pool_off.push_back(leaf_off);
-    leaf_off += (int64_t)1 << r;
-    t.elems = (int64_t)1 << t.axes.size();
-    if (!sl.empty()) {
-      if (sl.size() > 8) throw Error(TNB_ERR_SHAPE, "more than 8 sliced axes on one leaf");
-      t.variant = true;
-      t.pool = POOL_SLICE;
-      t.off = slice_off;
-      slice_off += align_up(t.elems, 128);
-      SlicedLeafDesc sd{};
-      sd.src_off = P->leaf_pool_off.back();
-      sd.dst_off = t.off;
-      sd.out_elems = (uint32_t)t.elems;
-      sd.n_sl = (uint32_t)sl.size();
-      sd.keep_lut_off = (uint32_t)keep.size();
-      for (size_t j = 0; j < sl.size(); ++j) { sd.sl_bit[j] = sl[j].first; sd.sl_stride[j] = sl[j].second; }
-      // out index bit p (LSB first) <-> kept axis keep_src.size()-1-p
-      const int nk = (int)keep_src.size();
-      for (int64_t jj = 0; jj < t.elems; ++jj) {
-        uint32_t o = 0;
-        for (int p = 0; p < nk; ++p)
-          if ((jj >> p) & 1) o |= 1u << keep_src[nk - 1 - p];
-        keep.push_back(o);
-      }
-      sl_descs.push_back(sd);
+  }
+}
+
+// Memory planning (program_create): pools, arena offsets and per-step
+// staging scratch; releases of a SIMT batch's operands wait for its last member.
+void plan_memory(Program* P) {
+  const int n_steps = (int)P->steps.size();
+  std::vector<int> batch_last(n_steps, -1);  // step -> global index of its batch's last member
+  for (auto& b : P->batches)
+    for (int i = b.first_step; i <= b.last_step; ++i)
+      if (P->steps[i].batch >= 0 && &P->batches[P->steps[i].batch] == &b) batch_last[i] = b.last_step;
+
+  // memory planning: persistent (hoisted) and arena (variant) tensors
+  int64_t persist_off = 0;
+  Arena arena;
+  std::vector<std::vector<int>> free_after(n_steps + 1);
+  for (int t = 0; t < (int)P->tensors.size(); ++t) {
+    const TensorRec& r = P->tensors[t];
+    if (r.def_step >= 0 && r.last_use >= 0 && r.last_use < n_steps) free_after[r.last_use].push_back(t);
+  }
+  int64_t scratch_bytes = 0;
+  std::vector<std::vector<int>> deferred(n_steps + 1);
+  for (int i = 0; i < n_steps; ++i) {
+    StepRec& s = P->steps[i];
+    TensorRec& o = P->tensors[s.out];
+    const int64_t ob = tensor_bytes(o, (int64_t)P->esize);  // fused: the consumer's fp16 planes
+    if (s.hoisted || !o.variant || o.cached) {
+      o.pool = POOL_PERSIST;
+      o.off = persist_off;
+      persist_off += align_up(ob / (int64_t)P->esize, 128);
+      if (o.cached) P->reuse_bytes += ob;
     } else {
-      t.pool = POOL_LEAF;
-      t.off = P->leaf_pool_off.back();
+      o.pool = POOL_ARENA;
+      o.off = arena.alloc(ob) / (int64_t)P->esize;
     }
-    if (id2t.count(d->leaf_ids[i])) throw Error(TNB_ERR_SHAPE, "duplicate leaf id");
-    id2t[d->leaf_ids[i]] = (int)P->tensors.size();
-    P->tensors.push_back(t);
+    if (s.kind == KIND_TC) {
+      // operand staging (+ split-K workspace) lives in the arena for the
+      // duration of this step only: it shares memory with dead tensors.
+      // Fused operands are already staged (their producer wrote them).
+      const int64_t Kp = 2 * s.K, Np = 2 * s.N;
+      int64_t need = (s.fuse_rows ? 0 : 2 * s.M * Kp * 2) + (s.fuse_cols ? 0 : 2 * Np * Kp * 2);
+      need = align_up(need, kAlign) + tc_workspace_elems(s.M, Np, Kp, P->num_sms) * 4;
+      s.scratch_bytes = need;
+      if (need > 0) s.scratch_off = arena.alloc(need);
+      scratch_bytes = std::max(scratch_bytes, need);
+    }
+    // variant operands whose last use is this step are released after it
+    // (after the batch's last member when the step runs in a SIMT batch)
+    const int rel_at = batch_last[i] >= 0 ? batch_last[i] : i;
+    if (rel_at != i) {
+      deferred[rel_at].insert(deferred[rel_at].end(), free_after[i].begin(), free_after[i].end());
+    } else {
+      for (int t : free_after[i]) {
+        TensorRec& r = P->tensors[t];
+        if (r.pool == POOL_ARENA) arena.release(r.off * (int64_t)P->esize, tensor_bytes(r, (int64_t)P->esize));
+      }
+    }
+    for (int t : deferred[i]) {
+      TensorRec& r = P->tensors[t];
+      if (r.pool == POOL_ARENA) arena.release(r.off * (int64_t)P->esize, tensor_bytes(r, (int64_t)P->esize));
+    }
+    if (s.kind == KIND_TC && s.scratch_bytes > 0) arena.release(s.scratch_off, s.scratch_bytes);
   }
-  P->leaf_pool_elems = leaf_off;
-  P->slice_pool_elems = slice_off;
+  P->persist_elems = persist_off;
+  P->arena_bytes = arena.top;
+  P->scratch_bytes = scratch_bytes;
 
-  // ---- pre-pass over index sets: kernel kind and operand roles of every
-  // step, the fused-staging edges (a tensor-core step whose result feeds a
-  // tensor-core step writes it in the consumer's staged fp16 layout from its
-  // epilogue), and the canonical index orders of every tensor-core step.
-  // Orders are planned consumer-first (reverse step order): a consumer puts
-  // contracted indices that sit on its producer's lowest result columns on
-  // its lowest K bits, and the producer then orders its free indices so that
-  // the consumer's lowest destination bits (low K bits, then the consumer's
-  // lowest free bits) are its thread-local columns / lane-local rows -- the
-  // epilogue's scattered stores then form contiguous runs.  Lists below are
-  // lowest-first (canonical bit 0 first).
-  // tensor-core eligibility: big enough to fill 128x256 tiles and amortise
-  // staging.  TNB_TC_MIN_RANK (read per program; tests lower it so small
-  // random networks exercise the tensor-core and fused-staging paths)
-  const int tc_min_rank = env_int("TNB_TC_MIN_RANK", 27);
-  auto tc_eligible = [&](int na, int nb, int nab) {
-    return use_tc && nab >= 3 && na + nb + nab >= tc_min_rank && std::max(na, nb) >= 7 &&
-           std::min(na, nb) >= 3;
+}
+
+// ---------------------------------------------------------------------------
+// Tensor-core plans (program_create): TMA descriptors over the fixed operand
+// addresses, the fp16 scale source of every operand, and the fused-staging
+// destination maps (GEMM epilogues and small-K SIMT producers).
+void plan_tensor_core_steps(Program* P) {
+  const int n_steps = (int)P->steps.size();
+  auto dmalloc = [](void** p, int64_t bytes) {
+    if (bytes <= 0) bytes = 256;
+    TNB_CUDA(cudaMalloc(p, (size_t)bytes));
   };
-  std::vector<std::vector<int64_t>> ord_k(d->n_steps), ord_rows(d->n_steps), ord_cols(d->n_steps);
-  std::vector<char> pre_rows_is_a(d->n_steps, 1);  // SIMT small-K producer: m/n roles swapped if 0
-  std::vector<int> fuse_role_pre;                           // tensor -> 1/2 when fused
-  std::vector<int> fuse_consumer_pre;                       // tensor -> consuming step
+  dmalloc((void**)&P->d_progress, (int64_t)P->num_sms * 4);
+  // fp16 split scale of a tensor-core operand: its own max when staged, the
+  // producer's a-priori bound 2 K max|A| max|B| when the producer's epilogue
+  // wrote it (fused); producer and consumer evaluate the same ScaleSrc
+  auto operand_scale = [&](int t) {
+    ScaleSrc sc;
+    const TensorRec& r = P->tensors[t];
+    if (r.fuse_role != 0) {
+      const StepRec& p = P->steps[r.def_step];
+      sc.a = P->d_tmax + P->slot[p.kind == KIND_TC ? p.rows_t : p.a];
+      sc.b = P->d_tmax + P->slot[p.kind == KIND_TC ? p.cols_t : p.b];
+      sc.f = (float)(2.0 * (double)p.K);
+    } else {
+      sc.a = P->d_tmax + P->slot[t];
+    }
+    return sc;
+  };
+  std::vector<ByteLut> fuse_luts;
+  std::vector<int> fuse_lut_step;
+  // destination map of a fused result in its consumer's operand layout
+  // (stage_kernel's): canonical (row r, k) -> half2 index (k >> L, r,
+  // k & (2^L-1)) in [K/2^L][rows][2^L], a zero bit inserted at L for the
+  // expanded cols operand.  Returns the destination bit of every result
+  // column bit (nvec) and row bit (mvec); fills everything but the kernel-
+  // specific store-path fields.
+  auto build_fuse_map = [&](int i, StepRec& s, FuseOut& f, std::vector<int>& nvec, std::vector<int>& mvec) {
+    const TensorRec& o = P->tensors[s.out];
+    const StepRec& c = P->steps[s.fuse_consumer];
+    const bool as_rows = o.fuse_role == 1;
+    const std::vector<int>& canon = as_rows ? c.canon_rows : c.canon_cols;
+    const int nk = ilog2(c.K), nr = ilog2(as_rows ? c.M : c.N);
+    const int L = std::min(nk, kKBlockLog);
+    const int nbits = (int)o.axes.size();
+    if (nbits != nk + nr || (int)canon.size() != nbits) throw Error(TNB_ERR_SHAPE, "fused staging: rank mismatch");
+    std::vector<int> dbit(nbits);
+    for (int p = 0; p < nbits; ++p) {
+      int db = p < L ? p : (p < nk ? p + nr : p - nk + L);
+      if (!as_rows && db >= L) db += 1;
+      dbit[canon[p]] = db;
+    }
+    const int ln = ilog2(s.N);  // result columns = the low source bits
+    nvec.assign(dbit.begin(), dbit.begin() + ln);
+    mvec.assign(dbit.begin() + ln, dbit.end());
+    f.mode = as_rows ? 1 : 2;
+    f.L = L;
+    for (int j = 0; j < 32; ++j) {
+      uint32_t v = 0;
+      for (int p = 0; p < std::min(5, ln); ++p)
+        if ((j >> p) & 1) v |= 1u << nvec[p];
+      f.dlow[j] = v;
+    }
+    f.hi = (__half2*)P->tensor_ptr(s.out);
+    f.lo = f.hi + (as_rows ? c.M * c.K : 2 * c.N * c.K);
+    f.scale = operand_scale(s.out);
+    fuse_luts.emplace_back();
+    build_lut(mvec, &fuse_luts.back());
+    fuse_luts.emplace_back();
+    build_lut(nvec, &fuse_luts.back());
+    fuse_lut_step.push_back(i);
+  };
+  auto debug_fuse = [&](int i, const StepRec& s, const FuseOut& f, const std::vector<int>& nvec,
+                        const std::vector<int>& mvec) {
+    if (!getenv("TNB_DEBUG_FUSE")) return;
+    fprintf(stderr, "TNB_FUSE step %d (%s) -> %d role %d out 2^%d fast %d vec %d nvec[0..4]", i,
+            s.kind == KIND_TC ? "tc" : "smallk", s.fuse_consumer, f.mode, (int)(nvec.size() + mvec.size()),
+            f.fast, f.vec);
+    for (size_t p = 0; p < std::min<size_t>(5, nvec.size()); ++p) fprintf(stderr, " %d", nvec[p]);
+    fprintf(stderr, " mvec[0..4]");
+    for (size_t p = 0; p < std::min<size_t>(5, mvec.size()); ++p) fprintf(stderr, " %d", mvec[p]);
+    fprintf(stderr, " lane_w");
+    for (int b = 0; b < 5; ++b) fprintf(stderr, " %d", f.fast ? ilog2(f.lane_w[b]) : -1);
+    fprintf(stderr, " exchanges %d\n", (f.xlane[0] != 0) + (f.xlane[1] != 0) + (f.xlane[2] != 0));
+  };
+  for (int i = 0; i < n_steps; ++i) {
+    StepRec& s = P->steps[i];
+    std::vector<int> nvec, mvec;
+    if (s.kind != KIND_TC) {
+      if (P->tensors[s.out].fuse_role == 0) continue;
+      // fused small-K SIMT producer: a thread owns 4 consecutive columns
+      if (!simt_uses_smallk(s.M, s.N, s.K)) throw Error(TNB_ERR_SHAPE, "fused output on a tiled SIMT step");
+      build_fuse_map(i, s, s.simt_fuse, nvec, mvec);
+      s.simt_fuse.vec = nvec.size() >= 2 && nvec[0] == 0 && nvec[1] == 1;
+      debug_fuse(i, s, s.simt_fuse, nvec, mvec);
+      continue;
+    }
+    const int64_t Kp = 2 * s.K, Np = 2 * s.N;
+    char* base = (char*)P->d_arena + s.scratch_off;
+    int64_t used = 0;
+    __half* ahi = s.fuse_rows ? (__half*)P->tensor_ptr(s.rows_t) : (__half*)base;
+    if (!s.fuse_rows) used += 2 * s.M * Kp * 2;
+    __half* alo = ahi + s.M * Kp;
+    __half* bhi = s.fuse_cols ? (__half*)P->tensor_ptr(s.cols_t) : (__half*)(base + used);
+    if (!s.fuse_cols) used += 2 * Np * Kp * 2;
+    __half* blo = bhi + Np * Kp;
+    float* ws = (float*)(base + align_up(used, kAlign));
+    const int64_t ws_elems = tc_workspace_elems(s.M, Np, Kp, P->num_sms);
+    tc_plan_gemm(&s.tc, ahi, alo, bhi, blo, s.M, Np, Kp, (float*)P->tensor_ptr(s.out), ws, ws_elems,
+                 operand_scale(s.rows_t), operand_scale(s.cols_t), P->d_tmax + P->slot[s.out],
+                 P->num_sms);
+    s.tc.progress = P->d_progress;
+    if (P->tensors[s.out].fuse_role == 0) continue;
+    if (s.tc.splits != 1) throw Error(TNB_ERR_SHAPE, "fused staging planned for a split-K step");
+    FuseOut& f = s.tc.fuse;
+    build_fuse_map(i, s, f, nvec, mvec);
+    const int ln = (int)nvec.size();
+    // fast path: vector bits n0,n1 -> destination bits 0,1; the lanes take
+    // the 5 thread-local source bits (slot bits n2..n4, lane bits m0..m4)
+    // with the lowest destination bits, swapped in by butterfly exchanges
+    f.fast = 0;
+    static const int fast_env = env_int("TNB_FUSE_FAST", 1);
+    if (fast_env && ln >= 5 && (int)mvec.size() >= 5 && nvec[0] == 0 && nvec[1] == 1) {
+      std::vector<std::pair<int, int>> loc;  // (destination bit, local bit: 0-2 slot, 3-7 lane)
+      for (int j = 0; j < 3; ++j) loc.push_back({nvec[2 + j], j});
+      for (int b = 0; b < 5; ++b) loc.push_back({mvec[b], 3 + b});
+      std::sort(loc.begin(), loc.end());
+      std::vector<char> on_lane(8, 0);
+      for (int x = 0; x < 5; ++x) on_lane[loc[x].second] = 1;
+      int dslot[3], dlane[5];
+      for (int j = 0; j < 3; ++j) dslot[j] = nvec[2 + j];
+      for (int b = 0; b < 5; ++b) dlane[b] = mvec[b];
+      int b = 0;
+      for (int j = 0; j < 3; ++j) {
+        f.xlane[j] = 0;
+        if (!on_lane[j]) continue;              // slot bit stays in the registers
+        while (on_lane[3 + b]) ++b;             // a lane bit that must leave the lanes
+        f.xlane[j] = 1 << b;
+        std::swap(dslot[j], dlane[b]);
+        ++b;
+      }
+      for (int bb = 0; bb < 5; ++bb) f.lane_w[bb] = 1u << dlane[bb];
+      for (int q = 0; q < 8; ++q) {
+        uint32_t v = 0;
+        for (int j = 0; j < 3; ++j)
+          if ((q >> j) & 1) v |= 1u << dslot[j];
+        f.slot_w[q] = v;
+      }
+      f.fast = 1;
+    }
+    debug_fuse(i, s, f, nvec, mvec);
+  }
+  P->n_fused = (int)fuse_lut_step.size();
+  if (!fuse_luts.empty()) {
+    dmalloc((void**)&P->d_fuse_luts, (int64_t)fuse_luts.size() * sizeof(ByteLut));
+    TNB_CUDA(cudaMemcpy(P->d_fuse_luts, fuse_luts.data(), fuse_luts.size() * sizeof(ByteLut),
+                        cudaMemcpyHostToDevice));
+    for (size_t e = 0; e < fuse_lut_step.size(); ++e) {
+      StepRec& st = P->steps[fuse_lut_step[e]];
+      FuseOut& f = st.kind == KIND_TC ? st.tc.fuse : st.simt_fuse;
+      f.lut_m = P->d_fuse_luts + 2 * e;
+      f.lut_n = P->d_fuse_luts + 2 * e + 1;
+    }
+  }
+
+}
+
+// ---------------------------------------------------------------------------
+// Index-order planning (the pre-pass of program_create).
+// Pre-pass over index sets: kernel kind and operand roles of every
+// step, the fused-staging edges (a tensor-core step whose result feeds a
+// tensor-core step writes it in the consumer's staged fp16 layout from its
+// epilogue), and the canonical index orders of every tensor-core step.
+// Orders are planned consumer-first (reverse step order): a consumer puts
+// contracted indices that sit on its producer's lowest result columns on
+// its lowest K bits, and the producer then orders its free indices so that
+// the consumer's lowest destination bits (low K bits, then the consumer's
+// lowest free bits) are its thread-local columns / lane-local rows -- the
+// epilogue's scattered stores then form contiguous runs.  Lists below are
+// lowest-first (canonical bit 0 first).
+struct OrderPlan {
+  std::vector<std::vector<int64_t>> ord_k, ord_rows, ord_cols;  // per step, lowest-first
+  std::vector<char> rows_is_a;      // SIMT small-K producer: m/n roles swapped if 0
+  std::vector<int> fuse_role;       // tensor -> 1/2 when written as its consumer's operand
+  std::vector<int> fuse_consumer;   // tensor -> consuming step
+};
+
+template <typename Eligible>
+OrderPlan plan_orders(const tnb_program_desc* d, const Program* P, bool use_tc, const Eligible& tc_eligible) {
+  OrderPlan op;
+  op.ord_k.resize(d->n_steps);
+  op.ord_rows.resize(d->n_steps);
+  op.ord_cols.resize(d->n_steps);
+  op.rows_is_a.assign(d->n_steps, 1);
+  auto& ord_k = op.ord_k;
+  auto& ord_rows = op.ord_rows;
+  auto& ord_cols = op.ord_cols;
+  auto& pre_rows_is_a = op.rows_is_a;
+  auto& fuse_role_pre = op.fuse_role;
+  auto& fuse_consumer_pre = op.fuse_consumer;
   {
     static const int fuse_env = [] {
       const char* e = getenv("TNB_FUSE");
@@ -554,6 +742,118 @@ Program* program_create(const tnb_program_desc* d) {
       }
     }
   }
+  return op;
+}
+
+// ---------------------------------------------------------------------------
+Program* program_create(const tnb_program_desc* d) {
+  if (!d) throw Error(TNB_ERR_ARG, "null descriptor");
+  if (d->precision != TNB_SINGLE && d->precision != TNB_DOUBLE)
+    throw Error(TNB_ERR_ARG, "precision must be TNB_SINGLE or TNB_DOUBLE");
+  if (d->n_leaves <= 0) throw Error(TNB_ERR_SHAPE, "program needs at least one leaf");
+  if (d->n_sliced < 0 || d->n_sliced > 64) throw Error(TNB_ERR_ARG, "n_sliced must be in [0, 64]");
+  int ndev = 0;
+  TNB_CUDA(cudaGetDeviceCount(&ndev));
+  if (d->device < 0 || d->device >= ndev) throw Error(TNB_ERR_NODEV, "device ordinal out of range");
+
+  std::unique_ptr<Program> P(new Program());
+  P->device = d->device;
+  P->precision = d->precision;
+  P->flags = d->flags;
+  P->esize = d->precision == TNB_SINGLE ? 8 : 16;
+  P->n_sliced = d->n_sliced;
+  P->reuse = (d->flags & TNB_FLAG_REUSE_SLICES) != 0;
+  TNB_CUDA(cudaSetDevice(P->device));
+  TNB_CUDA(cudaDeviceGetAttribute(&P->num_sms, cudaDevAttrMultiProcessorCount, P->device));
+  TNB_CUDA(cudaStreamCreateWithFlags(&P->stream, cudaStreamNonBlocking));
+  const bool use_tc = d->precision == TNB_SINGLE && !(d->flags & TNB_FLAG_NO_TENSOR_CORES) &&
+                      tc_available(P->device);
+
+  // sliced index -> mask bit (engine.py:276-279: bit n_e-1-pos pins sliced[pos])
+  std::unordered_map<int64_t, int> slice_bit;
+  for (int i = 0; i < d->n_sliced; ++i) {
+    if (slice_bit.count(d->sliced[i])) throw Error(TNB_ERR_ARG, "duplicate sliced index");
+    slice_bit[d->sliced[i]] = d->n_sliced - 1 - i;
+  }
+
+  // ---- leaves
+  std::unordered_map<int64_t, int> id2t;
+  std::vector<SlicedLeafDesc> sl_descs;
+  std::vector<uint32_t> keep;
+  int64_t leaf_off = 0, slice_off = 0, idx_off = 0;
+  P->leaf_ranks.assign(d->leaf_ranks, d->leaf_ranks + d->n_leaves);
+  for (int i = 0; i < d->n_leaves; ++i) {
+    const int r = d->leaf_ranks[i];
+    if (r < 0 || r > 32) throw Error(TNB_ERR_SHAPE, "leaf rank out of range");
+    TensorRec t;
+    t.leaf_pos = i;
+    std::vector<int64_t> full(d->leaf_indices + idx_off, d->leaf_indices + idx_off + r);
+    idx_off += r;
+    std::vector<std::pair<int, uint32_t>> sl;  // (mask bit, stride)
+    std::vector<int> keep_src;
+    for (int ax = 0; ax < r; ++ax) {
+      auto it = slice_bit.find(full[ax]);
+      if (it != slice_bit.end()) {
+        sl.push_back({it->second, 1u << (r - 1 - ax)});
+        t.dep |= 1ull << it->second;
+      } else {
+        t.axes.push_back(full[ax]);
+        keep_src.push_back(r - 1 - ax);
+      }
+    }
+    P->leaf_pool_off.push_back(leaf_off);
+    leaf_off += (int64_t)1 << r;
+    t.elems = (int64_t)1 << t.axes.size();
+    if (!sl.empty()) {
+      if (sl.size() > 8) throw Error(TNB_ERR_SHAPE, "more than 8 sliced axes on one leaf");
+      t.variant = true;
+      t.pool = POOL_SLICE;
+      t.off = slice_off;
+      slice_off += align_up(t.elems, 128);
+      SlicedLeafDesc sd{};
+      sd.src_off = P->leaf_pool_off.back();
+      sd.dst_off = t.off;
+      sd.out_elems = (uint32_t)t.elems;
+      sd.n_sl = (uint32_t)sl.size();
+      sd.keep_lut_off = (uint32_t)keep.size();
+      for (size_t j = 0; j < sl.size(); ++j) { sd.sl_bit[j] = sl[j].first; sd.sl_stride[j] = sl[j].second; }
+      // out index bit p (LSB first) <-> kept axis keep_src.size()-1-p
+      const int nk = (int)keep_src.size();
+      for (int64_t jj = 0; jj < t.elems; ++jj) {
+        uint32_t o = 0;
+        for (int p = 0; p < nk; ++p)
+          if ((jj >> p) & 1) o |= 1u << keep_src[nk - 1 - p];
+        keep.push_back(o);
+      }
+      sl_descs.push_back(sd);
+    } else {
+      t.pool = POOL_LEAF;
+      t.off = P->leaf_pool_off.back();
+    }
+    if (id2t.count(d->leaf_ids[i])) throw Error(TNB_ERR_SHAPE, "duplicate leaf id");
+    id2t[d->leaf_ids[i]] = (int)P->tensors.size();
+    P->tensors.push_back(t);
+  }
+  P->leaf_pool_elems = leaf_off;
+  P->slice_pool_elems = slice_off;
+
+  // ---- index orders and fused-staging edges (plan_orders)
+  // tensor-core eligibility: big enough to fill 128x256 tiles and amortise
+  // staging.  TNB_TC_MIN_RANK (read per program; tests lower it so small
+  // random networks exercise the tensor-core and fused-staging paths)
+  const int tc_min_rank = env_int("TNB_TC_MIN_RANK", 27);
+  auto tc_eligible = [&](int na, int nb, int nab) {
+    return use_tc && nab >= 3 && na + nb + nab >= tc_min_rank && std::max(na, nb) >= 7 &&
+           std::min(na, nb) >= 3;
+  };
+  OrderPlan op = plan_orders(d, P.get(), use_tc, tc_eligible);
+  auto& ord_k = op.ord_k;
+  auto& ord_rows = op.ord_rows;
+  auto& ord_cols = op.ord_cols;
+  auto& pre_rows_is_a = op.rows_is_a;
+  auto& fuse_role_pre = op.fuse_role;
+  auto& fuse_consumer_pre = op.fuse_consumer;
+
 
   // ---- steps: axis bookkeeping (engine.py:125-134)
   for (int i = 0; i < d->n_steps; ++i) {
@@ -677,98 +977,9 @@ Program* program_create(const tnb_program_desc* d) {
     P->root_lut = add_lut(P.get(), canon_bits(R.axes, want, {}));
   }
 
-  // ---- SIMT batching: consecutive tiled-SIMT steps of one execution
-  // sequence (the hoisted pass, or the per-slice pass) that do not consume
-  // each other's results run as one launch.  Memory planning below keeps
-  // every operand of a batch live until its last member, so members never
-  // alias each other's inputs or outputs.
-  {
-    static const int batch_env = env_int("TNB_SIMT_BATCH", 1);
-    const bool batching = batch_env && !P->reuse;
-    for (int seq = 0; batching && seq < 2; ++seq) {
-      std::vector<int> cur;
-      auto close = [&] {
-        if (cur.size() >= 2) {
-          Program::SimtBatch b{cur.front(), cur.back(), (int)cur.size(), 0, nullptr};
-          for (int i : cur) P->steps[i].batch = (int)P->batches.size();
-          P->batches.push_back(b);
-        }
-        cur.clear();
-      };
-      for (int i = 0; i < n_steps; ++i) {
-        StepRec& s = P->steps[i];
-        if ((int)s.hoisted != seq) continue;  // seq 1: hoisted pass, seq 0: per slice
-        const bool cand = s.kind == KIND_SIMT && !simt_uses_smallk(s.M, s.N, s.K) &&
-                          P->tensors[s.out].fuse_role == 0;
-        if (!cand) { close(); continue; }
-        bool dep = false;
-        for (int m : cur)
-          if (P->steps[m].out == s.a || P->steps[m].out == s.b) dep = true;
-        if (dep || cur.size() >= 128) close();
-        cur.push_back(i);
-      }
-      close();
-    }
-  }
-  std::vector<int> batch_last(n_steps, -1);  // step -> global index of its batch's last member
-  for (auto& b : P->batches)
-    for (int i = b.first_step; i <= b.last_step; ++i)
-      if (P->steps[i].batch >= 0 && &P->batches[P->steps[i].batch] == &b) batch_last[i] = b.last_step;
-
-  // ---- memory planning: persistent (hoisted) and arena (variant) tensors
-  int64_t persist_off = 0;
-  Arena arena;
-  std::vector<std::vector<int>> free_after(n_steps + 1);
-  for (int t = 0; t < (int)P->tensors.size(); ++t) {
-    const TensorRec& r = P->tensors[t];
-    if (r.def_step >= 0 && r.last_use >= 0 && r.last_use < n_steps) free_after[r.last_use].push_back(t);
-  }
-  int64_t scratch_bytes = 0;
-  std::vector<std::vector<int>> deferred(n_steps + 1);
-  for (int i = 0; i < n_steps; ++i) {
-    StepRec& s = P->steps[i];
-    TensorRec& o = P->tensors[s.out];
-    const int64_t ob = tensor_bytes(o, (int64_t)P->esize);  // fused: the consumer's fp16 planes
-    if (s.hoisted || !o.variant || o.cached) {
-      o.pool = POOL_PERSIST;
-      o.off = persist_off;
-      persist_off += align_up(ob / (int64_t)P->esize, 128);
-      if (o.cached) P->reuse_bytes += ob;
-    } else {
-      o.pool = POOL_ARENA;
-      o.off = arena.alloc(ob) / (int64_t)P->esize;
-    }
-    if (s.kind == KIND_TC) {
-      // operand staging (+ split-K workspace) lives in the arena for the
-      // duration of this step only: it shares memory with dead tensors.
-      // Fused operands are already staged (their producer wrote them).
-      const int64_t Kp = 2 * s.K, Np = 2 * s.N;
-      int64_t need = (s.fuse_rows ? 0 : 2 * s.M * Kp * 2) + (s.fuse_cols ? 0 : 2 * Np * Kp * 2);
-      need = align_up(need, kAlign) + tc_workspace_elems(s.M, Np, Kp, P->num_sms) * 4;
-      s.scratch_bytes = need;
-      if (need > 0) s.scratch_off = arena.alloc(need);
-      scratch_bytes = std::max(scratch_bytes, need);
-    }
-    // variant operands whose last use is this step are released after it
-    // (after the batch's last member when the step runs in a SIMT batch)
-    const int rel_at = batch_last[i] >= 0 ? batch_last[i] : i;
-    if (rel_at != i) {
-      deferred[rel_at].insert(deferred[rel_at].end(), free_after[i].begin(), free_after[i].end());
-    } else {
-      for (int t : free_after[i]) {
-        TensorRec& r = P->tensors[t];
-        if (r.pool == POOL_ARENA) arena.release(r.off * (int64_t)P->esize, tensor_bytes(r, (int64_t)P->esize));
-      }
-    }
-    for (int t : deferred[i]) {
-      TensorRec& r = P->tensors[t];
-      if (r.pool == POOL_ARENA) arena.release(r.off * (int64_t)P->esize, tensor_bytes(r, (int64_t)P->esize));
-    }
-    if (s.kind == KIND_TC && s.scratch_bytes > 0) arena.release(s.scratch_off, s.scratch_bytes);
-  }
-  P->persist_elems = persist_off;
-  P->arena_bytes = arena.top;
-  P->scratch_bytes = scratch_bytes;
+  // ---- SIMT batching, memory planning
+  plan_simt_batches(P.get());
+  plan_memory(P.get());
 
   // ---- device allocations
   auto dmalloc = [](void** p, int64_t bytes) {
@@ -883,159 +1094,8 @@ Program* program_create(const tnb_program_desc* d) {
     for (auto& b : P->batches) b.d_descs = P->d_simt_descs + reinterpret_cast<size_t>(b.d_descs);
   }
 
-  // ---- tensor-core plans (fixed addresses -> TMA descriptors built once)
-  dmalloc((void**)&P->d_progress, (int64_t)P->num_sms * 4);
-  // fp16 split scale of a tensor-core operand: its own max when staged, the
-  // producer's a-priori bound 2 K max|A| max|B| when the producer's epilogue
-  // wrote it (fused); producer and consumer evaluate the same ScaleSrc
-  auto operand_scale = [&](int t) {
-    ScaleSrc sc;
-    const TensorRec& r = P->tensors[t];
-    if (r.fuse_role != 0) {
-      const StepRec& p = P->steps[r.def_step];
-      sc.a = P->d_tmax + P->slot[p.kind == KIND_TC ? p.rows_t : p.a];
-      sc.b = P->d_tmax + P->slot[p.kind == KIND_TC ? p.cols_t : p.b];
-      sc.f = (float)(2.0 * (double)p.K);
-    } else {
-      sc.a = P->d_tmax + P->slot[t];
-    }
-    return sc;
-  };
-  std::vector<ByteLut> fuse_luts;
-  std::vector<int> fuse_lut_step;
-  // destination map of a fused result in its consumer's operand layout
-  // (stage_kernel's): canonical (row r, k) -> half2 index (k >> L, r,
-  // k & (2^L-1)) in [K/2^L][rows][2^L], a zero bit inserted at L for the
-  // expanded cols operand.  Returns the destination bit of every result
-  // column bit (nvec) and row bit (mvec); fills everything but the kernel-
-  // specific store-path fields.
-  auto build_fuse_map = [&](int i, StepRec& s, FuseOut& f, std::vector<int>& nvec, std::vector<int>& mvec) {
-    const TensorRec& o = P->tensors[s.out];
-    const StepRec& c = P->steps[s.fuse_consumer];
-    const bool as_rows = o.fuse_role == 1;
-    const std::vector<int>& canon = as_rows ? c.canon_rows : c.canon_cols;
-    const int nk = ilog2(c.K), nr = ilog2(as_rows ? c.M : c.N);
-    const int L = std::min(nk, kKBlockLog);
-    const int nbits = (int)o.axes.size();
-    if (nbits != nk + nr || (int)canon.size() != nbits) throw Error(TNB_ERR_SHAPE, "fused staging: rank mismatch");
-    std::vector<int> dbit(nbits);
-    for (int p = 0; p < nbits; ++p) {
-      int db = p < L ? p : (p < nk ? p + nr : p - nk + L);
-      if (!as_rows && db >= L) db += 1;
-      dbit[canon[p]] = db;
-    }
-    const int ln = ilog2(s.N);  // result columns = the low source bits
-    nvec.assign(dbit.begin(), dbit.begin() + ln);
-    mvec.assign(dbit.begin() + ln, dbit.end());
-    f.mode = as_rows ? 1 : 2;
-    f.L = L;
-    for (int j = 0; j < 32; ++j) {
-      uint32_t v = 0;
-      for (int p = 0; p < std::min(5, ln); ++p)
-        if ((j >> p) & 1) v |= 1u << nvec[p];
-      f.dlow[j] = v;
-    }
-    f.hi = (__half2*)P->tensor_ptr(s.out);
-    f.lo = f.hi + (as_rows ? c.M * c.K : 2 * c.N * c.K);
-    f.scale = operand_scale(s.out);
-    fuse_luts.emplace_back();
-    build_lut(mvec, &fuse_luts.back());
-    fuse_luts.emplace_back();
-    build_lut(nvec, &fuse_luts.back());
-    fuse_lut_step.push_back(i);
-  };
-  auto debug_fuse = [&](int i, const StepRec& s, const FuseOut& f, const std::vector<int>& nvec,
-                        const std::vector<int>& mvec) {
-    if (!getenv("TNB_DEBUG_FUSE")) return;
-    fprintf(stderr, "TNB_FUSE step %d (%s) -> %d role %d out 2^%d fast %d vec %d nvec[0..4]", i,
-            s.kind == KIND_TC ? "tc" : "smallk", s.fuse_consumer, f.mode, (int)(nvec.size() + mvec.size()),
-            f.fast, f.vec);
-    for (size_t p = 0; p < std::min<size_t>(5, nvec.size()); ++p) fprintf(stderr, " %d", nvec[p]);
-    fprintf(stderr, " mvec[0..4]");
-    for (size_t p = 0; p < std::min<size_t>(5, mvec.size()); ++p) fprintf(stderr, " %d", mvec[p]);
-    fprintf(stderr, " lane_w");
-    for (int b = 0; b < 5; ++b) fprintf(stderr, " %d", f.fast ? ilog2(f.lane_w[b]) : -1);
-    fprintf(stderr, " exchanges %d\n", (f.xlane[0] != 0) + (f.xlane[1] != 0) + (f.xlane[2] != 0));
-  };
-  for (int i = 0; i < n_steps; ++i) {
-    StepRec& s = P->steps[i];
-    std::vector<int> nvec, mvec;
-    if (s.kind != KIND_TC) {
-      if (P->tensors[s.out].fuse_role == 0) continue;
-      // fused small-K SIMT producer: a thread owns 4 consecutive columns
-      if (!simt_uses_smallk(s.M, s.N, s.K)) throw Error(TNB_ERR_SHAPE, "fused output on a tiled SIMT step");
-      build_fuse_map(i, s, s.simt_fuse, nvec, mvec);
-      s.simt_fuse.vec = nvec.size() >= 2 && nvec[0] == 0 && nvec[1] == 1;
-      debug_fuse(i, s, s.simt_fuse, nvec, mvec);
-      continue;
-    }
-    const int64_t Kp = 2 * s.K, Np = 2 * s.N;
-    char* base = (char*)P->d_arena + s.scratch_off;
-    int64_t used = 0;
-    __half* ahi = s.fuse_rows ? (__half*)P->tensor_ptr(s.rows_t) : (__half*)base;
-    if (!s.fuse_rows) used += 2 * s.M * Kp * 2;
-    __half* alo = ahi + s.M * Kp;
-    __half* bhi = s.fuse_cols ? (__half*)P->tensor_ptr(s.cols_t) : (__half*)(base + used);
-    if (!s.fuse_cols) used += 2 * Np * Kp * 2;
-    __half* blo = bhi + Np * Kp;
-    float* ws = (float*)(base + align_up(used, kAlign));
-    const int64_t ws_elems = tc_workspace_elems(s.M, Np, Kp, P->num_sms);
-    tc_plan_gemm(&s.tc, ahi, alo, bhi, blo, s.M, Np, Kp, (float*)P->tensor_ptr(s.out), ws, ws_elems,
-                 operand_scale(s.rows_t), operand_scale(s.cols_t), P->d_tmax + P->slot[s.out],
-                 P->num_sms);
-    s.tc.progress = P->d_progress;
-    if (P->tensors[s.out].fuse_role == 0) continue;
-    if (s.tc.splits != 1) throw Error(TNB_ERR_SHAPE, "fused staging planned for a split-K step");
-    FuseOut& f = s.tc.fuse;
-    build_fuse_map(i, s, f, nvec, mvec);
-    const int ln = (int)nvec.size();
-    // fast path: vector bits n0,n1 -> destination bits 0,1; the lanes take
-    // the 5 thread-local source bits (slot bits n2..n4, lane bits m0..m4)
-    // with the lowest destination bits, swapped in by butterfly exchanges
-    f.fast = 0;
-    static const int fast_env = env_int("TNB_FUSE_FAST", 1);
-    if (fast_env && ln >= 5 && (int)mvec.size() >= 5 && nvec[0] == 0 && nvec[1] == 1) {
-      std::vector<std::pair<int, int>> loc;  // (destination bit, local bit: 0-2 slot, 3-7 lane)
-      for (int j = 0; j < 3; ++j) loc.push_back({nvec[2 + j], j});
-      for (int b = 0; b < 5; ++b) loc.push_back({mvec[b], 3 + b});
-      std::sort(loc.begin(), loc.end());
-      std::vector<char> on_lane(8, 0);
-      for (int x = 0; x < 5; ++x) on_lane[loc[x].second] = 1;
-      int dslot[3], dlane[5];
-      for (int j = 0; j < 3; ++j) dslot[j] = nvec[2 + j];
-      for (int b = 0; b < 5; ++b) dlane[b] = mvec[b];
-      int b = 0;
-      for (int j = 0; j < 3; ++j) {
-        f.xlane[j] = 0;
-        if (!on_lane[j]) continue;              // slot bit stays in the registers
-        while (on_lane[3 + b]) ++b;             // a lane bit that must leave the lanes
-        f.xlane[j] = 1 << b;
-        std::swap(dslot[j], dlane[b]);
-        ++b;
-      }
-      for (int bb = 0; bb < 5; ++bb) f.lane_w[bb] = 1u << dlane[bb];
-      for (int q = 0; q < 8; ++q) {
-        uint32_t v = 0;
-        for (int j = 0; j < 3; ++j)
-          if ((q >> j) & 1) v |= 1u << dslot[j];
-        f.slot_w[q] = v;
-      }
-      f.fast = 1;
-    }
-    debug_fuse(i, s, f, nvec, mvec);
-  }
-  P->n_fused = (int)fuse_lut_step.size();
-  if (!fuse_luts.empty()) {
-    dmalloc((void**)&P->d_fuse_luts, (int64_t)fuse_luts.size() * sizeof(ByteLut));
-    TNB_CUDA(cudaMemcpy(P->d_fuse_luts, fuse_luts.data(), fuse_luts.size() * sizeof(ByteLut),
-                        cudaMemcpyHostToDevice));
-    for (size_t e = 0; e < fuse_lut_step.size(); ++e) {
-      StepRec& st = P->steps[fuse_lut_step[e]];
-      FuseOut& f = st.kind == KIND_TC ? st.tc.fuse : st.simt_fuse;
-      f.lut_m = P->d_fuse_luts + 2 * e;
-      f.lut_n = P->d_fuse_luts + 2 * e + 1;
-    }
-  }
+  // ---- tensor-core plans, fused-staging maps
+  plan_tensor_core_steps(P.get());
 
   // ---- upload leaf values
   {
