@@ -652,6 +652,9 @@ OrderPlan plan_orders(const tnb_program_desc* d, const Program* P, bool use_tc, 
       for (int r = 0; r < 2; ++r) {
         const int t = ops[r];
         if (def[t] < 0 || !fusable_producer(def[t])) continue;
+        // fused-store destination indices are 32-bit half2 offsets (the
+        // expanded cols operand has one more bit than the tensor)
+        if ((int)sets[t].size() + (r == 1 ? 1 : 0) > 31) continue;
         fuse_role_pre[t] = r + 1;
         fuse_consumer_pre[t] = c;
         if (primary < 0) primary = t;
