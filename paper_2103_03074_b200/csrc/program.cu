@@ -654,7 +654,7 @@ OrderPlan plan_orders(const tnb_program_desc* d, const Program* P, bool use_tc, 
         if (def[t] < 0 || !fusable_producer(def[t])) continue;
         // fused-store destination indices are 32-bit half2 offsets (the
         // expanded cols operand has one more bit than the tensor)
-        if ((int)sets[t].size() + (r == 1 ? 1 : 0) > 31) continue;
+        if ((int)sets[t].size() + (r == 1 ? 1 : 0) > 32) continue;
         fuse_role_pre[t] = r + 1;
         fuse_consumer_pre[t] = c;
         if (primary < 0) primary = t;

@@ -47,3 +47,30 @@ def test_n_e_63_mask_bits(gpu, workloads):
                                  precision="single")
     assert hv.slice_range == (top, top + 2)
     assert np.isfinite(hv.data).all() and np.abs(hv.data).max() > 0
+
+
+def test_c5_32_fused_matches_staged(gpu, workloads):
+    """t = 2^32 (n_e = 48): intermediates of 2^32 elements, whose fused
+    operands use the full 32-bit destination index range.  No reference
+    golden exists at this size (one CPU slice takes minutes), so the fused
+    program is checked against the staged one (TNB_FLAG_NO_FUSE), which the
+    other configs pin to the reference."""
+    import gc
+
+    from paper_2103_03074_b200 import _lib, engine as E
+
+    w = workloads("c5_32")
+    E.clear_cache()
+    fused = E.head_program(w.tn, w.tree, w.sliced, "single", flags=0)
+    assert fused.info.n_steps_fused > 0
+    hf = fused.run_range(0, 1)
+    del fused
+    E.clear_cache()
+    gc.collect()
+    staged = E.head_program(w.tn, w.tree, w.sliced, "single", flags=_lib.TNB_FLAG_NO_FUSE)
+    hs = staged.run_range(0, 1)
+    del staged
+    E.clear_cache()
+    gc.collect()
+    assert np.isfinite(hf).all() and np.abs(hs).max() > 0
+    assert rel_l2(hf, hs) < 1e-5
