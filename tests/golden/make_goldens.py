@@ -135,8 +135,10 @@ def make_golden(name):
         out["contract_tree_mask5"] = tengine.contract_tree(tn, tree, asg)
     else:
         ranges = {"s8": [(0, 4), (0, 1), (4, 8)], "m12": [(0, 1)], "c2": [(0, 1)],
-                  "c3": [(0, 1)], "c4": [(0, 1)], "c5_26": [(0, 2)]}[name]
-        stride = {"s8": 32, "m12": 64, "c2": 1, "c3": 4, "c4": 64, "c5_26": 64}[name]
+                  "c3": [(0, 1)], "c4": [(0, 1)], "c5_26": [(0, 2)], "c5_28": [(0, 1)],
+                  "c5_n21": [(0, 1)]}[name]
+        stride = {"s8": 32, "m12": 64, "c2": 1, "c3": 4, "c4": 64, "c5_26": 64, "c5_28": 64,
+                  "c5_n21": 64}[name]
         for (a, b) in ranges:
             st = tengine.EngineStats()
             t1 = time.time()
@@ -154,7 +156,8 @@ def make_golden(name):
                 out[f"head_double_{a}_{b}_sub"], out[f"head_double_{a}_{b}_norm2"] = sub(pd.data, stride)
             if (a, b) == ranges[0]:
                 full = dataclasses.replace(p, slice_range=(0, 1 << n_e))
-                amp_stride = {"s8": 1, "m12": 256, "c2": 1, "c3": 16, "c4": 16, "c5_26": 16}[name]
+                amp_stride = {"s8": 1, "m12": 256, "c2": 1, "c3": 16, "c4": 16, "c5_26": 16,
+                              "c5_28": 16, "c5_n21": 32}[name]
                 if name in ("s8", "c2"):
                     t1 = time.time()
                     tab = tengine.compute_tail_amplitudes(tn, tree, full, space_cap=30,

@@ -1,5 +1,6 @@
 """Further BASELINE configs on the GPU: C3 (m=14, 2^16 bitstrings, t=2^30) and
-the C5 sweep point t=2^26 (n_e=63) -- needs a B200."""
+the C5 sweep points t=2^26 (n_e=63), t=2^28 (n_e=58), 2^21 bitstrings, and
+t=2^32 (fused vs staged) -- needs a B200."""
 
 from __future__ import annotations
 
@@ -15,7 +16,8 @@ pytestmark = pytest.mark.gpu
 TOL = 1e-4
 
 
-@pytest.mark.parametrize("name,rng_", [("c3", (0, 1)), ("c5_26", (0, 2))])
+@pytest.mark.parametrize("name,rng_", [("c3", (0, 1)), ("c5_26", (0, 2)), ("c5_28", (0, 1)),
+                                       ("c5_n21", (0, 1))])
 def test_config_head_tail_xeb_vs_reference(gpu, workloads, name, rng_):
     w = workloads(name)
     g = golden(name)
