@@ -7,7 +7,8 @@ if len(sys.argv) > 1:
     import numpy as np, torch
     from paper_2103_03074_b200 import _lib
     lib = _lib.load()
-    M, N, K = 1 << 15, 1 << 12, 1 << 15
+    shape = [int(x) for x in os.environ.get("EXP_SHAPE", "15,12,15").split(",")]
+    M, N, K = (1 << shape[0]), (1 << shape[1]), (1 << shape[2])
     A = torch.randn(M, K, dtype=torch.complex64, device="cuda")
     B = torch.randn(K, N, dtype=torch.complex64, device="cuda")
     C = torch.empty(M, N, dtype=torch.complex64, device="cuda")
