@@ -285,6 +285,41 @@ def run_ours(args):
                "ms_per_step": e_ms / args.steps,
                "device_ms_per_step": e2e_dev_ms / args.steps}
 
+    # ---- optional: batched closed-bit assignments --
+    # 2^b s1 values in one head pass over the same slices; reported beside
+    # the headline as assignment-slices/s (a bigger correlated batch)
+    batched = None
+    if args.batch_s1 > 0:
+        from paper_2103_03074_b200.batched import cheapest_batch_qubits, compute_head_vectors_batched
+
+        qs, ratio = cheapest_batch_qubits(tn, tree, w.sliced, args.batch_s1)
+        closed = sorted(tn.fixed_output_bits)
+        s1_list = []
+        for v in range(1 << len(qs)):
+            s = dict(tn.fixed_output_bits)
+            for i, q in enumerate(qs):
+                s[q] = (v >> (len(qs) - 1 - i)) & 1
+            s1_list.append("".join(str(s[q]) for q in closed))
+        a = base
+        compute_head_vectors_batched(tn, tree, w.sliced, s1_list, slice_range=(a, a + S),
+                                     precision="single", device=local)  # compile + warm
+        barrier(dist, local)
+        b_t0 = time.perf_counter()
+        for s_ in range(args.steps):
+            a = base + s_ * S
+            compute_head_vectors_batched(tn, tree, w.sliced, s1_list, slice_range=(a, a + S),
+                                         precision="single", device=local)
+        barrier(dist, local)
+        b_ms = (time.perf_counter() - b_t0) * 1e3 / args.steps
+        batched = {"assignments": len(s1_list), "qubits": qs, "analytic_cost_ratio": ratio,
+                   "ms_per_step": b_ms,
+                   "assignment_slices_per_s": world * S * len(s1_list) / (b_ms / 1e3),
+                   "bitstrings_per_pass": len(s1_list) << len(tn.open_output_indices),
+                   "note": "head vectors of 2^b closed-bit assignments from one contraction with "
+                           "those qubits' output legs open (paper_2103_03074_b200.batched; equal to "
+                           "per-s1 runs, tests/test_batched.py); wall time incl. host copies"}
+        E.clear_cache()
+
     # ---- optional: cross-slice reuse (TNB_FLAG_REUSE_SLICES) -- reported beside the
     # headline, NOT as it: it skips re-computing results whose mask bits did not change
     reuse = None
@@ -377,6 +412,7 @@ def run_ours(args):
         "clocks": clk.summary(),
         "e2e": e2e,
         "cross_slice_reuse": reuse,
+        "batched_s1": batched,
         # linear XEB (analytics.py:46-58) of the synthetic partial amplitudes
         # accumulated over every bench step (the fixed slice subset)
         "xeb_partial_subset": float((2.0 ** 53 / amps_total.numel())
@@ -429,6 +465,8 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--reuse", type=int, default=1, help="also time TNB_FLAG_REUSE_SLICES (reported separately)")
+    ap.add_argument("--batch-s1", type=int, default=4,
+                    help="also time 2^b closed-bit assignments per head pass (reported separately)")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)
