@@ -19,6 +19,7 @@ from __future__ import annotations
 
 import argparse
 import json
+import math
 import os
 import subprocess
 import sys
@@ -320,6 +321,49 @@ def run_ours(args):
                            "per-s1 runs, tests/test_batched.py); wall time incl. host copies"}
         E.clear_cache()
 
+    # ---- optional: the co-optimised plan of the same network:
+    # same head leaves / cut / head vector, head tree + sliced set from
+    # treeopt.select_slices_b200 (frozen in tests/golden/<workload>_opt).
+    # Reported beside the headline: slices of a different plan are a
+    # different unit; the comparable figure is the time for ALL slices.
+    opt_plan = None
+    opt_dir = os.path.join(ROOT, "tests", "golden", args.workload + "_opt")
+    if args.opt_plan and os.path.isdir(opt_dir):
+        wo = tnb.load_workload(args.workload + "_opt")
+        op = E.head_program(wo.tn, wo.tree, wo.sliced, "single", device=local)
+        op.set_timing(2)
+        So = args.opt_slices
+        ob = rank * (args.warmup + args.steps) * So
+        for s_ in range(args.warmup):
+            op.run_range(ob + s_ * So, ob + (s_ + 1) * So, "fixed", out=hvec.data_ptr())
+        barrier(dist, local)
+        o_ms = o_gemm_ms = o_gemm_flops = 0.0
+        o_launches = 0
+        for s_ in range(args.warmup, args.warmup + args.steps):
+            op.run_range(ob + s_ * So, ob + (s_ + 1) * So, "fixed", out=hvec.data_ptr())
+            t = op.timing()
+            o_ms += t["total_ms"]
+            o_gemm_ms += t["gemm_ms"]
+            o_gemm_flops += t["gemm_flops"]
+            o_launches += t["launches"]
+        if dist is not None:
+            tt_ = torch.tensor([o_ms], device=dev)
+            dist.all_reduce(tt_, op=dist.ReduceOp.MAX)
+            o_ms = float(tt_.item())
+        sps = world * args.steps * So / (o_ms / 1e3)
+        opt_plan = {"workload": args.workload + "_opt", "n_e": wo.n_e,
+                    "target_space": wo.target_space, "flops_per_slice": 8.0 * wo.tc_per_slice,
+                    "slices_per_s": sps, "contraction_tflops": sps * 8.0 * wo.tc_per_slice / 1e12,
+                    "gemm_tflops": o_gemm_flops / (o_gemm_ms / 1e3) / 1e12 if o_gemm_ms else 0.0,
+                    "slices_per_step_per_gpu": So, "launches_per_step": o_launches / args.steps,
+                    "all_slices_head_s_log2": wo.n_e - math.log2(sps),
+                    "planner": wo.doc.get("planner", {}).get("tool"),
+                    "note": "device time of the co-optimised plan's head slices (same network, head "
+                            "leaves, cut and head vector as the reference plan; tests/test_gpu_treeopt.py "
+                            "pins its results to the reference engine run on that plan)"}
+        del op
+        E.clear_cache()
+
     # ---- optional: cross-slice reuse (TNB_FLAG_REUSE_SLICES) -- reported beside the
     # headline, NOT as it: it skips re-computing results whose mask bits did not change
     reuse = None
@@ -413,11 +457,17 @@ def run_ours(args):
         "e2e": e2e,
         "cross_slice_reuse": reuse,
         "batched_s1": batched,
+        "co_optimised_plan": opt_plan,
         # linear XEB (analytics.py:46-58) of the synthetic partial amplitudes
         # accumulated over every bench step (the fixed slice subset)
         "xeb_partial_subset": float((2.0 ** 53 / amps_total.numel())
                                     * float((amps_total.abs().double() ** 2).sum()) - 1.0),
     }
+    if opt_plan is not None:
+        # time for ALL 2^n_e head slices, reference plan vs co-optimised plan
+        ref_log2 = w.n_e - math.log2(value)
+        opt_plan["reference_plan_all_slices_head_s_log2"] = ref_log2
+        opt_plan["all_slices_speedup_log2"] = ref_log2 - opt_plan["all_slices_head_s_log2"]
     if world == 1 and not args.no_cpu:
         line["cpu_baseline"] = cpu_baseline(w)
     print(json.dumps(line), flush=True)
@@ -465,6 +515,9 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--reuse", type=int, default=1, help="also time TNB_FLAG_REUSE_SLICES (reported separately)")
+    ap.add_argument("--opt-plan", type=int, default=1,
+                    help="also time the co-optimised plan <workload>_opt (reported separately)")
+    ap.add_argument("--opt-slices", type=int, default=4, help="co-optimised plan slices per step per GPU")
     ap.add_argument("--batch-s1", type=int, default=4,
                     help="also time 2^b closed-bit assignments per head pass (reported separately)")
     args = ap.parse_args()

@@ -62,6 +62,10 @@ def build(force: bool = False, verbose: bool = False) -> str:
         tmp = LIB + ".tmp"
         run([nvcc, *ARCH, "-shared", "-o", tmp, *objs])
         os.replace(tmp, LIB)
+    # host-side plan optimiser (g++)
+    from .treeopt import build as build_plan
+
+    build_plan(force=force)
     return LIB
 
 

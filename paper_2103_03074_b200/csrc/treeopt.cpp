@@ -1,0 +1,664 @@
+// treeopt.cpp -- host-side head-tree / slice co-optimiser.
+//
+// The reference plans a head tree (ordering.py: hierarchical partition +
+// greedy, :256-285) and then slices it greedily on SPACE alone, rebuilding
+// the worst subtree with the same greedy after each pick
+// (slicing.py:76-196).  On the m=20 Sycamore head that leaves trees whose
+// unsliced cost is 2^81.6 multiplications and whose 2^30-space slicing
+// multiplies the work by 2.3e4 ("Planner quality").
+//
+// This optimiser keeps the reference's head/tail partition and the cut
+// indices (the head vector is unchanged: same leaves, same open legs) and
+// searches the head's pairwise order and its sliced-index set jointly for
+// the TOTAL head work 2^n_e * tc(slice) under the executor's space target:
+//   1. random-greedy trees (Boltzmann-sampled pair choice over the linear
+//      "result size - alpha * operand sizes" score; multi-threaded);
+//   2. the best few (plus the caller's tree) go through slice-and-
+//      reconfigure: slice the index that minimises the sliced cost among
+//      those on a largest tensor, then re-optimise every subtree of up to k
+//      operands EXACTLY by a subset DP (the step cost only needs the three
+//      ranks: |a u b| = (|a| + |b| + |a ^ b|) / 2 because every index has
+//      at most two endpoints), never creating a tensor above the current
+//      space;
+//   3. polish with larger subtrees, drop sliced indices the final tree no
+//      longer needs, keep the cheapest plan.
+// Cost of a step: multiplications 2^|a u b| (the reference's counter,
+// engine.py:138-140) or a B200 time model max(flops / P, bytes / BW) + t0.
+
+#include <algorithm>
+#include <array>
+#include <functional>
+#include <tuple>
+#include <atomic>
+#include <chrono>
+#include <cmath>
+#include <cstdint>
+#include <cstring>
+#include <mutex>
+#include <queue>
+#include <random>
+#include <string>
+#include <thread>
+#include <vector>
+
+#include "../../include/tnb_plan.h"
+
+namespace {
+
+constexpr int W = 32;  // 2048 index bits
+struct BS {
+  uint64_t w[W];
+  void clear() { std::memset(w, 0, sizeof(w)); }
+  void set(int i) { w[i >> 6] |= 1ull << (i & 63); }
+  void reset(int i) { w[i >> 6] &= ~(1ull << (i & 63)); }
+  bool test(int i) const { return (w[i >> 6] >> (i & 63)) & 1; }
+  int count() const {
+    int c = 0;
+    for (int k = 0; k < W; ++k) c += __builtin_popcountll(w[k]);
+    return c;
+  }
+};
+inline BS bxor(const BS& a, const BS& b) {
+  BS r;
+  for (int k = 0; k < W; ++k) r.w[k] = a.w[k] ^ b.w[k];
+  return r;
+}
+inline BS bandnot(const BS& a, const BS& b) {
+  BS r;
+  for (int k = 0; k < W; ++k) r.w[k] = a.w[k] & ~b.w[k];
+  return r;
+}
+inline int count_and(const BS& a, const BS& b) {
+  int c = 0;
+  for (int k = 0; k < W; ++k) c += __builtin_popcountll(a.w[k] & b.w[k]);
+  return c;
+}
+template <class F>
+inline void for_bits(const BS& a, F f) {
+  for (int k = 0; k < W; ++k) {
+    uint64_t x = a.w[k];
+    while (x) {
+      int b = __builtin_ctzll(x);
+      f(k * 64 + b);
+      x &= x - 1;
+    }
+  }
+}
+
+thread_local std::string g_err;
+
+struct Model {
+  int kind;        // 0 = multiplications, 1 = B200 time
+  double flops;    // complex-algorithmic FLOP/s of a contraction step
+  double bw;       // bytes/s for operand + result traffic
+  double t0;       // fixed cost per step (launch, tail of a wave)
+  double step(int ra, int rb, int ro) const {
+    int ru = (ra + rb + ro) >> 1;
+    if (kind == 0) return std::ldexp(1.0, ru);
+    double f = 8.0 * std::ldexp(1.0, ru) / flops;
+    double b = 8.0 * (std::ldexp(1.0, ra) + std::ldexp(1.0, rb) + std::ldexp(1.0, ro)) / bw;
+    return std::max(f, b) + t0;
+  }
+};
+
+struct Net {
+  int n;                 // leaves
+  int nidx;              // dense index count
+  std::vector<BS> leaf;  // index sets
+  BS sliceable;          // head-internal bonds
+};
+
+// SSA tree: nodes [0, n) leaves, [n, 2n-1) internal; kids of internal node
+// v are L[v-n], R[v-n]; children may have any id (order is rebuilt).
+struct Tree {
+  int n = 0;
+  std::vector<int> L, R;
+  int root() const { return 2 * n - 2; }
+};
+
+struct Eval {
+  std::vector<BS> set;   // per node, sliced removed
+  std::vector<int> rank;
+  std::vector<int> post; // internal nodes in post-order
+  double cost = 0;       // sum of step costs (one slice)
+  int sc = 0;            // max rank over leaves and results
+};
+
+void postorder(const Tree& t, std::vector<int>& out) {
+  out.clear();
+  if (t.n < 2) return;
+  std::vector<std::pair<int, int>> st;
+  st.push_back({t.root(), 0});
+  while (!st.empty()) {
+    auto& [v, s] = st.back();
+    if (v < t.n) { st.pop_back(); continue; }
+    if (s == 0) { s = 1; st.push_back({t.L[v - t.n], 0}); }
+    else if (s == 1) { s = 2; st.push_back({t.R[v - t.n], 0}); }
+    else { out.push_back(v); st.pop_back(); }
+  }
+}
+
+void evaluate(const Net& net, const Tree& t, const BS& sliced, const Model& m, Eval& e) {
+  int nn = 2 * t.n - 1;
+  e.set.resize(nn);
+  e.rank.resize(nn);
+  e.sc = 0;
+  for (int i = 0; i < t.n; ++i) {
+    e.set[i] = bandnot(net.leaf[i], sliced);
+    e.rank[i] = e.set[i].count();
+    e.sc = std::max(e.sc, e.rank[i]);
+  }
+  postorder(t, e.post);
+  e.cost = 0;
+  for (int v : e.post) {
+    int a = t.L[v - t.n], b = t.R[v - t.n];
+    e.set[v] = bxor(e.set[a], e.set[b]);
+    e.rank[v] = e.set[v].count();
+    e.sc = std::max(e.sc, e.rank[v]);
+    e.cost += m.step(e.rank[a], e.rank[b], e.rank[v]);
+  }
+}
+
+// ---------------------------------------------------------------- greedy
+Tree greedy_tree(const Net& net, std::mt19937_64& rng, double alpha, double tau) {
+  int n = net.n;
+  Tree t;
+  t.n = n;
+  t.L.assign(n - 1, -1);
+  t.R.assign(n - 1, -1);
+  std::vector<BS> set(2 * n - 1);
+  std::vector<int> rank(2 * n - 1);
+  std::vector<char> alive(2 * n - 1, 0);
+  std::vector<std::array<int, 2>> holder(net.nidx, {-1, -1});
+  for (int i = 0; i < n; ++i) {
+    set[i] = net.leaf[i];
+    rank[i] = set[i].count();
+    alive[i] = 1;
+    for_bits(set[i], [&](int ix) {
+      auto& h = holder[ix];
+      if (h[0] < 0) h[0] = i; else h[1] = i;
+    });
+  }
+  std::uniform_real_distribution<double> U(1e-12, 1.0);
+  auto score = [&](int a, int b) {
+    int ro = (int)(rank[a] + rank[b] - 2 * count_and(set[a], set[b]));
+    double s = std::ldexp(1.0, ro) - alpha * (std::ldexp(1.0, rank[a]) + std::ldexp(1.0, rank[b]));
+    double f = s >= 0 ? std::log2(1.0 + s) : -std::log2(1.0 - s);
+    if (tau > 0) f -= tau * -std::log(-std::log(U(rng)));
+    return f;
+  };
+  using Item = std::tuple<double, int, int>;
+  std::priority_queue<Item, std::vector<Item>, std::greater<Item>> pq;
+  for (int ix = 0; ix < net.nidx; ++ix) {
+    auto& h = holder[ix];
+    if (h[0] >= 0 && h[1] >= 0 && h[0] < h[1]) pq.push({score(h[0], h[1]), h[0], h[1]});
+  }
+  int next = n;
+  std::vector<int> nbrs;
+  while (!pq.empty()) {
+    auto [s, a, b] = pq.top();
+    pq.pop();
+    if (!alive[a] || !alive[b]) continue;
+    int c = next++;
+    t.L[c - n] = a;
+    t.R[c - n] = b;
+    alive[a] = alive[b] = 0;
+    alive[c] = 1;
+    set[c] = bxor(set[a], set[b]);
+    rank[c] = set[c].count();
+    nbrs.clear();
+    for_bits(set[c], [&](int ix) {
+      auto& h = holder[ix];
+      for (int k = 0; k < 2; ++k)
+        if (h[k] == a || h[k] == b) h[k] = c;
+      for (int k = 0; k < 2; ++k)
+        if (h[k] >= 0 && h[k] != c) nbrs.push_back(h[k]);
+    });
+    std::sort(nbrs.begin(), nbrs.end());
+    nbrs.erase(std::unique(nbrs.begin(), nbrs.end()), nbrs.end());
+    for (int o : nbrs)
+      if (alive[o]) pq.push({score(std::min(o, c), std::max(o, c)), std::min(o, c), std::max(o, c)});
+  }
+  // disconnected components: outer products, smallest first
+  std::vector<int> rest;
+  for (int v = 0; v < next; ++v)
+    if (alive[v]) rest.push_back(v);
+  while (rest.size() > 1) {
+    std::sort(rest.begin(), rest.end(), [&](int x, int y) { return rank[x] > rank[y]; });
+    int a = rest.back(); rest.pop_back();
+    int b = rest.back(); rest.pop_back();
+    int c = next++;
+    t.L[c - n] = a;
+    t.R[c - n] = b;
+    set[c] = bxor(set[a], set[b]);
+    rank[c] = set[c].count();
+    rest.push_back(c);
+  }
+  return t;
+}
+
+// ---------------------------------------------------------- reconfigure
+// Exact re-optimisation of the subtree below v restricted to a frontier of
+// <= k operands; intermediates are kept <= cap.  Returns true if improved.
+struct DP {
+  std::vector<int> rk;
+  std::vector<double> cost;
+  std::vector<int> split;
+  std::vector<BS> s;
+};
+
+bool reconf_node(const Net& net, Tree& t, int v, int k, int cap, const Model& m, Eval& e, DP& dp,
+                 std::vector<int>& freelist) {
+  (void)net;
+  int n = t.n;
+  std::vector<int> front = {t.L[v - n], t.R[v - n]};
+  std::vector<int> inner = {v};
+  while ((int)front.size() < k) {
+    int best = -1;
+    double bc = -1;
+    for (int i = 0; i < (int)front.size(); ++i) {
+      int u = front[i];
+      if (u < n) continue;
+      double c = m.step(e.rank[t.L[u - n]], e.rank[t.R[u - n]], e.rank[u]);
+      if (c > bc) { bc = c; best = i; }
+    }
+    if (best < 0) break;
+    int u = front[best];
+    front[best] = t.L[u - n];
+    front.push_back(t.R[u - n]);
+    inner.push_back(u);
+  }
+  int f = (int)front.size();
+  if (f < 3) return false;
+  double old = 0;
+  for (int u : inner) old += m.step(e.rank[t.L[u - n]], e.rank[t.R[u - n]], e.rank[u]);
+  int full = (1 << f) - 1;
+  dp.rk.resize(full + 1);
+  dp.cost.resize(full + 1);
+  dp.split.resize(full + 1);
+  dp.s.resize(full + 1);
+  dp.s[0].clear();
+  dp.rk[0] = 0;
+  for (int S = 1; S <= full; ++S) {
+    int low = __builtin_ctz(S);
+    dp.s[S] = bxor(dp.s[S & (S - 1)], e.set[front[low]]);
+    dp.rk[S] = dp.s[S].count();
+    if ((S & (S - 1)) == 0) { dp.cost[S] = 0; dp.split[S] = 0; continue; }
+    dp.cost[S] = INFINITY;
+    if (S != full && dp.rk[S] > cap) continue;
+    int lowbit = S & -S;
+    int rest = S ^ lowbit;
+    // A contains the lowest bit; enumerate A = lowbit | sub, sub proper subset of rest
+    for (int sub = (rest - 1) & rest;; sub = (sub - 1) & rest) {
+      int A = lowbit | sub, B = S ^ A;
+      double c = dp.cost[A] + dp.cost[B];
+      if (c < dp.cost[S]) {
+        c += m.step(dp.rk[A], dp.rk[B], dp.rk[S]);
+        if (c < dp.cost[S]) { dp.cost[S] = c; dp.split[S] = A; }
+      }
+      if (sub == 0) break;
+    }
+  }
+  if (!(dp.cost[full] < old * (1.0 - 1e-9))) return false;
+  // rebuild: reuse the inner ids (v stays the root of the subtree)
+  freelist.assign(inner.begin() + 1, inner.end());
+  std::vector<int> order;  // created nodes, post-order
+  std::function<int(int, bool)> build = [&](int S, bool top) -> int {
+    if ((S & (S - 1)) == 0) return front[__builtin_ctz(S)];
+    int A = dp.split[S], B = S ^ A;
+    int a = build(A, false), b = build(B, false);
+    int id;
+    if (top) id = v;
+    else { id = freelist.back(); freelist.pop_back(); }
+    t.L[id - n] = a;
+    t.R[id - n] = b;
+    e.set[id] = dp.s[S];
+    e.rank[id] = dp.rk[S];
+    return id;
+  };
+  build(full, true);
+  return true;
+}
+
+// one bottom-up pass over all internal nodes; returns number of improvements
+int reconf_pass(const Net& net, Tree& t, const BS& sliced, int k, int cap, const Model& m, Eval& e) {
+  DP dp;
+  std::vector<int> fl;
+  evaluate(net, t, sliced, m, e);
+  std::vector<int> order = e.post;
+  int improved = 0;
+  for (int v : order) {
+    if (reconf_node(net, t, v, k, cap, m, e, dp, fl)) ++improved;
+  }
+  evaluate(net, t, sliced, m, e);
+  return improved;
+}
+
+void reconf(const Net& net, Tree& t, const BS& sliced, int k, int cap, const Model& m, Eval& e,
+            int max_pass, double deadline_s, std::chrono::steady_clock::time_point t0) {
+  if (k < 3) return;
+  for (int p = 0; p < max_pass; ++p) {
+    double before = e.cost;
+    int imp = reconf_pass(net, t, sliced, k, cap, m, e);
+    if (imp == 0 || e.cost > before * (1 - 1e-4)) break;
+    if (std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count() > deadline_s) break;
+  }
+}
+
+// --------------------------------------------------------------- slicing
+struct Plan {
+  Tree t;
+  BS sliced;
+  std::vector<int> order;  // sliced indices in pick order
+  double cost = INFINITY;  // one slice
+  double total_log2 = INFINITY;
+  int sc = 0;
+};
+
+double log2_total(double cost, int ns) { return std::log2(cost) + ns; }
+
+// cost of the tree with index ix additionally sliced
+double cost_with(const Tree& t, const Eval& e, const Model& m, int ix) {
+  double c = 0;
+  int n = t.n;
+  for (int v : e.post) {
+    int a = t.L[v - n], b = t.R[v - n];
+    int ra = e.rank[a] - e.set[a].test(ix), rb = e.rank[b] - e.set[b].test(ix);
+    int ro = e.rank[v] - e.set[v].test(ix);
+    c += m.step(ra, rb, ro);
+  }
+  return c;
+}
+
+Plan slice_and_reconf(const Net& net, Tree t, const BS& init_sliced, const std::vector<int>& init_order,
+                      int target, int k, int polish_k, const Model& m, std::mt19937_64& rng,
+                      double tau, double deadline_s, std::chrono::steady_clock::time_point t0) {
+  Plan p;
+  p.sliced = init_sliced;
+  p.order = init_order;
+  Eval e;
+  evaluate(net, t, p.sliced, m, e);
+  reconf(net, t, p.sliced, k, std::max(e.sc, target), m, e, 4, deadline_s, t0);
+  std::uniform_real_distribution<double> U(1e-12, 1.0);
+  while (e.sc > target) {
+    // candidates: sliceable indices on a largest tensor
+    BS cand;
+    cand.clear();
+    for (int v = 0; v < 2 * t.n - 1; ++v)
+      if (e.rank[v] == e.sc)
+        for (int k2 = 0; k2 < W; ++k2) cand.w[k2] |= e.set[v].w[k2];
+    for (int k2 = 0; k2 < W; ++k2) cand.w[k2] &= net.sliceable.w[k2] & ~p.sliced.w[k2];
+    int best = -1;
+    double bk = INFINITY;
+    for_bits(cand, [&](int ix) {
+      double c = std::log2(cost_with(t, e, m, ix));
+      if (tau > 0) c -= tau * -std::log(-std::log(U(rng)));
+      if (c < bk) { bk = c; best = ix; }
+    });
+    if (best < 0) {
+      // a largest tensor holds only unsliceable indices: cannot reach target
+      p.cost = INFINITY;
+      p.sc = e.sc;
+      return p;
+    }
+    p.sliced.set(best);
+    p.order.push_back(best);
+    evaluate(net, t, p.sliced, m, e);
+    reconf(net, t, p.sliced, k, std::max(e.sc, target), m, e, 2, deadline_s, t0);
+  }
+  if (k < 3) {  // quick ranking mode: no reconfiguration, no polish
+    p.t = t;
+    p.cost = e.cost;
+    p.sc = e.sc;
+    p.total_log2 = log2_total(e.cost, (int)p.order.size());
+    return p;
+  }
+  // polish with bigger subtrees, then drop sliced indices that are no longer needed
+  reconf(net, t, p.sliced, polish_k, target, m, e, 3, deadline_s * 2, t0);
+  for (bool changed = true; changed;) {
+    changed = false;
+    for (size_t i = 0; i < p.order.size(); ++i) {
+      BS s2 = p.sliced;
+      s2.reset(p.order[i]);
+      Eval e2;
+      evaluate(net, t, s2, m, e2);
+      if (e2.sc <= target && log2_total(e2.cost, (int)p.order.size() - 1) < log2_total(e.cost, (int)p.order.size())) {
+        p.sliced = s2;
+        p.order.erase(p.order.begin() + i);
+        e = e2;
+        reconf(net, t, p.sliced, k, target, m, e, 2, deadline_s * 2, t0);
+        changed = true;
+        break;
+      }
+    }
+  }
+  p.t = t;
+  p.cost = e.cost;
+  p.sc = e.sc;
+  p.total_log2 = log2_total(e.cost, (int)p.order.size());
+  return p;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* tnbp_last_error(void) { return g_err.c_str(); }
+
+void tnbp_default_options(tnbp_options* o) {
+  o->target_log2 = 30;
+  o->trials = 1024;
+  o->keep_top = 16;
+  o->reconf_k = 10;
+  o->polish_k = 12;
+  o->threads = 0;
+  o->objective = 0;
+  o->seed = 0;
+  o->gemm_flops = 4.1e14;
+  o->hbm_bytes = 4.0e12;
+  o->step_s = 5e-6;
+  o->time_budget_s = 60.0;
+  o->slice_repeats = 2;
+}
+
+int tnbp_tree_cost(int n_leaves, const int* leaf_ptr, const int* leaf_idx, int n_index,
+                   const int* children, const int* sliced, int n_sliced, int objective,
+                   double* out_stats) {
+  if (n_index > W * 64) { g_err = "too many indices"; return 1; }
+  Net net;
+  net.n = n_leaves;
+  net.nidx = n_index;
+  net.leaf.resize(n_leaves);
+  for (int i = 0; i < n_leaves; ++i) {
+    net.leaf[i].clear();
+    for (int p = leaf_ptr[i]; p < leaf_ptr[i + 1]; ++p) net.leaf[i].set(leaf_idx[p]);
+  }
+  Tree t;
+  t.n = n_leaves;
+  t.L.resize(n_leaves - 1);
+  t.R.resize(n_leaves - 1);
+  for (int i = 0; i < n_leaves - 1; ++i) { t.L[i] = children[2 * i]; t.R[i] = children[2 * i + 1]; }
+  BS s;
+  s.clear();
+  for (int i = 0; i < n_sliced; ++i) s.set(sliced[i]);
+  Model m{objective, 4.1e14, 4.0e12, 5e-6};
+  Eval e;
+  evaluate(net, t, s, m, e);
+  out_stats[0] = std::log2(e.cost);
+  out_stats[1] = e.sc;
+  out_stats[2] = std::log2(e.cost) + n_sliced;
+  return 0;
+}
+
+int tnbp_optimize(int n_leaves, const int* leaf_ptr, const int* leaf_idx, int n_index,
+                  const unsigned char* sliceable, const int* init_children, const int* init_sliced,
+                  int n_init_sliced, const tnbp_options* opt, int* out_children, int* out_sliced,
+                  int* out_n_sliced, double* out_stats) {
+  try {
+    auto t0 = std::chrono::steady_clock::now();
+    if (n_leaves < 2) { g_err = "need at least two head leaves"; return 1; }
+    if (n_index > W * 64) { g_err = "more than 2048 distinct indices"; return 1; }
+    Net net;
+    net.n = n_leaves;
+    net.nidx = n_index;
+    net.leaf.resize(n_leaves);
+    std::vector<int> deg(n_index, 0);
+    for (int i = 0; i < n_leaves; ++i) {
+      net.leaf[i].clear();
+      for (int p = leaf_ptr[i]; p < leaf_ptr[i + 1]; ++p) {
+        int ix = leaf_idx[p];
+        if (ix < 0 || ix >= n_index) { g_err = "index id out of range"; return 1; }
+        net.leaf[i].set(ix);
+        ++deg[ix];
+      }
+    }
+    for (int ix = 0; ix < n_index; ++ix)
+      if (deg[ix] > 2) { g_err = "index with more than two endpoints"; return 1; }
+    net.sliceable.clear();
+    for (int ix = 0; ix < n_index; ++ix)
+      if (sliceable[ix] && deg[ix] == 2) net.sliceable.set(ix);
+    // The search runs on multiplications (its DP/slicing steer best on the
+    // raw count); objective 1 then re-ranks every finished plan by the B200
+    // time model, so the winner is the fastest of the candidates.
+    Model m{0, opt->gemm_flops, opt->hbm_bytes, opt->step_s};
+    Model mfinal{opt->objective, opt->gemm_flops, opt->hbm_bytes, opt->step_s};
+    int threads = opt->threads > 0 ? opt->threads : (int)std::max(1u, std::thread::hardware_concurrency());
+    double budget = opt->time_budget_s;
+
+    // 1. random-greedy trials (trial 0 deterministic)
+    struct Cand { double cost; int trial; Tree t; };
+    std::vector<Cand> cands;
+    std::mutex mu;
+    std::atomic<int> next{0};
+    auto worker = [&](int tid) {
+      (void)tid;
+      std::uniform_real_distribution<double> Ua(0.0, 1.2), Ut(-2.5, 0.5);
+      Eval e;
+      BS none;
+      none.clear();
+      for (;;) {
+        int i = next.fetch_add(1);
+        if (i >= opt->trials) break;
+        std::mt19937_64 rng(opt->seed * 1000003ull + (uint64_t)i * 7919ull + 1);  // per trial: thread-independent
+        if (std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count() > budget * 0.3) break;
+        double alpha = i == 0 ? 1.0 : Ua(rng);
+        double tau = i == 0 ? 0.0 : std::pow(10.0, Ut(rng));
+        Tree t = greedy_tree(net, rng, alpha, tau);
+        // rank by the total work after a quick (reconfiguration-free) slicing
+        Plan q = slice_and_reconf(net, t, none, {}, opt->target_log2, 0, 0, m, rng, 0.0, budget, t0);
+        std::lock_guard<std::mutex> g(mu);
+        cands.push_back({q.total_log2, i, std::move(t)});
+      }
+    };
+    std::vector<std::thread> pool;
+    for (int i = 0; i < threads; ++i) pool.emplace_back(worker, i);
+    for (auto& th : pool) th.join();
+    pool.clear();
+    std::sort(cands.begin(), cands.end(), [](const Cand& a, const Cand& b) {
+      return a.cost < b.cost || (a.cost == b.cost && a.trial < b.trial);
+    });
+    double best_quick = cands.empty() ? INFINITY : cands[0].cost;
+    if ((int)cands.size() > opt->keep_top) cands.resize(opt->keep_top);
+    bool have_init = init_children != nullptr;
+    if (have_init) {
+      Tree t;
+      t.n = n_leaves;
+      t.L.resize(n_leaves - 1);
+      t.R.resize(n_leaves - 1);
+      for (int i = 0; i < n_leaves - 1; ++i) { t.L[i] = init_children[2 * i]; t.R[i] = init_children[2 * i + 1]; }
+      cands.insert(cands.begin(), Cand{0, -1, std::move(t)});
+    }
+    double best_unsliced = INFINITY;
+    {
+      Eval e;
+      BS none;
+      none.clear();
+      for (auto& c : cands) {
+        evaluate(net, c.t, none, m, e);
+        best_unsliced = std::min(best_unsliced, e.cost);
+      }
+    }
+
+    // 2. slice-and-reconfigure each candidate (repeats with noisy slice picks)
+    std::vector<std::pair<int, int>> jobs;
+    for (int c = 0; c < (int)cands.size(); ++c)
+      for (int r = 0; r < std::max(1, opt->slice_repeats); ++r) jobs.push_back({c, r});
+    std::vector<Plan> plans(jobs.size());
+    next = 0;
+    BS init_s;
+    init_s.clear();
+    std::vector<int> init_order;
+    auto sworker = [&](int tid) {
+      for (;;) {
+        int j = next.fetch_add(1);
+        if (j >= (int)jobs.size()) break;
+        auto [c, r] = jobs[j];
+        (void)tid;
+        std::mt19937_64 rng(opt->seed * 7777ull + j * 131ull);
+        plans[j] = slice_and_reconf(net, cands[c].t, init_s, init_order, opt->target_log2, opt->reconf_k,
+                                    opt->polish_k, m, rng, r == 0 ? 0.0 : 0.3, budget, t0);
+      }
+    };
+    for (int i = 0; i < threads; ++i) pool.emplace_back(sworker, i);
+    for (auto& th : pool) th.join();
+    pool.clear();
+    // the caller's own sliced plan, unchanged, is a candidate too
+    if (have_init && init_sliced && n_init_sliced > 0) {
+      Plan p;
+      p.t = cands[0].t;
+      p.sliced.clear();
+      for (int i = 0; i < n_init_sliced; ++i) { p.sliced.set(init_sliced[i]); p.order.push_back(init_sliced[i]); }
+      Eval e;
+      evaluate(net, p.t, p.sliced, m, e);
+      if (e.sc <= opt->target_log2) {
+        p.cost = e.cost;
+        p.sc = e.sc;
+        p.total_log2 = log2_total(e.cost, n_init_sliced);
+        plans.push_back(std::move(p));
+      }
+    }
+    if (opt->objective != 0) {
+      Eval e;
+      for (auto& p : plans) {
+        if (!std::isfinite(p.total_log2)) continue;
+        evaluate(net, p.t, p.sliced, mfinal, e);
+        p.cost = e.cost;
+        p.total_log2 = log2_total(e.cost, (int)p.order.size());
+      }
+    }
+    int bi = -1;
+    for (int j = 0; j < (int)plans.size(); ++j)
+      if (std::isfinite(plans[j].total_log2) && (bi < 0 || plans[j].total_log2 < plans[bi].total_log2)) bi = j;
+    if (bi < 0) { g_err = "no plan reaches the space target (a largest tensor holds only cut indices)"; return 2; }
+    const Plan& P = plans[bi];
+
+    // 3. emit: internal nodes renumbered in post-order
+    std::vector<int> post;
+    postorder(P.t, post);
+    std::vector<int> newid(2 * n_leaves - 1, -1);
+    for (int i = 0; i < n_leaves; ++i) newid[i] = i;
+    for (int i = 0; i < (int)post.size(); ++i) newid[post[i]] = n_leaves + i;
+    for (int i = 0; i < (int)post.size(); ++i) {
+      int v = post[i];
+      out_children[2 * i] = newid[P.t.L[v - n_leaves]];
+      out_children[2 * i + 1] = newid[P.t.R[v - n_leaves]];
+    }
+    *out_n_sliced = (int)P.order.size();
+    for (size_t i = 0; i < P.order.size(); ++i) out_sliced[i] = P.order[i];
+    out_stats[0] = std::log2(P.cost);
+    out_stats[1] = P.sc;
+    out_stats[2] = P.total_log2;
+    out_stats[3] = std::log2(best_unsliced);
+    out_stats[4] = (double)cands.size();
+    out_stats[5] = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    out_stats[6] = (double)bi;
+    (void)best_quick;
+    out_stats[7] = (double)plans.size();
+    return 0;
+  } catch (const std::exception& ex) {
+    g_err = ex.what();
+    return 3;
+  }
+}
+
+}  // extern "C"

@@ -10,6 +10,7 @@ from __future__ import annotations
 
 try:  # pragma: no cover - depends on the environment
     from tncut.errors import (  # type: ignore
+        CannotReachCap,
         ProvenanceMismatch,
         RangeGap,
         RangeOutOfBounds,
@@ -37,6 +38,9 @@ except Exception:  # tncut not installed (e.g. the GPU box)
     class ProvenanceMismatch(TncutError):
         """Inputs were produced from different circuits, orders or modes."""
 
+    class CannotReachCap(TncutError):
+        """Slicing every contracted index still misses the space target (errors.py:77-78)."""
+
 
 __all__ = ["TncutError", "ShapeMismatch", "RangeOutOfBounds", "RangeGap", "RangeOverlap",
-           "ProvenanceMismatch"]
+           "ProvenanceMismatch", "CannotReachCap"]

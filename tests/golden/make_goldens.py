@@ -133,11 +133,21 @@ def make_golden(name):
         # whole-tree contraction with a fixed assignment (contract_tree, engine.py:147-165)
         asg = {ix: (5 >> (n_e - 1 - p)) & 1 for p, ix in enumerate(sliced)}
         out["contract_tree_mask5"] = tengine.contract_tree(tn, tree, asg)
+    elif name == "c1_opt":
+        # co-optimised plan (treeopt): the full slice sum is plan-independent,
+        # so it must equal c1's head vector and amplitudes
+        hv = tengine.compute_head_vector(tn, tree, sliced, None, precision="double")
+        out["head_full_double"] = hv.data
+        out["amps_double"] = tengine.compute_tail_amplitudes(tn, tree, hv, space_cap=8,
+                                                             precision="double").amplitudes
+        for a, b in [(0, 1), (1, 4)]:
+            out[f"head_fixed_{a}_{b}"] = tengine.compute_head_vector(
+                tn, tree, sliced, None, slice_range=(a, b), precision="double").data
     else:
-        ranges = {"s8": [(0, 4), (0, 1), (4, 8)], "m12": [(0, 1)], "c2": [(0, 1)],
+        ranges = {"s8": [(0, 4), (0, 1), (4, 8)], "s8_opt": [(0, 4), (0, 1)], "c4_opt": [(0, 1)], "m12": [(0, 1)], "c2": [(0, 1)],
                   "c3": [(0, 1)], "c4": [(0, 1)], "c5_26": [(0, 2)], "c5_28": [(0, 1)],
                   "c5_n21": [(0, 1)]}[name]
-        stride = {"s8": 32, "m12": 64, "c2": 1, "c3": 4, "c4": 64, "c5_26": 64, "c5_28": 64,
+        stride = {"s8_opt": 32, "c4_opt": 64, "s8": 32, "m12": 64, "c2": 1, "c3": 4, "c4": 64, "c5_26": 64, "c5_28": 64,
                   "c5_n21": 64}[name]
         for (a, b) in ranges:
             st = tengine.EngineStats()
@@ -150,15 +160,15 @@ def make_golden(name):
             out[f"head_single_{a}_{b}_stats"] = np.array([st.multiplications, st.head_contractions,
                                                           0, st.steps_executed])
             out[f"head_single_{a}_{b}_cpu_s"] = np.array(dt)
-            if name in ("s8", "m12"):
+            if name in ("s8", "m12", "s8_opt"):
                 pd = tengine.compute_head_vector(tn, tree, sliced, None, slice_range=(a, b),
                                                  precision="double", mode="fixed")
                 out[f"head_double_{a}_{b}_sub"], out[f"head_double_{a}_{b}_norm2"] = sub(pd.data, stride)
             if (a, b) == ranges[0]:
                 full = dataclasses.replace(p, slice_range=(0, 1 << n_e))
-                amp_stride = {"s8": 1, "m12": 256, "c2": 1, "c3": 16, "c4": 16, "c5_26": 16,
+                amp_stride = {"s8_opt": 1, "c4_opt": 16, "s8": 1, "m12": 256, "c2": 1, "c3": 16, "c4": 16, "c5_26": 16,
                               "c5_28": 16, "c5_n21": 32}[name]
-                if name in ("s8", "c2"):
+                if name in ("s8", "c2", "s8_opt"):
                     t1 = time.time()
                     tab = tengine.compute_tail_amplitudes(tn, tree, full, space_cap=30,
                                                           precision="single")

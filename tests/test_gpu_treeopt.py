@@ -1,0 +1,57 @@
+"""Co-optimised plans (treeopt) on the GPU executor.
+
+The plans in tests/golden/*_opt keep the reference's network, head/tail
+partition and cut; their goldens come from the unmodified reference engine
+run on the SAME plans (make_goldens.py).  c1_opt additionally checks the
+plan-independence of the full slice sum against c1 and the state vector.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+import paper_2103_03074_b200 as tnb
+from conftest import golden, rel_l2
+from oracle import engine_np as O
+
+pytestmark = pytest.mark.gpu
+
+TOL = 1e-4
+
+
+@pytest.mark.parametrize("precision,tol", [("double", 1e-10), ("single", TOL)])
+def test_c1_opt_full_sum_equals_reference_plan_and_statevector(gpu, workloads, precision, tol):
+    w = workloads("c1_opt")
+    g1, g = golden("c1"), golden("c1_opt")
+    hv = tnb.compute_head_vector(w.tn, w.tree, w.sliced, None, precision=precision)
+    assert rel_l2(hv.data, g["head_full_double"]) < tol
+    assert rel_l2(hv.data, g1["head_full_double"]) < tol
+    tab = tnb.compute_tail_amplitudes(w.tn, w.tree, hv, precision=precision)
+    assert rel_l2(tab.amplitudes, g1["amps_statevector"][0]) < tol
+    for a, b in [(0, 1), (1, 4)]:
+        p = tnb.compute_head_vector(w.tn, w.tree, w.sliced, None, slice_range=(a, b),
+                                    precision=precision)
+        assert rel_l2(p.data, g[f"head_fixed_{a}_{b}"]) < tol
+
+
+@pytest.mark.parametrize("name,rng_", [("s8_opt", (0, 4)), ("s8_opt", (0, 1)), ("c4_opt", (0, 1))])
+def test_opt_plan_head_tail_xeb_vs_reference(gpu, workloads, name, rng_):
+    w, g = workloads(name), golden(name)
+    a, b = rng_
+    st = tnb.EngineStats()
+    hv = tnb.compute_head_vector(w.tn, w.tree, w.sliced, None, slice_range=rng_,
+                                 precision="single", stats=st)
+    key = f"head_single_{a}_{b}"
+    stride = int(g["stride"])
+    assert rel_l2(hv.data[::stride], g[key + "_sub"]) < TOL
+    assert abs(float(np.vdot(hv.data, hv.data).real) / float(g[key + "_norm2"]) - 1) < 2 * TOL
+    assert [st.multiplications, st.head_contractions] == [int(g[key + "_stats"][0]),
+                                                          int(g[key + "_stats"][1])]
+    if (a, b) != (0, 1) or name == "c4_opt":
+        tab = tnb.tail_amplitudes_unchecked(w.tn, w.tree, hv, precision="single")
+        s2 = int(g["amps_stride"])
+        assert rel_l2(tab.amplitudes[::s2], g["amps_sub"]) < TOL
+        probs = np.abs(tab.amplitudes.astype(np.complex128)) ** 2
+        f_ref = (2.0 ** 53 / probs.size) * float(g["amps_probsum"]) - 1.0
+        assert abs(O.xeb(probs, 53) - f_ref) < 1e-3
