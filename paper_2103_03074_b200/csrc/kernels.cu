@@ -226,17 +226,19 @@ template <typename T>
 __global__ void __launch_bounds__(256)
 contract_smallk_kernel(const T* __restrict__ A, const T* __restrict__ B, T* __restrict__ C,
                        int64_t M, int64_t N, int K, const ByteLut* __restrict__ gla,
-                       const ByteLut* __restrict__ glb, unsigned int* __restrict__ max_out,
-                       const __grid_constant__ FuseOut fo) {
+                       const ByteLut* __restrict__ glb, const ByteLut* __restrict__ gle,
+                       unsigned int* __restrict__ max_out, const __grid_constant__ FuseOut fo) {
   using S = typename Scalar<T>::type;
   __shared__ uint32_t la[4][256];
   __shared__ uint32_t lb[4][256];
   __shared__ uint32_t fm[4][256];
   __shared__ uint32_t fn[4][256];
+  __shared__ uint32_t le[4][256];
   const bool fused = std::is_same<T, float2>::value && fo.mode != 0;
   for (int i = threadIdx.x; i < 1024; i += 256) {
     la[i >> 8][i & 255] = gla->t[i >> 8][i & 255];
     lb[i >> 8][i & 255] = glb->t[i >> 8][i & 255];
+    if (gle) le[i >> 8][i & 255] = gle->t[i >> 8][i & 255];
     if (fused) {
       fm[i >> 8][i & 255] = fo.lut_m->t[i >> 8][i & 255];
       fn[i >> 8][i & 255] = fo.lut_n->t[i >> 8][i & 255];
@@ -249,7 +251,12 @@ contract_smallk_kernel(const T* __restrict__ A, const T* __restrict__ B, T* __re
   float vmax = 0.f;
   for (int64_t idx = (int64_t)blockIdx.x * 256 + threadIdx.x; idx < total;
        idx += (int64_t)gridDim.x * 256) {
-    const int64_t m = idx / nq, n0 = (idx - m * nq) << 2;
+    // thread-quad index -> output quad: the enumeration LUT keeps the 5 lane
+    // bits on the output's lowest quad bits (coalesced stores) and puts the
+    // big operand's lowest storage bits right above them, so the lines a
+    // warp gathers are consumed by neighbouring warps while still in L2
+    const int64_t cq = gle ? (int64_t)lut_map(le, (uint32_t)idx) : idx;
+    const int64_t m = cq / nq, n0 = (cq - m * nq) << 2;
     S re[4] = {0, 0, 0, 0}, im[4] = {0, 0, 0, 0};
     // K is a power of two <= 8 and n0 a multiple of 4, so the canonical
     // indices m*K + k and (n0 + j)*K + k split into disjoint bit fields: one
@@ -573,13 +580,18 @@ void launch_prepare_leaves(const T* leaf_pool, T* slice_pool, const SlicedLeafDe
 
 template <typename T>
 void launch_contract_simt(const T* A, const T* B, T* C, int64_t M, int64_t N, int64_t K,
-                          const ByteLut* lutA, const ByteLut* lutB, unsigned int* max_out,
-                          const FuseOut* fuse, cudaStream_t s) {
+                          const ByteLut* lutA, const ByteLut* lutB, const ByteLut* lutE,
+                          unsigned int* max_out, const FuseOut* fuse, cudaStream_t s) {
   if (simt_uses_smallk(M, N, K)) {
     // outer-product-like: stream the output
     const FuseOut fo = fuse ? *fuse : FuseOut{};
-    contract_smallk_kernel<T><<<grid_for(M * (N >> 2), 256), 256, 0, s>>>(A, B, C, M, N, (int)K, lutA,
-                                                                            lutB, max_out, fo);
+    // resident blocks per SM: fewer keeps the gathered lines in flight
+    // inside L2 (the operand gathers are scattered below the 2^11-quad window)
+    static const int per_sm = [] { const char* e = getenv("TNB_SMALLK_BLOCKS"); return e ? atoi(e) : 16; }();
+    int64_t g = grid_for(M * (N >> 2), 256);
+    if (g > (int64_t)kSms * per_sm) g = (int64_t)kSms * per_sm;
+    contract_smallk_kernel<T><<<(int)g, 256, 0, s>>>(A, B, C, M, N, (int)K, lutA,
+                                                                            lutB, lutE, max_out, fo);
     check_launch("contract_smallk");
     return;
   }
@@ -757,8 +769,8 @@ void launch_splitk_reduce(const float* ws, int splits, int64_t elems, float* C,
   template void launch_prepare_leaves<T>(const T*, T*, const SlicedLeafDesc*, int,         \
                                          const uint32_t*, uint64_t, cudaStream_t);         \
   template void launch_contract_simt<T>(const T*, const T*, T*, int64_t, int64_t, int64_t, \
-                                        const ByteLut*, const ByteLut*, unsigned int*,     \
-                                        const FuseOut*, cudaStream_t);                     \
+                                        const ByteLut*, const ByteLut*, const ByteLut*,    \
+                                        unsigned int*, const FuseOut*, cudaStream_t);      \
   template void launch_contract_simt_batch<T>(const SimtStepDesc*, int, int64_t, cudaStream_t); \
   template void launch_permute<T>(const T*, T*, int64_t, const ByteLut*, cudaStream_t);    \
   template void launch_counter_merge<T>(const T*, const T*, int64_t, int, T*, int64_t, cudaStream_t); \

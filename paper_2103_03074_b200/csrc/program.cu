@@ -121,6 +121,7 @@ struct StepRec {
   int64_t M = 1, N = 1, K = 1;   // SIMT: rows of a, cols of b, shared. TC: rows/cols operand.
   int rows_t = -1, cols_t = -1;  // TC operand tensors (rows unexpanded, cols expanded)
   int lut_a = -1, lut_b = -1;    // SIMT: indices into the LUT table
+  int lut_e = -1;                // small-K SIMT: output-quad enumeration LUT (-1: identity)
   std::vector<int> canon_rows, canon_cols;  // TC: canonical bit -> source bit
   int st_rows = -1, st_cols = -1;           // TC: indices into Program::stages
   double mults = 0;
@@ -244,6 +245,41 @@ std::vector<int> canon_bits(const std::vector<int64_t>& axes, const std::vector<
   for (int p = 0; p < (int)kaxes.size(); ++p) src.push_back(r - 1 - pos.at(kaxes[kaxes.size() - 1 - p]));
   for (int p = 0; p < (int)raxes.size(); ++p) src.push_back(r - 1 - pos.at(raxes[raxes.size() - 1 - p]));
   return src;
+}
+
+// Enumeration order of the small-K kernel's output quads (4 consecutive
+// columns per thread): thread-index bit p -> output-quad bit order[p].
+// Lane bits 0-4 stay on the output's lowest quad bits (the store pattern the
+// fusion planner arranged); the next bits are the output bits holding the
+// big operand's lowest storage bits, so a 2^11-quad window of threads reads
+// whole lines of it (before: a fused producer's planned orders could put
+// those bits 2^20 threads apart, and every 8-B gather cost a DRAM line).
+// src_x: canonical bit -> storage bit (canon_bits: k bits first, then free).
+std::vector<int> smallk_enumeration(const std::vector<int>& src_a, const std::vector<int>& src_b,
+                                    int lm, int ln, int lk) {
+  const int Q = lm + ln - 2;
+  std::vector<int> order;
+  std::vector<char> used(std::max(Q, 0), 0);
+  for (int j = 0; j < std::min(5, Q); ++j) { order.push_back(j); used[j] = 1; }
+  const bool a_big = lm >= ln;
+  const std::vector<int>& src = a_big ? src_a : src_b;
+  std::vector<int> inv(src.size(), -1);
+  for (int c = 0; c < (int)src.size(); ++c) inv[src[c]] = c;
+  int placed = 0;
+  for (int sb = 0; sb < (int)inv.size() && placed < 6; ++sb) {
+    const int c = inv[sb];
+    if (c < lk) continue;                          // contracted: every thread loops over k
+    const int ob = a_big ? ln + (c - lk) : c - lk;  // output bit (n bits lowest)
+    if (ob < 2) continue;                          // per-thread vector bits
+    const int qb = ob - 2;
+    if (qb >= Q || used[qb]) continue;
+    order.push_back(qb);
+    used[qb] = 1;
+    ++placed;
+  }
+  for (int qb = 0; qb < Q; ++qb)
+    if (!used[qb]) order.push_back(qb);
+  return order;
 }
 
 int add_lut(Program* P, const std::vector<int>& src_bit) {
@@ -942,8 +978,15 @@ Program* program_create(const tnb_program_desc* d) {
       const TensorRec& SA = P->tensors[s.a];
       const TensorRec& SB = P->tensors[s.b];
       o.axes = afree; o.axes.insert(o.axes.end(), bfree.begin(), bfree.end());
-      s.lut_a = add_lut(P.get(), canon_bits(SA.axes, afree, shared));
-      s.lut_b = add_lut(P.get(), canon_bits(SB.axes, bfree, shared));
+      const std::vector<int> src_a = canon_bits(SA.axes, afree, shared);
+      const std::vector<int> src_b = canon_bits(SB.axes, bfree, shared);
+      s.lut_a = add_lut(P.get(), src_a);
+      s.lut_b = add_lut(P.get(), src_b);
+      static const int enum_env = env_int("TNB_SMALLK_ENUM", 1);
+      if (enum_env && simt_uses_smallk((int64_t)1 << afree.size(), (int64_t)1 << bfree.size(),
+                                       (int64_t)1 << shared.size()))
+        s.lut_e = add_lut(P.get(), smallk_enumeration(src_a, src_b, (int)afree.size(),
+                                                      (int)bfree.size(), (int)shared.size()));
     }
     if (o.axes.size() > 32) throw Error(TNB_ERR_SHAPE, "intermediate rank above 32");
     o.elems = (int64_t)1 << o.axes.size();
@@ -1314,7 +1357,7 @@ void exec_step(Program* P, StepRec& s, int parts) {
     cudaEvent_t e = C.mark(2);
     launch_contract_simt<T>((const T*)P->tensor_ptr(s.a), (const T*)P->tensor_ptr(s.b),
                             (T*)P->tensor_ptr(s.out), s.M, s.N, s.K, P->d_luts + s.lut_a,
-                            P->d_luts + s.lut_b,
+                            P->d_luts + s.lut_b, s.lut_e >= 0 ? P->d_luts + s.lut_e : nullptr,
                             P->precision == TNB_SINGLE ? P->d_tmax + P->slot[s.out] : nullptr,
                             s.simt_fuse.mode ? &s.simt_fuse : nullptr, P->stream);
     C.close(2, e);

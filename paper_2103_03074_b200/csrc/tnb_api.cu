@@ -189,7 +189,7 @@ int tnb_cgemm(int32_t device, int64_t M, int64_t N, int64_t K, const void* A, co
       TNB_CUDA(cudaMemcpyAsync(dl.p, hl, sizeof(hl), cudaMemcpyHostToDevice, st));
       const ByteLut* lut = (const ByteLut*)dl.p;
       launch_contract_simt<float2>((const float2*)pa, (const float2*)pb, (float2*)pc, M, N, K, lut,
-                                   lut + 1, nullptr, nullptr, st);
+                                   lut + 1, nullptr, nullptr, nullptr, st);
       TNB_CUDA(cudaStreamSynchronize(st));
     } else {
       const int64_t Kp = 2 * K, Np = 2 * N;

@@ -110,9 +110,10 @@ struct FuseOut;
 // C = A B over the gathered layouts; `fuse` (single precision, small-K kernel
 // only, may be null): write C as a tensor-core consumer's staged operand
 template <typename T>
+// lutE (small-K kernel only, may be null): thread-quad -> output-quad enumeration
 void launch_contract_simt(const T* A, const T* B, T* C, int64_t M, int64_t N, int64_t K,
-                          const ByteLut* lutA, const ByteLut* lutB, unsigned int* max_out,
-                          const FuseOut* fuse, cudaStream_t s);
+                          const ByteLut* lutA, const ByteLut* lutB, const ByteLut* lutE,
+                          unsigned int* max_out, const FuseOut* fuse, cudaStream_t s);
 // one step of a batched SIMT launch (contract_simt_batch_kernel)
 struct SimtStepDesc {
   const void* A;
