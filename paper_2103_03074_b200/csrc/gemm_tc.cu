@@ -25,28 +25,35 @@ namespace tnb {
 namespace {
 
 constexpr int BM = 128;                      // rows per CTA
-constexpr int BN = 256;                      // accumulator columns (fp32) per tile
+constexpr int BN = 256;                      // accumulator columns (fp32) of the widest tile
 constexpr int BK = 32;                       // fp16 elements per stage row (64 B, SWIZZLE_64B)
 constexpr int A_TILE = BM * BK * 2;          // 8 KB
-constexpr int EPI_SPLIT = 4;                 // column groups per TMEM lane quadrant
-constexpr int EPI_THREADS = 128 * EPI_SPLIT; // 16 epilogue warps: 4 lane quadrants x 4 column groups
-constexpr int EPI_COLS = BN / EPI_SPLIT;     // fp32 register accumulator columns per epilogue thread
-constexpr int NUM_THREADS = 128 + EPI_THREADS;
+constexpr int EPI_COLS = 64;                 // fp32 register accumulator columns per epilogue thread
+// Tile width NB (accumulator columns): 256 for wide B operands; 128 / 64 for
+// skinny ones (Np <= NB), whose 256-wide tiles were >= 75 % padding -- MMA,
+// TMEM and epilogue work on columns that do not exist.  One epilogue warp
+// group (4 lane quadrants) per 64 columns.
+template <int NB>
+struct Epi {
+  static constexpr int SPLIT = NB / EPI_COLS;     // column groups per TMEM lane quadrant
+  static constexpr int THREADS = 128 * SPLIT;     // epilogue threads
+  static constexpr int NUM_THREADS = 128 + THREADS;
+};
 constexpr int TMEM_COLS = 512;
 constexpr int kDefaultChunkKb = 8;           // K blocks (of 32 fp16) per promotion chunk
 constexpr int GROUP_M = 8;                   // rasterisation band height (m-tiles / CTA pairs)
 constexpr int kDefaultPaceSlack = 32;        // K blocks a unit may run ahead of the slowest
 
-template <int CG>
+template <int CG, int NB = BN>
 struct Cfg {
-  static constexpr int B_ROWS = BN / CG;                 // B rows staged by each CTA
+  static constexpr int B_ROWS = NB / CG;                 // B rows staged by each CTA
   static constexpr int B_TILE = B_ROWS * BK * 2;
   static constexpr int STAGE_BYTES = 2 * A_TILE + 2 * B_TILE;
   static constexpr int STAGES = CG == 1 ? 4 : 6;
   static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
-  // instruction descriptor: F32 accum, F16 x F16, K-major both, M = 128*CG, N = 256
+  // instruction descriptor: F32 accum, F16 x F16, K-major both, M = 128*CG, N = NB
   static constexpr uint32_t IDESC =
-      (1u << 4) | ((uint32_t)(BN >> 3) << 17) | ((uint32_t)((BM * CG) >> 4) << 24);
+      (1u << 4) | ((uint32_t)(NB >> 3) << 17) | ((uint32_t)((BM * CG) >> 4) << 24);
 };
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -153,20 +160,20 @@ __device__ __forceinline__ uint64_t make_desc_sw64(const void* smem_ptr) {
   return d;
 }
 
-template <int CG>
+template <int CG, int NB>
 __device__ __forceinline__ void umma_f16(uint32_t tmem_c, uint64_t da, uint64_t db, uint32_t acc) {
   if constexpr (CG == 1) {
     asm volatile(
         "{\n\t.reg .pred p;\n\t"
         "setp.ne.b32 p, %4, 0;\n\t"
         "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_c),
-        "l"(da), "l"(db), "r"(Cfg<1>::IDESC), "r"(acc));
+        "l"(da), "l"(db), "r"(Cfg<1, NB>::IDESC), "r"(acc));
   } else {
     asm volatile(
         "{\n\t.reg .pred p;\n\t"
         "setp.ne.b32 p, %4, 0;\n\t"
         "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_c),
-        "l"(da), "l"(db), "r"(Cfg<2>::IDESC), "r"(acc));
+        "l"(da), "l"(db), "r"(Cfg<2, NB>::IDESC), "r"(acc));
   }
 }
 
@@ -330,15 +337,15 @@ __device__ __forceinline__ WorkCoord decode(int w, int nm, int nn, int group_m) 
 // partial accumulators; the epilogue warps promote every finished partial
 // into an IEEE fp32 register accumulator (DeepGEMM-style promotion), while
 // the MMA warp fills the other partial.
-template <int CG>
-__global__ void __launch_bounds__(NUM_THREADS, 1)
+template <int CG, int NB>
+__global__ void __launch_bounds__(Epi<NB>::NUM_THREADS, 1)
 gemm_f16x3_kernel(const __grid_constant__ CUtensorMap tm_ahi, const __grid_constant__ CUtensorMap tm_alo,
                   const __grid_constant__ CUtensorMap tm_bhi, const __grid_constant__ CUtensorMap tm_blo,
                   float* __restrict__ C, int M, int Np, int Kp, int splits, int k_per_split,
                   int chunk_kb, int group_m, const ScaleSrc scale_rows, const ScaleSrc scale_cols,
                   unsigned int* __restrict__ max_out, unsigned int* __restrict__ progress,
                   int pace_slack, const __grid_constant__ FuseOut fo, int exp_skip, int epi_spin) {
-  using CF = Cfg<CG>;
+  using CF = Cfg<CG, NB>;
   constexpr int STAGES = CF::STAGES;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -355,7 +362,7 @@ gemm_f16x3_kernel(const __grid_constant__ CUtensorMap tm_ahi, const __grid_const
   const int unit = blockIdx.x / CG;       // tile-processing unit (CTA or CTA pair)
   const int n_units = gridDim.x / CG;
   const int nm = (M + BM * CG - 1) / (BM * CG);
-  const int nn = (Np + BN - 1) / BN;
+  const int nn = (Np + NB - 1) / NB;
   const int total = nm * nn * splits;
 
   if (warp == 0 && lane == 0) {
@@ -371,7 +378,7 @@ gemm_f16x3_kernel(const __grid_constant__ CUtensorMap tm_ahi, const __grid_const
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&pfull_bar[i], 1);          // MMA commit (multicast)
-      mbar_init(&pempty_bar[i], CG * EPI_THREADS);  // leader: epilogue threads of both CTAs
+      mbar_init(&pempty_bar[i], CG * Epi<NB>::THREADS);  // leader: epilogue threads of both CTAs
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -407,7 +414,7 @@ gemm_f16x3_kernel(const __grid_constant__ CUtensorMap tm_ahi, const __grid_const
       const int k_begin = wc.split * k_per_split;
       const int k_end = min(Kp, k_begin + k_per_split);
       const int m0 = wc.mb * BM * CG + (int)rank * BM;
-      const int n0 = wc.nb * BN + (int)rank * CF::B_ROWS;
+      const int n0 = wc.nb * NB + (int)rank * CF::B_ROWS;
       for (int k = k_begin; k < k_end; k += BK, ++issued) {
         if (pace && (issued & 15) == 0) {
           if (lane == 0) atomicExch(progress + unit, issued);
@@ -460,7 +467,7 @@ gemm_f16x3_kernel(const __grid_constant__ CUtensorMap tm_ahi, const __grid_const
           if (epi_spin & 2) mbar_wait(&pempty_bar[buf], ((gchunk >> 1) & 1) ^ 1);
           else mbar_wait_sleep(&pempty_bar[buf], ((gchunk >> 1) & 1) ^ 1);
           tc_fence_after();
-          const uint32_t tmem_c = tmem_base + buf * BN;
+          const uint32_t tmem_c = tmem_base + buf * NB;
           const int c1 = min(nkb, c0 + chunk_kb);
           for (int kb = c0; kb < c1; ++kb) {
             if (epi_spin & 2) mbar_wait(&full_bar[stage], phase);
@@ -475,9 +482,9 @@ gemm_f16x3_kernel(const __grid_constant__ CUtensorMap tm_ahi, const __grid_const
 #pragma unroll
               for (int kk = 0; kk < BK / 16; ++kk) {
                 const uint64_t adv = (uint64_t)(kk * 32) >> 4;  // 16 fp16 = 32 B along K
-                umma_f16<CG>(tmem_c, d_ahi + adv, d_blo + adv, (kb == c0 && kk == 0) ? 0u : 1u);
-                umma_f16<CG>(tmem_c, d_alo + adv, d_bhi + adv, 1u);
-                umma_f16<CG>(tmem_c, d_ahi + adv, d_bhi + adv, 1u);
+                umma_f16<CG, NB>(tmem_c, d_ahi + adv, d_blo + adv, (kb == c0 && kk == 0) ? 0u : 1u);
+                umma_f16<CG, NB>(tmem_c, d_alo + adv, d_bhi + adv, 1u);
+                umma_f16<CG, NB>(tmem_c, d_ahi + adv, d_bhi + adv, 1u);
               }
               umma_commit<CG>(&empty_bar[stage]);
             }
@@ -510,7 +517,7 @@ gemm_f16x3_kernel(const __grid_constant__ CUtensorMap tm_ahi, const __grid_const
         if (epi_spin & 1) mbar_wait(&pfull_bar[buf], (gchunk >> 1) & 1);
         else mbar_wait_sleep(&pfull_bar[buf], (gchunk >> 1) & 1);
         tc_fence_after();
-        const uint32_t taddr = tmem_base + ((uint32_t)(q * 32) << 16) + buf * BN + grp * EPI_COLS;
+        const uint32_t taddr = tmem_base + ((uint32_t)(q * 32) << 16) + buf * NB + grp * EPI_COLS;
 #pragma unroll
         for (int s = 0; s < EPI_COLS / 16; ++s) {
           uint32_t r[16];
@@ -524,7 +531,7 @@ gemm_f16x3_kernel(const __grid_constant__ CUtensorMap tm_ahi, const __grid_const
       }
       const int row0 = wc.mb * BM * CG + (int)rank * BM + q * 32;
       const int row = row0 + lane;
-      const int col0 = wc.nb * BN + grp * EPI_COLS;
+      const int col0 = wc.nb * NB + grp * EPI_COLS;
       {
         // max |C| of the tile (alpha > 0 is a power of two: max|x alpha| = alpha max|x|)
         float tm = 0.f;
@@ -583,6 +590,11 @@ gemm_f16x3_kernel(const __grid_constant__ CUtensorMap tm_ahi, const __grid_const
 #pragma unroll
           for (int j = 0; j < EPI_COLS; j += 4)
             *reinterpret_cast<float4*>(dst + j) = make_float4(acc[j], acc[j + 1], acc[j + 2], acc[j + 3]);
+        } else if (((Np - col0) & 3) == 0) {  // skinny B: the valid columns in 16-B stores
+#pragma unroll
+          for (int j = 0; j < EPI_COLS; j += 4)
+            if (col0 + j < Np)
+              *reinterpret_cast<float4*>(dst + j) = make_float4(acc[j], acc[j + 1], acc[j + 2], acc[j + 3]);
         } else {
 #pragma unroll
           for (int j = 0; j < EPI_COLS; ++j)
@@ -664,12 +676,21 @@ int choose_cg(int64_t M) {
   return M >= 256 ? 2 : 1;
 }
 
+// tile width: the narrowest of 64 / 128 / 256 that holds the B operand's
+// columns (TNB_GEMM_NB forces one; 0 = auto)
+int choose_nb(int64_t Np) {
+  static const int forced = env_int("TNB_GEMM_NB", 0);
+  if (forced == 64 || forced == 128 || forced == 256) return forced;
+  return Np <= 64 ? 64 : (Np <= 128 ? 128 : 256);
+}
+
 int choose_splits(int64_t M, int64_t Np, int64_t Kp, int num_sms) {
   static const int no_split = env_int("TNB_NO_SPLITK", 0);
   if (no_split) return 1;
   const int cg = choose_cg(M);
+  const int nb = choose_nb(Np);
   const int64_t units = num_sms / cg;
-  const int64_t tiles = ((M + BM * cg - 1) / (BM * cg)) * ((Np + BN - 1) / BN);
+  const int64_t tiles = ((M + BM * cg - 1) / (BM * cg)) * ((Np + nb - 1) / nb);
   const int64_t kblocks = (Kp + BK - 1) / BK;
   // split K when the tiles leave CTA units idle: as many splits as fill the
   // units (any count, not only powers of two), each keeping >= 16 K blocks
@@ -705,12 +726,13 @@ void tc_plan_gemm(TcGemmPlan* p, const __half* Ahi, const __half* Alo, const __h
     throw Error(TNB_ERR_SHAPE, "tensor-core GEMM dimension too large");
   p->M = M; p->Np = Np; p->Kp = Kp;
   p->cta_group = choose_cg(M);
+  p->nb = choose_nb(Np);
   p->splits = choose_splits(M, Np, Kp, num_sms);
   const int64_t kblocks = (Kp + BK - 1) / BK;
   p->k_per_split = ((kblocks + p->splits - 1) / p->splits) * BK;
   static const int max_sms = env_int("TNB_GEMM_MAX_SMS", 0);  // diagnostic: cap the persistent grid
   const int64_t units = (max_sms > 0 && max_sms < num_sms ? max_sms : num_sms) / p->cta_group;
-  const int64_t work = ((M + BM * p->cta_group - 1) / (BM * p->cta_group)) * ((Np + BN - 1) / BN) * p->splits;
+  const int64_t work = ((M + BM * p->cta_group - 1) / (BM * p->cta_group)) * ((Np + p->nb - 1) / p->nb) * p->splits;
   p->grid = (int)((work < units ? work : units) * p->cta_group);
   if (p->splits > 1) {
     if (workspace == nullptr || workspace_elems < (int64_t)p->splits * M * Np)
@@ -733,22 +755,22 @@ void tc_plan_gemm(TcGemmPlan* p, const __half* Ahi, const __half* Alo, const __h
   p->pace_slack = kblocks / p->splits >= pace_min_kb ? env_int("TNB_PACE", kDefaultPaceSlack) : 0;
   static const int spin = env_int("TNB_EPI_SPIN", -1);
   p->epi_spin = spin >= 0 ? spin : 0;
-  const int b_rows = BN / p->cta_group;
+  const int b_rows = p->nb / p->cta_group;
   make_map(p->tmap[0], Ahi, M, Kp, BM);
   make_map(p->tmap[1], Alo, M, Kp, BM);
   make_map(p->tmap[2], Bhi, Np, Kp, b_rows);
   make_map(p->tmap[3], Blo, Np, Kp, b_rows);
 }
 
-template <int CG>
+template <int CG, int NB>
 void launch_cg(const TcGemmPlan* p, cudaStream_t s) {
-  auto kern = gemm_f16x3_kernel<CG>;
-  TNB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg<CG>::SMEM_BYTES));
+  auto kern = gemm_f16x3_kernel<CG, NB>;
+  TNB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg<CG, NB>::SMEM_BYTES));
   const CUtensorMap* maps = reinterpret_cast<const CUtensorMap*>(p->tmap);
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(p->grid);
-  cfg.blockDim = dim3(NUM_THREADS);
-  cfg.dynamicSmemBytes = Cfg<CG>::SMEM_BYTES;
+  cfg.blockDim = dim3(Epi<NB>::NUM_THREADS);
+  cfg.dynamicSmemBytes = Cfg<CG, NB>::SMEM_BYTES;
   cfg.stream = s;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeClusterDimension;
@@ -766,8 +788,16 @@ void launch_cg(const TcGemmPlan* p, cudaStream_t s) {
 }
 
 void tc_launch_gemm(const TcGemmPlan* p, cudaStream_t s) {
-  if (p->cta_group == 2) launch_cg<2>(p, s);
-  else launch_cg<1>(p, s);
+  const int key = p->cta_group * 1000 + p->nb;
+  switch (key) {
+    case 2256: launch_cg<2, 256>(p, s); break;
+    case 2128: launch_cg<2, 128>(p, s); break;
+    case 2064: launch_cg<2, 64>(p, s); break;
+    case 1256: launch_cg<1, 256>(p, s); break;
+    case 1128: launch_cg<1, 128>(p, s); break;
+    case 1064: launch_cg<1, 64>(p, s); break;
+    default: throw Error(TNB_ERR_ARG, "unsupported GEMM tile configuration");
+  }
   check_launch("gemm_f16x3");
 }
 

@@ -217,6 +217,7 @@ struct TcGemmPlan {
   int chunk_kb = 8;              // promotion chunk (K blocks); see gemm_tc.cu
   int group_m = 16;              // raster band height (m-tiles)
   int cta_group = 1;             // 1: one CTA per 128x256 tile; 2: CTA pair per 256x256 tile
+  int nb = 256;                  // tile width (accumulator columns): 64 / 128 / 256
   unsigned int* progress = nullptr;  // device [num units]: K-block progress for soft pacing
   int pace_slack = 0;            // K blocks a unit may lead the slowest one (0: off)
   int epi_spin = 0;              // epilogue polls the TMEM-ready barrier instead of sleeping
