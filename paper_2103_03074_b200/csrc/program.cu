@@ -256,26 +256,55 @@ std::vector<int> canon_bits(const std::vector<int64_t>& axes, const std::vector<
 // those bits 2^20 threads apart, and every 8-B gather cost a DRAM line).
 // src_x: canonical bit -> storage bit (canon_bits: k bits first, then free).
 std::vector<int> smallk_enumeration(const std::vector<int>& src_a, const std::vector<int>& src_b,
-                                    int lm, int ln, int lk) {
+                                    int lm, int ln, int lk, int mode) {
   const int Q = lm + ln - 2;
   std::vector<int> order;
   std::vector<char> used(std::max(Q, 0), 0);
-  for (int j = 0; j < std::min(5, Q); ++j) { order.push_back(j); used[j] = 1; }
   const bool a_big = lm >= ln;
   const std::vector<int>& src = a_big ? src_a : src_b;
   std::vector<int> inv(src.size(), -1);
   for (int c = 0; c < (int)src.size(); ++c) inv[src[c]] = c;
-  int placed = 0;
-  for (int sb = 0; sb < (int)inv.size() && placed < 6; ++sb) {
-    const int c = inv[sb];
-    if (c < lk) continue;                          // contracted: every thread loops over k
-    const int ob = a_big ? ln + (c - lk) : c - lk;  // output bit (n bits lowest)
-    if (ob < 2) continue;                          // per-thread vector bits
-    const int qb = ob - 2;
-    if (qb >= Q || used[qb]) continue;
-    order.push_back(qb);
-    used[qb] = 1;
-    ++placed;
+  int sb = 0;
+  auto place_src = [&](int count) {  // next `count` output-quad bits by source storage order
+    int placed = 0;
+    for (; sb < (int)inv.size() && placed < count; ++sb) {
+      const int c = inv[sb];
+      if (c < lk) continue;                          // contracted: every thread loops over k
+      const int ob = a_big ? ln + (c - lk) : c - lk;  // output bit (n bits lowest)
+      if (ob < 2) continue;                          // per-thread vector bits
+      const int qb = ob - 2;
+      if (qb >= Q || used[qb]) continue;
+      order.push_back(qb);
+      used[qb] = 1;
+      ++placed;
+    }
+  };
+  auto place_out = [&](int count) {
+    for (int j = 0, placed = 0; j < Q && placed < count; ++j)
+      if (!used[j]) { order.push_back(j); used[j] = 1; ++placed; }
+  };
+  if (mode == 3) {
+    // auto: keep the output on the lanes when the big operand's lowest
+    // storage bits (below the per-thread/contracted ones) already map there
+    std::vector<char> lane(std::max(Q, 0), 0);
+    for (int j = 0; j < std::min(5, Q); ++j) lane[j] = 1;
+    int seen = 0, on_lanes = 0;
+    for (int b = 0; b < (int)inv.size() && seen < 3; ++b) {
+      const int c = inv[b];
+      if (c < lk) continue;
+      const int ob = a_big ? ln + (c - lk) : c - lk;
+      if (ob < 2 || ob - 2 >= Q) continue;
+      ++seen;
+      on_lanes += lane[ob - 2];
+    }
+    mode = seen > 0 && on_lanes == seen ? 1 : 2;
+  }
+  if (mode == 2) {  // lanes read the big operand's lines; output runs right above
+    place_src(5);
+    place_out(6);
+  } else {          // lanes write the output's lines; source lines right above
+    place_out(5);
+    place_src(6);
   }
   for (int qb = 0; qb < Q; ++qb)
     if (!used[qb]) order.push_back(qb);
@@ -982,11 +1011,11 @@ Program* program_create(const tnb_program_desc* d) {
       const std::vector<int> src_b = canon_bits(SB.axes, bfree, shared);
       s.lut_a = add_lut(P.get(), src_a);
       s.lut_b = add_lut(P.get(), src_b);
-      static const int enum_env = env_int("TNB_SMALLK_ENUM", 1);
+      static const int enum_env = env_int("TNB_SMALLK_ENUM", 3);  // 1 out-lanes, 2 src-lanes, 3 auto
       if (enum_env && simt_uses_smallk((int64_t)1 << afree.size(), (int64_t)1 << bfree.size(),
                                        (int64_t)1 << shared.size()))
         s.lut_e = add_lut(P.get(), smallk_enumeration(src_a, src_b, (int)afree.size(),
-                                                      (int)bfree.size(), (int)shared.size()));
+                                                      (int)bfree.size(), (int)shared.size(), enum_env));
     }
     if (o.axes.size() > 32) throw Error(TNB_ERR_SHAPE, "intermediate rank above 32");
     o.elems = (int64_t)1 << o.axes.size();
