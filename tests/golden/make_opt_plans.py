@@ -31,7 +31,7 @@ from paper_2103_03074_b200.workloads import load_workload  # noqa: E402
 PLANS = {
     "c1_opt": ("c1", 8, "mults", {}),
     "s8_opt": ("s8", 18, "mults", {}),
-    "c4_opt": ("c4", 30, "mults", {}),
+    "c4_opt": ("c4", 30, "mults", {"restarts": 16}),
 }
 
 
