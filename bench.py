@@ -323,13 +323,15 @@ def run_ours(args):
 
     # ---- optional: the co-optimised plan of the same network:
     # same head leaves / cut / head vector, head tree + sliced set from
-    # treeopt.select_slices_b200 (frozen in tests/golden/<workload>_opt).
+    # treeopt.select_slices_b200 (frozen in tests/golden/<workload>_opt_b200,
+    # else <workload>_opt).
     # Reported beside the headline: slices of a different plan are a
     # different unit; the comparable figure is the time for ALL slices.
     opt_plan = None
-    opt_dir = os.path.join(ROOT, "tests", "golden", args.workload + "_opt")
-    if args.opt_plan and os.path.isdir(opt_dir):
-        wo = tnb.load_workload(args.workload + "_opt")
+    opt_name = next((args.workload + sfx for sfx in ("_opt_b200", "_opt")
+                     if os.path.isdir(os.path.join(ROOT, "tests", "golden", args.workload + sfx))), None)
+    if args.opt_plan and opt_name is not None:
+        wo = tnb.load_workload(opt_name)
         op = E.head_program(wo.tn, wo.tree, wo.sliced, "single", device=local)
         op.set_timing(2)
         So = args.opt_slices
@@ -351,7 +353,7 @@ def run_ours(args):
             dist.all_reduce(tt_, op=dist.ReduceOp.MAX)
             o_ms = float(tt_.item())
         sps = world * args.steps * So / (o_ms / 1e3)
-        opt_plan = {"workload": args.workload + "_opt", "n_e": wo.n_e,
+        opt_plan = {"workload": opt_name, "n_e": wo.n_e,
                     "target_space": wo.target_space, "flops_per_slice": 8.0 * wo.tc_per_slice,
                     "slices_per_s": sps, "contraction_tflops": sps * 8.0 * wo.tc_per_slice / 1e12,
                     "gemm_tflops": o_gemm_flops / (o_gemm_ms / 1e3) / 1e12 if o_gemm_ms else 0.0,
@@ -362,6 +364,48 @@ def run_ours(args):
                             "leaves, cut and head vector as the reference plan; tests/test_gpu_treeopt.py "
                             "pins its results to the reference engine run on that plan)"}
         del op
+        E.clear_cache()
+
+    # ---- optional: the SAME slices (reference sliced set, same masks, same
+    # partial head vectors) through a re-ordered head tree
+    # (treeopt keep_slices; tests/golden/<workload>_reordered).  Reported
+    # beside the headline, which executes the reference tree as given.
+    reordered = None
+    ro_name = args.workload + "_reordered"
+    if args.reordered and os.path.isdir(os.path.join(ROOT, "tests", "golden", ro_name)):
+        wr = tnb.load_workload(ro_name)
+        assert wr.sliced == w.sliced
+        rp = E.head_program(wr.tn, wr.tree, wr.sliced, "single", device=local)
+        rp.set_timing(2)
+        Sr = args.reordered_slices
+        rb = rank * (args.warmup + args.steps) * Sr
+        for s_ in range(args.warmup):
+            rp.run_range(rb + s_ * Sr, rb + (s_ + 1) * Sr, "fixed", out=hvec.data_ptr())
+        barrier(dist, local)
+        r_ms = r_gemm_ms = r_gemm_flops = 0.0
+        r_launches = 0
+        for s_ in range(args.warmup, args.warmup + args.steps):
+            rp.run_range(rb + s_ * Sr, rb + (s_ + 1) * Sr, "fixed", out=hvec.data_ptr())
+            t = rp.timing()
+            r_ms += t["total_ms"]
+            r_gemm_ms += t["gemm_ms"]
+            r_gemm_flops += t["gemm_flops"]
+            r_launches += t["launches"]
+        if dist is not None:
+            tt_ = torch.tensor([r_ms], device=dev)
+            dist.all_reduce(tt_, op=dist.ReduceOp.MAX)
+            r_ms = float(tt_.item())
+        rsps = world * args.steps * Sr / (r_ms / 1e3)
+        reordered = {"workload": ro_name, "slices_per_s": rsps,
+                     "executed_flops_per_slice": 8.0 * wr.tc_per_slice,
+                     "executed_tflops": rsps * 8.0 * wr.tc_per_slice / 1e12,
+                     "gemm_tflops": r_gemm_flops / (r_gemm_ms / 1e3) / 1e12 if r_gemm_ms else 0.0,
+                     "slices_per_step_per_gpu": Sr, "launches_per_step": r_launches / args.steps,
+                     "note": "the reference plan's own slices (same sliced set and masks, same partial "
+                             "head vectors: tests/test_gpu_treeopt.py) with the head tree re-ordered by "
+                             "treeopt (keep_slices, exact subtree DP + B200 polish); executed FLOPs "
+                             "are the re-ordered tree's"}
+        del rp
         E.clear_cache()
 
     # ---- optional: cross-slice reuse (TNB_FLAG_REUSE_SLICES) -- reported beside the
@@ -458,11 +502,14 @@ def run_ours(args):
         "cross_slice_reuse": reuse,
         "batched_s1": batched,
         "co_optimised_plan": opt_plan,
+        "reordered_same_slices": reordered,
         # linear XEB (analytics.py:46-58) of the synthetic partial amplitudes
         # accumulated over every bench step (the fixed slice subset)
         "xeb_partial_subset": float((2.0 ** 53 / amps_total.numel())
                                     * float((amps_total.abs().double() ** 2).sum()) - 1.0),
     }
+    if reordered is not None:
+        reordered["speedup_vs_headline"] = reordered["slices_per_s"] / value
     if opt_plan is not None:
         # time for ALL 2^n_e head slices, reference plan vs co-optimised plan
         ref_log2 = w.n_e - math.log2(value)
@@ -518,6 +565,9 @@ def main():
     ap.add_argument("--opt-plan", type=int, default=1,
                     help="also time the co-optimised plan <workload>_opt (reported separately)")
     ap.add_argument("--opt-slices", type=int, default=4, help="co-optimised plan slices per step per GPU")
+    ap.add_argument("--reordered", type=int, default=1,
+                    help="also time the same slices through the re-ordered tree <workload>_reordered")
+    ap.add_argument("--reordered-slices", type=int, default=16)
     ap.add_argument("--batch-s1", type=int, default=4,
                     help="also time 2^b closed-bit assignments per head pass (reported separately)")
     args = ap.parse_args()

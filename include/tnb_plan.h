@@ -39,6 +39,8 @@ typedef struct {
   double step_s;        /* model t0: fixed seconds per step                 */
   double time_budget_s; /* soft wall-clock budget                           */
   int slice_repeats;    /* slicing runs per tree (1st greedy, rest noisy)   */
+  int keep_slices;      /* 1: init_sliced is kept as is; only the caller's  */
+                        /*    tree is re-optimised (same slices, new order) */
 } tnbp_options;
 
 void tnbp_default_options(tnbp_options* opt);

@@ -459,6 +459,7 @@ void tnbp_default_options(tnbp_options* o) {
   o->step_s = 5e-6;
   o->time_budget_s = 60.0;
   o->slice_repeats = 2;
+  o->keep_slices = 0;
 }
 
 int tnbp_tree_cost(int n_leaves, const int* leaf_ptr, const int* leaf_idx, int n_index,
@@ -550,10 +551,13 @@ int tnbp_optimize(int n_leaves, const int* leaf_ptr, const int* leaf_idx, int n_
         cands.push_back({q.total_log2, i, std::move(t)});
       }
     };
+    const bool keep = opt->keep_slices && init_children && init_sliced && n_init_sliced > 0;
     std::vector<std::thread> pool;
-    for (int i = 0; i < threads; ++i) pool.emplace_back(worker, i);
-    for (auto& th : pool) th.join();
-    pool.clear();
+    if (!keep) {
+      for (int i = 0; i < threads; ++i) pool.emplace_back(worker, i);
+      for (auto& th : pool) th.join();
+      pool.clear();
+    }
     std::sort(cands.begin(), cands.end(), [](const Cand& a, const Cand& b) {
       return a.cost < b.cost || (a.cost == b.cost && a.trial < b.trial);
     });
@@ -581,7 +585,7 @@ int tnbp_optimize(int n_leaves, const int* leaf_ptr, const int* leaf_idx, int n_
 
     // 2. slice-and-reconfigure each candidate (repeats with noisy slice picks)
     std::vector<std::pair<int, int>> jobs;
-    for (int c = 0; c < (int)cands.size(); ++c)
+    for (int c = 0; !keep && c < (int)cands.size(); ++c)
       for (int r = 0; r < std::max(1, opt->slice_repeats); ++r) jobs.push_back({c, r});
     std::vector<Plan> plans(jobs.size());
     next = 0;
@@ -630,7 +634,29 @@ int tnbp_optimize(int n_leaves, const int* leaf_ptr, const int* leaf_idx, int n_
     for (int j = 0; j < (int)plans.size(); ++j)
       if (std::isfinite(plans[j].total_log2) && (bi < 0 || plans[j].total_log2 < plans[bi].total_log2)) bi = j;
     if (bi < 0) { g_err = "no plan reaches the space target (a largest tensor holds only cut indices)"; return 2; }
-    const Plan& P = plans[bi];
+    Plan& P = plans[bi];
+    if (keep) {  // same slices: exact re-optimisation of the order (then the B200 polish)
+      Eval e;
+      evaluate(net, P.t, P.sliced, m, e);
+      reconf(net, P.t, P.sliced, opt->polish_k, opt->target_log2, m, e, 6, budget * 4, t0);
+      P.cost = e.cost;
+      P.sc = e.sc;
+      P.total_log2 = log2_total(e.cost, (int)P.order.size());
+    }
+    if (opt->objective != 0) {
+      // B200 polish: re-optimise every subtree under the time model with the
+      // sliced set fixed.  A big tensor absorbing small operands one at a
+      // time costs an HBM pass per step although its multiplication count
+      // is small; the exact DP merges the small operands first where that
+      // is faster (the reference's branch merging, ordering.py:547-661,
+      // generalised to any subtree of <= polish_k operands).
+      Eval e;
+      evaluate(net, P.t, P.sliced, mfinal, e);
+      reconf(net, P.t, P.sliced, opt->polish_k, opt->target_log2, mfinal, e, 6, budget * 4, t0);
+      P.cost = e.cost;
+      P.sc = e.sc;
+      P.total_log2 = log2_total(e.cost, (int)P.order.size());
+    }
 
     // 3. emit: internal nodes renumbered in post-order
     std::vector<int> post;

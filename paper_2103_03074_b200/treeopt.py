@@ -57,6 +57,7 @@ class Options(ctypes.Structure):  # tnb_plan.h: tnbp_options
         ("step_s", ctypes.c_double),
         ("time_budget_s", ctypes.c_double),
         ("slice_repeats", ctypes.c_int),
+        ("keep_slices", ctypes.c_int),
     ]
 
 
@@ -200,7 +201,7 @@ def select_slices_b200(tn, tree, target_space: int, *, objective: str = "mults",
                        seed: int = 0, time_budget_s: float = 60.0,
                        initial_slices=None, gemm_flops: float = 4.1e14,
                        hbm_bytes: float = 4.0e12, step_s: float = 5e-6, stats: dict | None = None,
-                       restarts: int = 1):
+                       restarts: int = 1, keep_slices: bool = False):
     """Drop-in for ``tncut.slicing.select_slices`` (slicing.py:76-196).
 
     Returns ``(SlicePlan, ContractionTree)``.  ``initial_slices`` (e.g. the
@@ -208,7 +209,10 @@ def select_slices_b200(tn, tree, target_space: int, *, objective: str = "mults",
     receives the optimiser's figures (log2 costs, seconds, candidates).
     ``restarts`` runs the search with seeds seed, seed+1, ... and keeps the
     cheapest plan: the greedy slicing path is seed-sensitive (C4 at 2^30:
-    2^69.8 - 2^77.0 total over seeds 0-6).
+    2^69.8 - 2^77.0 total over seeds 0-6).  ``keep_slices`` (with
+    ``initial_slices``) keeps the caller's sliced set and only re-optimises
+    the head tree's order: the same slices (same mask -> same partial head
+    vector), computed by a cheaper tree.
     """
     if restarts > 1:
         best = None
@@ -219,7 +223,7 @@ def select_slices_b200(tn, tree, target_space: int, *, objective: str = "mults",
                                      slice_repeats=slice_repeats, threads=threads, seed=seed + r,
                                      time_budget_s=time_budget_s, initial_slices=initial_slices,
                                      gemm_flops=gemm_flops, hbm_bytes=hbm_bytes, step_s=step_s,
-                                     stats=st)
+                                     stats=st, keep_slices=keep_slices)
             if best is None or st["log2_total"] < best[1]["log2_total"]:
                 best = (res, dict(st, seed=seed + r))
         if stats is not None:
@@ -244,6 +248,7 @@ def select_slices_b200(tn, tree, target_space: int, *, objective: str = "mults",
     opt.step_s = float(step_s)
     opt.time_budget_s = float(time_budget_s)
     opt.slice_repeats = int(slice_repeats)
+    opt.keep_slices = int(bool(keep_slices))
     n = hp.n
     out_ch = np.zeros(2 * (n - 1), np.int32)
     out_sl = np.zeros(len(hp.index_ids), np.int32)

@@ -35,7 +35,8 @@ def test_c1_opt_full_sum_equals_reference_plan_and_statevector(gpu, workloads, p
         assert rel_l2(p.data, g[f"head_fixed_{a}_{b}"]) < tol
 
 
-@pytest.mark.parametrize("name,rng_", [("s8_opt", (0, 4)), ("s8_opt", (0, 1)), ("c4_opt", (0, 1))])
+@pytest.mark.parametrize("name,rng_", [("s8_opt", (0, 4)), ("s8_opt", (0, 1)), ("c4_opt", (0, 1)),
+                                       ("c4_opt_b200", (0, 1))])
 def test_opt_plan_head_tail_xeb_vs_reference(gpu, workloads, name, rng_):
     w, g = workloads(name), golden(name)
     a, b = rng_
@@ -48,10 +49,26 @@ def test_opt_plan_head_tail_xeb_vs_reference(gpu, workloads, name, rng_):
     assert abs(float(np.vdot(hv.data, hv.data).real) / float(g[key + "_norm2"]) - 1) < 2 * TOL
     assert [st.multiplications, st.head_contractions] == [int(g[key + "_stats"][0]),
                                                           int(g[key + "_stats"][1])]
-    if (a, b) != (0, 1) or name == "c4_opt":
+    if (a, b) != (0, 1) or name.startswith("c4_opt"):
         tab = tnb.tail_amplitudes_unchecked(w.tn, w.tree, hv, precision="single")
         s2 = int(g["amps_stride"])
         assert rel_l2(tab.amplitudes[::s2], g["amps_sub"]) < TOL
         probs = np.abs(tab.amplitudes.astype(np.complex128)) ** 2
         f_ref = (2.0 ** 53 / probs.size) * float(g["amps_probsum"]) - 1.0
         assert abs(O.xeb(probs, 53) - f_ref) < 1e-3
+
+
+def test_c4_reordered_same_slices_as_reference_plan(gpu, workloads):
+    """c4_reordered keeps the reference plan's sliced set (same masks, same
+    partial head vectors) with a re-ordered head tree: its slice [0,1)
+    equals the reference engine's c4 golden; slices [0,4) equal the
+    executor's own result on the reference tree."""
+    w, r = workloads("c4_reordered"), workloads("c4")
+    assert w.sliced == r.sliced
+    g = golden("c4")
+    hv = tnb.compute_head_vector(w.tn, w.tree, w.sliced, None, slice_range=(0, 1), precision="single")
+    stride = int(g["stride"])
+    assert rel_l2(hv.data[::stride], g["head_single_0_1_sub"]) < TOL
+    a = tnb.compute_head_vector(w.tn, w.tree, w.sliced, None, slice_range=(0, 4), precision="single")
+    b = tnb.compute_head_vector(r.tn, r.tree, r.sliced, None, slice_range=(0, 4), precision="single")
+    assert rel_l2(a.data, b.data) < TOL

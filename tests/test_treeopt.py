@@ -23,7 +23,7 @@ from conftest import ROOT, golden, import_reference, reference_available, rel_l2
 from paper_2103_03074_b200 import treeopt
 from paper_2103_03074_b200.planner import split, step_mults
 
-OPT = {"c1_opt": "c1", "s8_opt": "s8", "c4_opt": "c4"}
+OPT = {"c1_opt": "c1", "s8_opt": "s8", "c4_opt": "c4", "c4_opt_b200": "c4", "c4_reordered": "c4"}
 
 
 @pytest.fixture(scope="module")
@@ -103,10 +103,39 @@ def test_optimiser_deterministic_and_never_worse(workloads, lib):
     ref_total = math.log2(w.tc_per_slice) + w.n_e
     assert math.log2(p1.per_subtask.tc) + len(p1.sliced_indices) <= ref_total
     assert p1.per_subtask.sc_log2 <= w.target_space
-    # the b200 objective re-ranks candidates by the time model: never slower
+    # the b200 objective re-ranks candidates by the time model and polishes
+    # the winner under it: never slower (in the model) than the mults plan
     pb, tb = treeopt.select_slices_b200(w.tn, w.tree, w.target_space, objective="b200", **kw)
     assert (treeopt.tree_cost(w.tn, tb, pb.sliced_indices, "b200")[2]
             <= treeopt.tree_cost(w.tn, t1, p1.sliced_indices, "b200")[2] + 1e-9)
+
+
+def test_b200_polish_keeps_slices_and_lowers_model_time(workloads, lib):
+    """c4_opt_b200 = c4_opt's sliced set, subtrees re-optimised under the
+    B200 time model (merging small operands before they meet a big one)."""
+    w, b = workloads("c4_opt"), workloads("c4_opt_b200")
+    assert b.sliced == w.sliced
+    assert (treeopt.tree_cost(b.tn, b.tree, b.sliced, "b200")[0]
+            < treeopt.tree_cost(w.tn, w.tree, w.sliced, "b200")[0] - 0.2)
+
+
+def test_reordered_keeps_the_reference_slices(workloads, lib):
+    w, r = workloads("c4_reordered"), workloads("c4")
+    assert w.sliced == r.sliced
+    assert math.log2(w.tc_per_slice) < math.log2(r.tc_per_slice) - 4
+
+
+def test_restarts_keep_the_best_seed(workloads, lib):
+    w = workloads("s8")
+    kw = dict(trials=16, keep_top=2, reconf_k=6, polish_k=6, time_budget_s=600, threads=2)
+    totals = []
+    for sd in (5, 6):
+        st = {}
+        treeopt.select_slices_b200(w.tn, w.tree, w.target_space, seed=sd, stats=st, **kw)
+        totals.append(st["log2_total"])
+    st = {}
+    treeopt.select_slices_b200(w.tn, w.tree, w.target_space, seed=5, restarts=2, stats=st, **kw)
+    assert abs(st["log2_total"] - min(totals)) < 1e-9 and st["restarts"] == 2
 
 
 def test_unreachable_target_raises(workloads, lib):
