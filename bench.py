@@ -407,6 +407,25 @@ def run_ours(args):
                              "are the re-ordered tree's"}
         del rp
         E.clear_cache()
+        # the same through the public API (set_reorder; host buffers, leaves
+        # H2D and the head vector D2H every call)
+        tnb.set_reorder(True)
+        try:
+            a0 = base + total_slices  # slices beyond the headline subset
+            tnb.compute_head_vector(tn, tree, w.sliced, None, slice_range=(a0, a0 + Sr),
+                                    precision="single", device=local)  # plan + compile
+            barrier(dist, local)
+            e_t0 = time.perf_counter()
+            for s_ in range(args.steps):
+                a = a0 + (s_ + 1) * Sr
+                hv = tnb.compute_head_vector(tn, tree, w.sliced, None, slice_range=(a, a + Sr),
+                                             precision="single", device=local)
+            barrier(dist, local)
+            re_ms = (time.perf_counter() - e_t0) * 1e3
+        finally:
+            tnb.set_reorder(False)
+        reordered["e2e_api_slices_per_s"] = world * args.steps * Sr / (re_ms / 1e3)
+        E.clear_cache()
 
     # ---- optional: cross-slice reuse (TNB_FLAG_REUSE_SLICES) -- reported beside the
     # headline, NOT as it: it skips re-computing results whose mask bits did not change

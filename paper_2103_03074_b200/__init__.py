@@ -19,6 +19,7 @@ from .engine import (  # noqa: F401
     reduce_partials,
     set_device,
     set_flags,
+    set_reorder,
     tail_amplitudes_unchecked,
 )
 from .errors import (  # noqa: F401

@@ -72,3 +72,24 @@ def test_c4_reordered_same_slices_as_reference_plan(gpu, workloads):
     a = tnb.compute_head_vector(w.tn, w.tree, w.sliced, None, slice_range=(0, 4), precision="single")
     b = tnb.compute_head_vector(r.tn, r.tree, r.sliced, None, slice_range=(0, 4), precision="single")
     assert rel_l2(a.data, b.data) < TOL
+
+
+def test_set_reorder_same_head_vectors(gpu, workloads):
+    """Opt-in re-ordering through the public API: same slices, same partial
+    head vectors (vs the reference goldens), reference counters unchanged."""
+    from paper_2103_03074_b200 import engine as E
+
+    try:
+        tnb.set_reorder(True)
+        for name, rng_ in (("s8", (0, 4)), ("c4", (0, 1))):
+            w, g = workloads(name), golden(name)
+            st = tnb.EngineStats()
+            hv = tnb.compute_head_vector(w.tn, w.tree, w.sliced, None, slice_range=rng_,
+                                         precision="single", stats=st)
+            key = f"head_single_{rng_[0]}_{rng_[1]}"
+            assert rel_l2(hv.data[::int(g["stride"])], g[key + "_sub"]) < TOL
+            assert [st.multiplications, st.head_contractions] == [int(g[key + "_stats"][0]),
+                                                                  int(g[key + "_stats"][1])]
+        assert len(E._reorder_cache) >= 2
+    finally:
+        tnb.set_reorder(False)
