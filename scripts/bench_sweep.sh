@@ -18,6 +18,8 @@ import json
 for line in open("$OUT"):
     d = json.loads(line)
     r = d.get("cross_slice_reuse") or {}
+    o = d.get("reordered_same_slices") or {}
     print(f"{d['config']['workload'][:40]:40s} n_e? slices/s {d['value']:.3f} TFLOP/s {d['contraction_tflops']:.1f} "
-          f"gemm {d['roofline']['achieved']:.0f} reuse {r.get('value', 0):.2f} xeb {d['xeb_partial_subset']:.4g}")
+          f"gemm {d['roofline']['achieved']:.0f} reuse {r.get('value', 0):.2f} xeb {d['xeb_partial_subset']:.4g} "
+          f"reordered {o.get('slices_per_s', 0):.2f} ({o.get('executed_tflops', 0):.0f} TFLOP/s executed)")
 EOF

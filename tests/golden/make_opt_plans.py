@@ -38,6 +38,9 @@ PLANS = {
     # the reference plan's OWN sliced set (same slices, same partial head
     # vectors), head tree re-ordered: exact DP, then the B200 polish
     "c4_reordered": ("c4", 30, "b200", {"keep_slices": True}),
+    "c5_26_reordered": ("c5_26", 26, "b200", {"keep_slices": True}),
+    "c5_28_reordered": ("c5_28", 28, "b200", {"keep_slices": True}),
+    "c5_32_reordered": ("c5_32", 32, "b200", {"keep_slices": True}),
 }
 
 

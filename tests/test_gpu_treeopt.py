@@ -93,3 +93,24 @@ def test_set_reorder_same_head_vectors(gpu, workloads):
         assert len(E._reorder_cache) >= 2
     finally:
         tnb.set_reorder(False)
+
+
+@pytest.mark.parametrize("name,rng_", [("c5_26", (0, 2)), ("c5_28", (0, 1))])
+def test_sweep_reordered_same_slices_vs_reference(gpu, workloads, name, rng_):
+    w, g = workloads(name + "_reordered"), golden(name)
+    assert w.sliced == workloads(name).sliced
+    hv = tnb.compute_head_vector(w.tn, w.tree, w.sliced, None, slice_range=rng_, precision="single")
+    key = f"head_single_{rng_[0]}_{rng_[1]}"
+    assert rel_l2(hv.data[::int(g["stride"])], g[key + "_sub"]) < TOL
+
+
+def test_c5_32_reordered_matches_given_tree(gpu, workloads):
+    import gc
+
+    w, r = workloads("c5_32_reordered"), workloads("c5_32")
+    a = tnb.compute_head_vector(w.tn, w.tree, w.sliced, None, slice_range=(0, 1), precision="single")
+    tnb.clear_cache()
+    gc.collect()
+    b = tnb.compute_head_vector(r.tn, r.tree, r.sliced, None, slice_range=(0, 1), precision="single")
+    tnb.clear_cache()
+    assert rel_l2(a.data, b.data) < TOL
