@@ -427,6 +427,67 @@ def run_ours(args):
         reordered["e2e_api_slices_per_s"] = world * args.steps * Sr / (re_ms / 1e3)
         E.clear_cache()
 
+    # ---- optional: batched slices (slice_batch.py): 2^k aligned slices of the
+    # SAME plan per contraction (the k lowest-mask-bit sliced indices
+    # un-sliced), head tree re-ordered for the reduced sliced set
+    batched_slices = None
+    if args.batch_slices > 0:
+        from paper_2103_03074_b200 import slice_batch as SB
+
+        kb = args.batch_slices
+        bp = SB.batched_program(tn, tree, w.sliced, kb, "single", local)
+        steps_b, reduced_b, sc_b = SB.batched_plan(tn, tree, w.sliced, kb)
+        bp.set_timing(2)
+        Bb = 4  # blocks per step
+        # blocks beyond the headline subset, disjoint per rank
+        bb = ((world * total_slices) >> kb) + 1 + rank * (args.warmup + args.steps) * Bb
+        for s_ in range(args.warmup):
+            bp.run_range(bb + s_ * Bb, bb + (s_ + 1) * Bb, "fixed", out=hvec.data_ptr())
+        barrier(dist, local)
+        b_ms = b_gemm_ms = b_gemm_flops = 0.0
+        for s_ in range(args.warmup, args.warmup + args.steps):
+            bp.run_range(bb + s_ * Bb, bb + (s_ + 1) * Bb, "fixed", out=hvec.data_ptr())
+            t = bp.timing()
+            b_ms += t["total_ms"]
+            b_gemm_ms += t["gemm_ms"]
+            b_gemm_flops += t["gemm_flops"]
+        if dist is not None:
+            tt_ = torch.tensor([b_ms], device=dev)
+            dist.all_reduce(tt_, op=dist.ReduceOp.MAX)
+            b_ms = float(tt_.item())
+        from paper_2103_03074_b200.planner import step_mults
+
+        mb, _ = step_mults({n: tn.nodes[n].indices for n in hl}, steps_b, frozenset(reduced_b))
+        sps_b = world * args.steps * Bb * (1 << kb) / (b_ms / 1e3)
+        batched_slices = {"batch_log2": kb, "slices_per_s": sps_b, "max_rank": sc_b,
+                          "executed_flops_per_slice": 8.0 * mb / (1 << kb),
+                          "executed_tflops": sps_b * 8.0 * mb / (1 << kb) / 1e12,
+                          "gemm_tflops": b_gemm_flops / (b_gemm_ms / 1e3) / 1e12 if b_gemm_ms else 0.0,
+                          "speedup_vs_headline": None,
+                          "note": "the reference plan's slices, 2^k aligned slices per contraction "
+                                  "(lowest-mask-bit sliced indices un-sliced, tree re-ordered; "
+                                  "tests/test_gpu_slice_batch.py); executed FLOPs are the batched tree's"}
+        del bp
+        E.clear_cache()
+        # the same through the public API (set_slice_batch; host buffers)
+        tnb.set_slice_batch(kb)
+        try:
+            a0 = (bb + (args.warmup + args.steps) * Bb) << kb
+            tnb.compute_head_vector(tn, tree, w.sliced, None, slice_range=(a0, a0 + (Bb << kb)),
+                                    precision="single", device=local)  # plan + compile
+            barrier(dist, local)
+            e_t0 = time.perf_counter()
+            for s_ in range(args.steps):
+                a = a0 + ((s_ + 1) * Bb << kb)
+                tnb.compute_head_vector(tn, tree, w.sliced, None, slice_range=(a, a + (Bb << kb)),
+                                        precision="single", device=local)
+            barrier(dist, local)
+            be_ms = (time.perf_counter() - e_t0) * 1e3
+        finally:
+            tnb.set_slice_batch(0)
+        batched_slices["e2e_api_slices_per_s"] = world * args.steps * (Bb << kb) / (be_ms / 1e3)
+        E.clear_cache()
+
     # ---- optional: cross-slice reuse (TNB_FLAG_REUSE_SLICES) -- reported beside the
     # headline, NOT as it: it skips re-computing results whose mask bits did not change
     reuse = None
@@ -522,6 +583,7 @@ def run_ours(args):
         "batched_s1": batched,
         "co_optimised_plan": opt_plan,
         "reordered_same_slices": reordered,
+        "batched_slices": batched_slices,
         # linear XEB (analytics.py:46-58) of the synthetic partial amplitudes
         # accumulated over every bench step (the fixed slice subset)
         "xeb_partial_subset": float((2.0 ** 53 / amps_total.numel())
@@ -529,6 +591,8 @@ def run_ours(args):
     }
     if reordered is not None:
         reordered["speedup_vs_headline"] = reordered["slices_per_s"] / value
+    if batched_slices is not None:
+        batched_slices["speedup_vs_headline"] = batched_slices["slices_per_s"] / value
     if opt_plan is not None:
         # time for ALL 2^n_e head slices, reference plan vs co-optimised plan
         ref_log2 = w.n_e - math.log2(value)
@@ -587,6 +651,8 @@ def main():
     ap.add_argument("--reordered", type=int, default=1,
                     help="also time the same slices through the re-ordered tree <workload>_reordered")
     ap.add_argument("--reordered-slices", type=int, default=16)
+    ap.add_argument("--batch-slices", type=int, default=4,
+                    help="also time 2^k-slice blocks per contraction (slice_batch.py; 0 = off)")
     ap.add_argument("--batch-s1", type=int, default=4,
                     help="also time 2^b closed-bit assignments per head pass (reported separately)")
     args = ap.parse_args()

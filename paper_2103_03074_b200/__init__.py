@@ -20,6 +20,7 @@ from .engine import (  # noqa: F401
     set_device,
     set_flags,
     set_reorder,
+    set_slice_batch,
     tail_amplitudes_unchecked,
 )
 from .errors import (  # noqa: F401
