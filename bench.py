@@ -435,8 +435,15 @@ def run_ours(args):
         from paper_2103_03074_b200 import slice_batch as SB
 
         kb = args.batch_slices
+        while True:  # the largest k <= --batch-slices whose intermediates fit rank 32
+            try:
+                steps_b, reduced_b, sc_b = SB.batched_plan(tn, tree, w.sliced, kb)
+                break
+            except tnb.ShapeMismatch:
+                kb -= 1
+                if kb == 0:
+                    raise
         bp = SB.batched_program(tn, tree, w.sliced, kb, "single", local)
-        steps_b, reduced_b, sc_b = SB.batched_plan(tn, tree, w.sliced, kb)
         bp.set_timing(2)
         Bb = 4  # blocks per step
         # blocks beyond the headline subset, disjoint per rank
