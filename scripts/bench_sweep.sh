@@ -21,5 +21,7 @@ for line in open("$OUT"):
     o = d.get("reordered_same_slices") or {}
     print(f"{d['config']['workload'][:40]:40s} n_e? slices/s {d['value']:.3f} TFLOP/s {d['contraction_tflops']:.1f} "
           f"gemm {d['roofline']['achieved']:.0f} reuse {r.get('value', 0):.2f} xeb {d['xeb_partial_subset']:.4g} "
-          f"reordered {o.get('slices_per_s', 0):.2f} ({o.get('executed_tflops', 0):.0f} TFLOP/s executed)")
+          f"reordered {o.get('slices_per_s', 0):.2f} ({o.get('executed_tflops', 0):.0f} TFLOP/s executed) "
+          f"batched k={(d.get('batched_slices') or {}).get('batch_log2')} {(d.get('batched_slices') or {}).get('slices_per_s', 0):.1f} "
+          f"({(d.get('batched_slices') or {}).get('executed_tflops', 0):.0f} TFLOP/s executed)")
 EOF
