@@ -323,12 +323,12 @@ def run_ours(args):
 
     # ---- optional: the co-optimised plan of the same network:
     # same head leaves / cut / head vector, head tree + sliced set from
-    # treeopt.select_slices_b200 (frozen in tests/golden/<workload>_opt_b200,
-    # else <workload>_opt).
+    # treeopt.select_slices_b200 (frozen in tests/golden/<workload>_opt31_b200,
+    # else _opt_b200, else _opt).
     # Reported beside the headline: slices of a different plan are a
     # different unit; the comparable figure is the time for ALL slices.
     opt_plan = None
-    opt_name = next((args.workload + sfx for sfx in ("_opt_b200", "_opt")
+    opt_name = next((args.workload + sfx for sfx in ("_opt31_b200", "_opt_b200", "_opt")
                      if os.path.isdir(os.path.join(ROOT, "tests", "golden", args.workload + sfx))), None)
     if args.opt_plan and opt_name is not None:
         wo = tnb.load_workload(opt_name)

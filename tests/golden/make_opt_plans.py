@@ -35,6 +35,10 @@ PLANS = {
     "c4_opt": ("c4", 30, "mults", {"restarts": 16}),
     # c4_opt's tree + slices, then the B200 polish (time-model subtree DP)
     "c4_opt_b200": ("c4_opt", 30, "b200", {"trials": 0, "keep_top": 0, "slice_repeats": 1}, "c4"),
+    # space target 2^31 (the executor runs rank-32 intermediates; C4 at 2^31:
+    # fewer, bigger slices), then the B200 polish
+    "c4_opt31": ("c4", 31, "mults", {"restarts": 16}),
+    "c4_opt31_b200": ("c4_opt31", 31, "b200", {"trials": 0, "keep_top": 0, "slice_repeats": 1}, "c4"),
     # the reference plan's OWN sliced set (same slices, same partial head
     # vectors), head tree re-ordered: exact DP, then the B200 polish
     "c4_reordered": ("c4", 30, "b200", {"keep_slices": True}),

@@ -36,7 +36,7 @@ def test_c1_opt_full_sum_equals_reference_plan_and_statevector(gpu, workloads, p
 
 
 @pytest.mark.parametrize("name,rng_", [("s8_opt", (0, 4)), ("s8_opt", (0, 1)), ("c4_opt", (0, 1)),
-                                       ("c4_opt_b200", (0, 1))])
+                                       ("c4_opt_b200", (0, 1)), ("c4_opt31_b200", (0, 1))])
 def test_opt_plan_head_tail_xeb_vs_reference(gpu, workloads, name, rng_):
     w, g = workloads(name), golden(name)
     a, b = rng_
