@@ -365,6 +365,35 @@ def run_ours(args):
                             "pins its results to the reference engine run on that plan)"}
         del op
         E.clear_cache()
+        # the co-optimised plan's slices in 2^k blocks (slice_batch.py, rank <= 32)
+        from paper_2103_03074_b200 import slice_batch as SB
+
+        for ko in (3, 2, 1):
+            try:
+                SB.batched_plan(wo.tn, wo.tree, wo.sliced, ko, max_rank=32)
+                break
+            except (tnb.ShapeMismatch, tnb.TncutError, ValueError):
+                ko = 0
+        if ko:
+            bo = SB.batched_program(wo.tn, wo.tree, wo.sliced, ko, "single", local, max_rank=32)
+            bo.set_timing(2)
+            ob2 = (1 << (wo.n_e - ko)) // 2 + rank * (args.warmup + args.steps)
+            for s_ in range(args.warmup):
+                bo.run_range(ob2 + s_, ob2 + s_ + 1, "fixed", out=hvec.data_ptr())
+            barrier(dist, local)
+            bo_ms = 0.0
+            for s_ in range(args.warmup, args.warmup + args.steps):
+                bo.run_range(ob2 + s_, ob2 + s_ + 1, "fixed", out=hvec.data_ptr())
+                bo_ms += bo.timing()["total_ms"]
+            if dist is not None:
+                tt_ = torch.tensor([bo_ms], device=dev)
+                dist.all_reduce(tt_, op=dist.ReduceOp.MAX)
+                bo_ms = float(tt_.item())
+            bsps = world * args.steps * (1 << ko) / (bo_ms / 1e3)
+            opt_plan["batched"] = {"batch_log2": ko, "slices_per_s": bsps,
+                                   "all_slices_head_s_log2": wo.n_e - math.log2(bsps)}
+            del bo
+            E.clear_cache()
 
     # ---- optional: the SAME slices (reference sliced set, same masks, same
     # partial head vectors) through a re-ordered head tree
@@ -605,6 +634,8 @@ def run_ours(args):
         ref_log2 = w.n_e - math.log2(value)
         opt_plan["reference_plan_all_slices_head_s_log2"] = ref_log2
         opt_plan["all_slices_speedup_log2"] = ref_log2 - opt_plan["all_slices_head_s_log2"]
+        if opt_plan.get("batched"):
+            opt_plan["batched"]["all_slices_speedup_log2"] = ref_log2 - opt_plan["batched"]["all_slices_head_s_log2"]
     if world == 1 and not args.no_cpu:
         line["cpu_baseline"] = cpu_baseline(w)
     print(json.dumps(line), flush=True)

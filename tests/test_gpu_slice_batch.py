@@ -71,3 +71,17 @@ def test_public_api_opt_in(gpu, workloads):
     assert st.head_contractions == 16 and st.multiplications == 16 * w.tc_per_slice
     assert odd.slice_range == (16, 18)
     tnb.clear_cache()
+
+
+def test_co_optimised_plan_blocks_match_per_slice(gpu, workloads):
+    """Batching on top of the co-optimised plan (rank-32 intermediates)."""
+    import gc
+
+    w = workloads("c4_opt31_b200")
+    hv = batched(w.tn, w.tree, w.sliced, None, slice_range=(0, 4), batch_log2=2, max_rank=32)
+    tnb.clear_cache()
+    gc.collect()
+    ref = tnb.compute_head_vector(w.tn, w.tree, w.sliced, None, slice_range=(0, 4),
+                                  precision="single")
+    tnb.clear_cache()
+    assert rel_l2(hv.data, ref.data) < TOL
