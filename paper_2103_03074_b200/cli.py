@@ -20,16 +20,36 @@ ANALYTICS_NAMES = ("xeb", "histogram", "postselect_curve", "mixed_xeb", "margina
                    "ks_to_porter_thomas")
 
 
-def bind() -> dict:
+def b200_select_slices(tn, tree, target_space, reconfigure=True, leaf_limit=60):
+    """``select_slices`` (slicing.py:76-82 signature) backed by the plan
+    co-optimiser: head tree + sliced set searched jointly for total head
+    work, then the B200 time-model polish (treeopt.py).  ``reconfigure`` /
+    ``leaf_limit`` tune the reference's own greedy rebuild and have no
+    counterpart here."""
+    from .treeopt import select_slices_b200
+
+    return select_slices_b200(tn, tree, target_space, objective="b200")
+
+
+def bind(slicer: bool | None = None) -> dict:
     """Rebind the engine/analytics names inside the reference's cli and
-    pipeline modules (they import them by name) to this package's.
+    pipeline modules (they import them by name) to this package's; with
+    ``slicer`` (default: env TNB_CLI_SLICER=b200) also ``tncut slice``'s
+    ``select_slices`` to the plan co-optimiser.
     Returns {module.name: previous object} so callers can restore."""
+    import os
+
     import tncut.cli as cli
     import tncut.pipeline as pipeline
 
     from . import analytics, engine
 
     previous = {}
+    if slicer is None:
+        slicer = os.environ.get("TNB_CLI_SLICER", "") == "b200"
+    if slicer:
+        previous["tncut.cli.select_slices"] = cli.select_slices
+        cli.select_slices = b200_select_slices
     for mod in (cli, pipeline):
         for name in ENGINE_NAMES:
             if hasattr(mod, name):
@@ -53,11 +73,13 @@ def unbind(previous: dict) -> None:
 def main(argv=None) -> int:
     import tncut.cli as cli
 
-    bind()
+    previous = bind()
     try:
         cli.main(args=list(sys.argv[1:] if argv is None else argv), standalone_mode=True)
     except SystemExit as exc:  # click exits with the reference's exit codes
         return int(exc.code or 0)
+    finally:
+        unbind(previous)
     return 0
 
 

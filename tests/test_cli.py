@@ -94,3 +94,31 @@ def test_tncut_run_and_reduce_on_the_executor(gpu, tmp_path):
         got = table(red)
         a = np.array([got[k] for k in ref]); b = np.array([ref[k] for k in ref])
         assert np.linalg.norm(a - b) / np.linalg.norm(b) < 1e-10
+
+
+def test_tncut_slice_with_the_co_optimiser(tmp_path, monkeypatch):
+    """`tncut slice` (cli.py:253-303) with select_slices rebound to the plan
+    co-optimiser (TNB_CLI_SLICER=b200): a valid reference order document
+    whose total head work is below the reference slicer's (CPU only)."""
+    _tncut()
+    import json
+    import math
+
+    import tncut.cli as cli
+
+    from paper_2103_03074_b200 import cli as ours
+
+    circ = os.path.join(GOLDEN, "s8", "circuit.qsim")
+    order = os.path.join(GOLDEN, "s8", "order.json")
+    out_ref, out_b200 = str(tmp_path / "ref.json"), str(tmp_path / "b200.json")
+    args = ["slice", circ, order, "--target-space", "18", "-o"]
+    with pytest.raises(SystemExit) as e:
+        cli.main(args=args + [out_ref], standalone_mode=True)
+    assert e.value.code in (0, None)
+    monkeypatch.setenv("TNB_CLI_SLICER", "b200")
+    assert ours.main(args + [out_b200]) == 0
+    assert cli.select_slices is not ours.b200_select_slices  # unbound again
+    ref, b200 = json.load(open(out_ref)), json.load(open(out_b200))
+    tot = lambda d: math.log2(d["subtask"]["tc"]) + d["subtask"]["n_e"]  # noqa: E731
+    assert b200["subtask"]["sc_log2"] <= 18
+    assert tot(b200) < tot(ref)
