@@ -229,8 +229,14 @@ def select_slices_b200(tn, tree, target_space: int, *, objective: str = "mults",
         if stats is not None:
             stats.update(best[1], restarts=restarts)
         return best[0]
+    if keep_slices and not initial_slices:
+        raise ValueError("keep_slices needs initial_slices (the sliced set to keep)")
     hp = head_problem(tn, tree)
     dense = {ix: k for k, ix in enumerate(hp.index_ids)}
+    unknown = [ix for ix in (initial_slices or []) if ix not in dense]
+    if unknown:
+        from .errors import ShapeMismatch
+        raise ShapeMismatch(f"sliced indices {unknown[:4]} are not head indices")
     init_sl = np.asarray([dense[ix] for ix in (initial_slices or [])], np.int32)
     opt = Options()
     lib = load()

@@ -177,3 +177,18 @@ def test_reference_accepts_the_plan(workloads):
         tree = tord.doc_to_tree(json.load(fh))
     assert tree.first_cut == len(tree.steps) - 1
     assert [(s.lhs, s.rhs, s.out) for s in tree.steps] == [(s.lhs, s.rhs, s.out) for s in w.tree.steps]
+
+
+def test_keep_slices_argument_checks(workloads, lib):
+    from paper_2103_03074_b200.errors import ShapeMismatch
+
+    w = workloads("s8")
+    with pytest.raises(ValueError):
+        treeopt.select_slices_b200(w.tn, w.tree, w.target_space, keep_slices=True)
+    with pytest.raises(ShapeMismatch):
+        treeopt.select_slices_b200(w.tn, w.tree, w.target_space, keep_slices=True,
+                                   initial_slices=[10 ** 9])
+    plan, tree = treeopt.select_slices_b200(w.tn, w.tree, w.target_space, keep_slices=True,
+                                            initial_slices=w.sliced)
+    assert plan.sliced_indices == w.sliced
+    assert plan.per_subtask.tc <= w.tc_per_slice
