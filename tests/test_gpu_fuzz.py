@@ -126,3 +126,28 @@ def test_random_networks_exercise_fusion(gpu, monkeypatch):
         total_fused += prog.info.n_steps_fused
         del prog
     assert total_fused >= 5, total_fused
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("seed", range(8))
+def test_random_networks_slice_blocks(gpu, seed, monkeypatch):
+    """Batched slices at program level (slice_batch.py's principle): the plan
+    with the LAST k sliced indices un-sliced, mask j, equals the full plan's
+    masks [j*2^k, (j+1)*2^k) summed (engine.py:276-279 mask convention)."""
+    from paper_2103_03074_b200.engine import Program
+
+    rng = np.random.default_rng(1000 + seed)
+    for _ in range(50):
+        leaves, steps, sliced, opens = _random_network(rng)
+        if len(sliced) >= 2:
+            break
+    else:
+        pytest.skip("no network with two sliced bonds")
+    monkeypatch.setenv("TNB_TC_MIN_RANK", "14")
+    full = Program(leaves, steps, sliced, opens, "single", 0, 0)
+    k = 1
+    blk = Program(leaves, steps, sliced[: len(sliced) - k], opens, "single", 0, 0)
+    for j in range(1 << (len(sliced) - k)):
+        want = full.run_range(j << k, (j + 1) << k, "fixed")
+        got = blk.run_range(j, j + 1, "fixed")
+        assert rel_l2(got, want) < 1e-5, (j, rel_l2(got, want))
