@@ -152,6 +152,24 @@ def cpu_baseline(w):
             "sample": sample, "est_s_per_slice": est, "tflops": flops / est / 1e12}
 
 
+def _run_leg(name, fn):
+    """An optional bench leg: its failure (e.g. device memory on another box)
+    is reported in the JSON line instead of losing the headline."""
+    try:
+        if os.environ.get("TNB_BENCH_FAIL_LEG") == name:  # test hook
+            raise RuntimeError("injected failure")
+        return fn()
+    except Exception as exc:  # noqa: BLE001
+        print(f"[bench] leg {name} failed: {exc!r}", file=sys.stderr, flush=True)
+        try:
+            from paper_2103_03074_b200 import engine as _E
+
+            _E.clear_cache()
+        except Exception:  # noqa: BLE001
+            pass
+        return {"unavailable": f"{type(exc).__name__}: {str(exc)[:200]}"}
+
+
 def run_ours(args):
     import torch
 
@@ -289,37 +307,41 @@ def run_ours(args):
     # ---- optional: batched closed-bit assignments --
     # 2^b s1 values in one head pass over the same slices; reported beside
     # the headline as assignment-slices/s (a bigger correlated batch)
-    batched = None
-    if args.batch_s1 > 0:
-        from paper_2103_03074_b200.batched import cheapest_batch_qubits, compute_head_vectors_batched
+    def _leg_batched():
+        batched = None
+        if args.batch_s1 > 0:
+            from paper_2103_03074_b200.batched import cheapest_batch_qubits, compute_head_vectors_batched
 
-        qs, ratio = cheapest_batch_qubits(tn, tree, w.sliced, args.batch_s1)
-        closed = sorted(tn.fixed_output_bits)
-        s1_list = []
-        for v in range(1 << len(qs)):
-            s = dict(tn.fixed_output_bits)
-            for i, q in enumerate(qs):
-                s[q] = (v >> (len(qs) - 1 - i)) & 1
-            s1_list.append("".join(str(s[q]) for q in closed))
-        a = base
-        compute_head_vectors_batched(tn, tree, w.sliced, s1_list, slice_range=(a, a + S),
-                                     precision="single", device=local)  # compile + warm
-        barrier(dist, local)
-        b_t0 = time.perf_counter()
-        for s_ in range(args.steps):
-            a = base + s_ * S
+            qs, ratio = cheapest_batch_qubits(tn, tree, w.sliced, args.batch_s1)
+            closed = sorted(tn.fixed_output_bits)
+            s1_list = []
+            for v in range(1 << len(qs)):
+                s = dict(tn.fixed_output_bits)
+                for i, q in enumerate(qs):
+                    s[q] = (v >> (len(qs) - 1 - i)) & 1
+                s1_list.append("".join(str(s[q]) for q in closed))
+            a = base
             compute_head_vectors_batched(tn, tree, w.sliced, s1_list, slice_range=(a, a + S),
-                                         precision="single", device=local)
-        barrier(dist, local)
-        b_ms = (time.perf_counter() - b_t0) * 1e3 / args.steps
-        batched = {"assignments": len(s1_list), "qubits": qs, "analytic_cost_ratio": ratio,
-                   "ms_per_step": b_ms,
-                   "assignment_slices_per_s": world * S * len(s1_list) / (b_ms / 1e3),
-                   "bitstrings_per_pass": len(s1_list) << len(tn.open_output_indices),
-                   "note": "head vectors of 2^b closed-bit assignments from one contraction with "
-                           "those qubits' output legs open (paper_2103_03074_b200.batched; equal to "
-                           "per-s1 runs, tests/test_batched.py); wall time incl. host copies"}
-        E.clear_cache()
+                                         precision="single", device=local)  # compile + warm
+            barrier(dist, local)
+            b_t0 = time.perf_counter()
+            for s_ in range(args.steps):
+                a = base + s_ * S
+                compute_head_vectors_batched(tn, tree, w.sliced, s1_list, slice_range=(a, a + S),
+                                             precision="single", device=local)
+            barrier(dist, local)
+            b_ms = (time.perf_counter() - b_t0) * 1e3 / args.steps
+            batched = {"assignments": len(s1_list), "qubits": qs, "analytic_cost_ratio": ratio,
+                       "ms_per_step": b_ms,
+                       "assignment_slices_per_s": world * S * len(s1_list) / (b_ms / 1e3),
+                       "bitstrings_per_pass": len(s1_list) << len(tn.open_output_indices),
+                       "note": "head vectors of 2^b closed-bit assignments from one contraction with "
+                               "those qubits' output legs open (paper_2103_03074_b200.batched; equal to "
+                               "per-s1 runs, tests/test_batched.py); wall time incl. host copies"}
+            E.clear_cache()
+        return batched
+
+    batched = _run_leg("batched", _leg_batched)
 
     # ---- optional: the co-optimised plan of the same network:
     # same head leaves / cut / head vector, head tree + sliced set from
@@ -327,202 +349,214 @@ def run_ours(args):
     # else _opt_b200, else _opt).
     # Reported beside the headline: slices of a different plan are a
     # different unit; the comparable figure is the time for ALL slices.
-    opt_plan = None
-    opt_name = next((args.workload + sfx for sfx in ("_opt31_b200", "_opt_b200", "_opt")
-                     if os.path.isdir(os.path.join(ROOT, "tests", "golden", args.workload + sfx))), None)
-    if args.opt_plan and opt_name is not None:
-        wo = tnb.load_workload(opt_name)
-        op = E.head_program(wo.tn, wo.tree, wo.sliced, "single", device=local)
-        op.set_timing(2)
-        So = args.opt_slices
-        ob = rank * (args.warmup + args.steps) * So
-        for s_ in range(args.warmup):
-            op.run_range(ob + s_ * So, ob + (s_ + 1) * So, "fixed", out=hvec.data_ptr())
-        barrier(dist, local)
-        o_ms = o_gemm_ms = o_gemm_flops = 0.0
-        o_launches = 0
-        for s_ in range(args.warmup, args.warmup + args.steps):
-            op.run_range(ob + s_ * So, ob + (s_ + 1) * So, "fixed", out=hvec.data_ptr())
-            t = op.timing()
-            o_ms += t["total_ms"]
-            o_gemm_ms += t["gemm_ms"]
-            o_gemm_flops += t["gemm_flops"]
-            o_launches += t["launches"]
-        if dist is not None:
-            tt_ = torch.tensor([o_ms], device=dev)
-            dist.all_reduce(tt_, op=dist.ReduceOp.MAX)
-            o_ms = float(tt_.item())
-        sps = world * args.steps * So / (o_ms / 1e3)
-        opt_plan = {"workload": opt_name, "n_e": wo.n_e,
-                    "target_space": wo.target_space, "flops_per_slice": 8.0 * wo.tc_per_slice,
-                    "slices_per_s": sps, "contraction_tflops": sps * 8.0 * wo.tc_per_slice / 1e12,
-                    "gemm_tflops": o_gemm_flops / (o_gemm_ms / 1e3) / 1e12 if o_gemm_ms else 0.0,
-                    "slices_per_step_per_gpu": So, "launches_per_step": o_launches / args.steps,
-                    "all_slices_head_s_log2": wo.n_e - math.log2(sps),
-                    "planner": wo.doc.get("planner", {}).get("tool"),
-                    "note": "device time of the co-optimised plan's head slices (same network, head "
-                            "leaves, cut and head vector as the reference plan; tests/test_gpu_treeopt.py "
-                            "pins its results to the reference engine run on that plan)"}
-        del op
-        E.clear_cache()
-        # the co-optimised plan's slices in 2^k blocks (slice_batch.py, rank <= 32)
-        from paper_2103_03074_b200 import slice_batch as SB
-
-        for ko in (3, 2, 1):
-            try:
-                SB.batched_plan(wo.tn, wo.tree, wo.sliced, ko, max_rank=32)
-                break
-            except (tnb.ShapeMismatch, tnb.TncutError, ValueError):
-                ko = 0
-        if ko:
-            bo = SB.batched_program(wo.tn, wo.tree, wo.sliced, ko, "single", local, max_rank=32)
-            bo.set_timing(2)
-            ob2 = (1 << (wo.n_e - ko)) // 2 + rank * (args.warmup + args.steps)
+    def _leg_opt_plan():
+        opt_plan = None
+        opt_name = next((args.workload + sfx for sfx in ("_opt31_b200", "_opt_b200", "_opt")
+                         if os.path.isdir(os.path.join(ROOT, "tests", "golden", args.workload + sfx))), None)
+        if args.opt_plan and opt_name is not None:
+            wo = tnb.load_workload(opt_name)
+            op = E.head_program(wo.tn, wo.tree, wo.sliced, "single", device=local)
+            op.set_timing(2)
+            So = args.opt_slices
+            ob = rank * (args.warmup + args.steps) * So
             for s_ in range(args.warmup):
-                bo.run_range(ob2 + s_, ob2 + s_ + 1, "fixed", out=hvec.data_ptr())
+                op.run_range(ob + s_ * So, ob + (s_ + 1) * So, "fixed", out=hvec.data_ptr())
             barrier(dist, local)
-            bo_ms = 0.0
+            o_ms = o_gemm_ms = o_gemm_flops = 0.0
+            o_launches = 0
             for s_ in range(args.warmup, args.warmup + args.steps):
-                bo.run_range(ob2 + s_, ob2 + s_ + 1, "fixed", out=hvec.data_ptr())
-                bo_ms += bo.timing()["total_ms"]
+                op.run_range(ob + s_ * So, ob + (s_ + 1) * So, "fixed", out=hvec.data_ptr())
+                t = op.timing()
+                o_ms += t["total_ms"]
+                o_gemm_ms += t["gemm_ms"]
+                o_gemm_flops += t["gemm_flops"]
+                o_launches += t["launches"]
             if dist is not None:
-                tt_ = torch.tensor([bo_ms], device=dev)
+                tt_ = torch.tensor([o_ms], device=dev)
                 dist.all_reduce(tt_, op=dist.ReduceOp.MAX)
-                bo_ms = float(tt_.item())
-            bsps = world * args.steps * (1 << ko) / (bo_ms / 1e3)
-            opt_plan["batched"] = {"batch_log2": ko, "slices_per_s": bsps,
-                                   "all_slices_head_s_log2": wo.n_e - math.log2(bsps)}
-            del bo
+                o_ms = float(tt_.item())
+            sps = world * args.steps * So / (o_ms / 1e3)
+            opt_plan = {"workload": opt_name, "n_e": wo.n_e,
+                        "target_space": wo.target_space, "flops_per_slice": 8.0 * wo.tc_per_slice,
+                        "slices_per_s": sps, "contraction_tflops": sps * 8.0 * wo.tc_per_slice / 1e12,
+                        "gemm_tflops": o_gemm_flops / (o_gemm_ms / 1e3) / 1e12 if o_gemm_ms else 0.0,
+                        "slices_per_step_per_gpu": So, "launches_per_step": o_launches / args.steps,
+                        "all_slices_head_s_log2": wo.n_e - math.log2(sps),
+                        "planner": wo.doc.get("planner", {}).get("tool"),
+                        "note": "device time of the co-optimised plan's head slices (same network, head "
+                                "leaves, cut and head vector as the reference plan; tests/test_gpu_treeopt.py "
+                                "pins its results to the reference engine run on that plan)"}
+            del op
             E.clear_cache()
+            # the co-optimised plan's slices in 2^k blocks (slice_batch.py, rank <= 32)
+            from paper_2103_03074_b200 import slice_batch as SB
+
+            for ko in (3, 2, 1):
+                try:
+                    SB.batched_plan(wo.tn, wo.tree, wo.sliced, ko, max_rank=32)
+                    break
+                except (tnb.ShapeMismatch, tnb.TncutError, ValueError):
+                    ko = 0
+            if ko:
+                bo = SB.batched_program(wo.tn, wo.tree, wo.sliced, ko, "single", local, max_rank=32)
+                bo.set_timing(2)
+                ob2 = (1 << (wo.n_e - ko)) // 2 + rank * (args.warmup + args.steps)
+                for s_ in range(args.warmup):
+                    bo.run_range(ob2 + s_, ob2 + s_ + 1, "fixed", out=hvec.data_ptr())
+                barrier(dist, local)
+                bo_ms = 0.0
+                for s_ in range(args.warmup, args.warmup + args.steps):
+                    bo.run_range(ob2 + s_, ob2 + s_ + 1, "fixed", out=hvec.data_ptr())
+                    bo_ms += bo.timing()["total_ms"]
+                if dist is not None:
+                    tt_ = torch.tensor([bo_ms], device=dev)
+                    dist.all_reduce(tt_, op=dist.ReduceOp.MAX)
+                    bo_ms = float(tt_.item())
+                bsps = world * args.steps * (1 << ko) / (bo_ms / 1e3)
+                opt_plan["batched"] = {"batch_log2": ko, "slices_per_s": bsps,
+                                       "all_slices_head_s_log2": wo.n_e - math.log2(bsps)}
+                del bo
+                E.clear_cache()
+        return opt_plan
+
+    opt_plan = _run_leg("opt_plan", _leg_opt_plan)
 
     # ---- optional: the SAME slices (reference sliced set, same masks, same
     # partial head vectors) through a re-ordered head tree
     # (treeopt keep_slices; tests/golden/<workload>_reordered).  Reported
     # beside the headline, which executes the reference tree as given.
-    reordered = None
-    ro_name = args.workload + "_reordered"
-    if args.reordered and os.path.isdir(os.path.join(ROOT, "tests", "golden", ro_name)):
-        wr = tnb.load_workload(ro_name)
-        assert wr.sliced == w.sliced
-        rp = E.head_program(wr.tn, wr.tree, wr.sliced, "single", device=local)
-        rp.set_timing(2)
-        Sr = args.reordered_slices
-        rb = rank * (args.warmup + args.steps) * Sr
-        for s_ in range(args.warmup):
-            rp.run_range(rb + s_ * Sr, rb + (s_ + 1) * Sr, "fixed", out=hvec.data_ptr())
-        barrier(dist, local)
-        r_ms = r_gemm_ms = r_gemm_flops = 0.0
-        r_launches = 0
-        for s_ in range(args.warmup, args.warmup + args.steps):
-            rp.run_range(rb + s_ * Sr, rb + (s_ + 1) * Sr, "fixed", out=hvec.data_ptr())
-            t = rp.timing()
-            r_ms += t["total_ms"]
-            r_gemm_ms += t["gemm_ms"]
-            r_gemm_flops += t["gemm_flops"]
-            r_launches += t["launches"]
-        if dist is not None:
-            tt_ = torch.tensor([r_ms], device=dev)
-            dist.all_reduce(tt_, op=dist.ReduceOp.MAX)
-            r_ms = float(tt_.item())
-        rsps = world * args.steps * Sr / (r_ms / 1e3)
-        reordered = {"workload": ro_name, "slices_per_s": rsps,
-                     "executed_flops_per_slice": 8.0 * wr.tc_per_slice,
-                     "executed_tflops": rsps * 8.0 * wr.tc_per_slice / 1e12,
-                     "gemm_tflops": r_gemm_flops / (r_gemm_ms / 1e3) / 1e12 if r_gemm_ms else 0.0,
-                     "slices_per_step_per_gpu": Sr, "launches_per_step": r_launches / args.steps,
-                     "note": "the reference plan's own slices (same sliced set and masks, same partial "
-                             "head vectors: tests/test_gpu_treeopt.py) with the head tree re-ordered by "
-                             "treeopt (keep_slices, exact subtree DP + B200 polish); executed FLOPs "
-                             "are the re-ordered tree's"}
-        del rp
-        E.clear_cache()
-        # the same through the public API (set_reorder; host buffers, leaves
-        # H2D and the head vector D2H every call)
-        tnb.set_reorder(True)
-        try:
-            a0 = base + total_slices  # slices beyond the headline subset
-            tnb.compute_head_vector(tn, tree, w.sliced, None, slice_range=(a0, a0 + Sr),
-                                    precision="single", device=local)  # plan + compile
+    def _leg_reordered():
+        reordered = None
+        ro_name = args.workload + "_reordered"
+        if args.reordered and os.path.isdir(os.path.join(ROOT, "tests", "golden", ro_name)):
+            wr = tnb.load_workload(ro_name)
+            assert wr.sliced == w.sliced
+            rp = E.head_program(wr.tn, wr.tree, wr.sliced, "single", device=local)
+            rp.set_timing(2)
+            Sr = args.reordered_slices
+            rb = rank * (args.warmup + args.steps) * Sr
+            for s_ in range(args.warmup):
+                rp.run_range(rb + s_ * Sr, rb + (s_ + 1) * Sr, "fixed", out=hvec.data_ptr())
             barrier(dist, local)
-            e_t0 = time.perf_counter()
-            for s_ in range(args.steps):
-                a = a0 + (s_ + 1) * Sr
-                hv = tnb.compute_head_vector(tn, tree, w.sliced, None, slice_range=(a, a + Sr),
-                                             precision="single", device=local)
-            barrier(dist, local)
-            re_ms = (time.perf_counter() - e_t0) * 1e3
-        finally:
-            tnb.set_reorder(False)
-        reordered["e2e_api_slices_per_s"] = world * args.steps * Sr / (re_ms / 1e3)
-        E.clear_cache()
+            r_ms = r_gemm_ms = r_gemm_flops = 0.0
+            r_launches = 0
+            for s_ in range(args.warmup, args.warmup + args.steps):
+                rp.run_range(rb + s_ * Sr, rb + (s_ + 1) * Sr, "fixed", out=hvec.data_ptr())
+                t = rp.timing()
+                r_ms += t["total_ms"]
+                r_gemm_ms += t["gemm_ms"]
+                r_gemm_flops += t["gemm_flops"]
+                r_launches += t["launches"]
+            if dist is not None:
+                tt_ = torch.tensor([r_ms], device=dev)
+                dist.all_reduce(tt_, op=dist.ReduceOp.MAX)
+                r_ms = float(tt_.item())
+            rsps = world * args.steps * Sr / (r_ms / 1e3)
+            reordered = {"workload": ro_name, "slices_per_s": rsps,
+                         "executed_flops_per_slice": 8.0 * wr.tc_per_slice,
+                         "executed_tflops": rsps * 8.0 * wr.tc_per_slice / 1e12,
+                         "gemm_tflops": r_gemm_flops / (r_gemm_ms / 1e3) / 1e12 if r_gemm_ms else 0.0,
+                         "slices_per_step_per_gpu": Sr, "launches_per_step": r_launches / args.steps,
+                         "note": "the reference plan's own slices (same sliced set and masks, same partial "
+                                 "head vectors: tests/test_gpu_treeopt.py) with the head tree re-ordered by "
+                                 "treeopt (keep_slices, exact subtree DP + B200 polish); executed FLOPs "
+                                 "are the re-ordered tree's"}
+            del rp
+            E.clear_cache()
+            # the same through the public API (set_reorder; host buffers, leaves
+            # H2D and the head vector D2H every call)
+            tnb.set_reorder(True)
+            try:
+                a0 = base + total_slices  # slices beyond the headline subset
+                tnb.compute_head_vector(tn, tree, w.sliced, None, slice_range=(a0, a0 + Sr),
+                                        precision="single", device=local)  # plan + compile
+                barrier(dist, local)
+                e_t0 = time.perf_counter()
+                for s_ in range(args.steps):
+                    a = a0 + (s_ + 1) * Sr
+                    hv = tnb.compute_head_vector(tn, tree, w.sliced, None, slice_range=(a, a + Sr),
+                                                 precision="single", device=local)
+                barrier(dist, local)
+                re_ms = (time.perf_counter() - e_t0) * 1e3
+            finally:
+                tnb.set_reorder(False)
+            reordered["e2e_api_slices_per_s"] = world * args.steps * Sr / (re_ms / 1e3)
+            E.clear_cache()
+        return reordered
+
+    reordered = _run_leg("reordered", _leg_reordered)
 
     # ---- optional: batched slices (slice_batch.py): 2^k aligned slices of the
     # SAME plan per contraction (the k lowest-mask-bit sliced indices
     # un-sliced), head tree re-ordered for the reduced sliced set
-    batched_slices = None
-    if args.batch_slices > 0:
-        from paper_2103_03074_b200 import slice_batch as SB
+    def _leg_batched_slices():
+        batched_slices = None
+        if args.batch_slices > 0:
+            from paper_2103_03074_b200 import slice_batch as SB
 
-        kb = args.batch_slices
-        while True:  # the largest k <= --batch-slices whose intermediates fit rank 32
+            kb = args.batch_slices
+            while True:  # the largest k <= --batch-slices whose intermediates fit rank 32
+                try:
+                    steps_b, reduced_b, sc_b = SB.batched_plan(tn, tree, w.sliced, kb)
+                    break
+                except tnb.ShapeMismatch:
+                    kb -= 1
+                    if kb == 0:
+                        raise
+            bp = SB.batched_program(tn, tree, w.sliced, kb, "single", local)
+            bp.set_timing(2)
+            Bb = 4  # blocks per step
+            # blocks beyond the headline subset, disjoint per rank
+            bb = ((world * total_slices) >> kb) + 1 + rank * (args.warmup + args.steps) * Bb
+            for s_ in range(args.warmup):
+                bp.run_range(bb + s_ * Bb, bb + (s_ + 1) * Bb, "fixed", out=hvec.data_ptr())
+            barrier(dist, local)
+            b_ms = b_gemm_ms = b_gemm_flops = 0.0
+            for s_ in range(args.warmup, args.warmup + args.steps):
+                bp.run_range(bb + s_ * Bb, bb + (s_ + 1) * Bb, "fixed", out=hvec.data_ptr())
+                t = bp.timing()
+                b_ms += t["total_ms"]
+                b_gemm_ms += t["gemm_ms"]
+                b_gemm_flops += t["gemm_flops"]
+            if dist is not None:
+                tt_ = torch.tensor([b_ms], device=dev)
+                dist.all_reduce(tt_, op=dist.ReduceOp.MAX)
+                b_ms = float(tt_.item())
+            from paper_2103_03074_b200.planner import step_mults
+
+            mb, _ = step_mults({n: tn.nodes[n].indices for n in hl}, steps_b, frozenset(reduced_b))
+            sps_b = world * args.steps * Bb * (1 << kb) / (b_ms / 1e3)
+            batched_slices = {"batch_log2": kb, "slices_per_s": sps_b, "max_rank": sc_b,
+                              "executed_flops_per_slice": 8.0 * mb / (1 << kb),
+                              "executed_tflops": sps_b * 8.0 * mb / (1 << kb) / 1e12,
+                              "gemm_tflops": b_gemm_flops / (b_gemm_ms / 1e3) / 1e12 if b_gemm_ms else 0.0,
+                              "speedup_vs_headline": None,
+                              "note": "the reference plan's slices, 2^k aligned slices per contraction "
+                                      "(lowest-mask-bit sliced indices un-sliced, tree re-ordered; "
+                                      "tests/test_gpu_slice_batch.py); executed FLOPs are the batched tree's"}
+            del bp
+            E.clear_cache()
+            # the same through the public API (set_slice_batch; host buffers)
+            tnb.set_slice_batch(kb)
             try:
-                steps_b, reduced_b, sc_b = SB.batched_plan(tn, tree, w.sliced, kb)
-                break
-            except tnb.ShapeMismatch:
-                kb -= 1
-                if kb == 0:
-                    raise
-        bp = SB.batched_program(tn, tree, w.sliced, kb, "single", local)
-        bp.set_timing(2)
-        Bb = 4  # blocks per step
-        # blocks beyond the headline subset, disjoint per rank
-        bb = ((world * total_slices) >> kb) + 1 + rank * (args.warmup + args.steps) * Bb
-        for s_ in range(args.warmup):
-            bp.run_range(bb + s_ * Bb, bb + (s_ + 1) * Bb, "fixed", out=hvec.data_ptr())
-        barrier(dist, local)
-        b_ms = b_gemm_ms = b_gemm_flops = 0.0
-        for s_ in range(args.warmup, args.warmup + args.steps):
-            bp.run_range(bb + s_ * Bb, bb + (s_ + 1) * Bb, "fixed", out=hvec.data_ptr())
-            t = bp.timing()
-            b_ms += t["total_ms"]
-            b_gemm_ms += t["gemm_ms"]
-            b_gemm_flops += t["gemm_flops"]
-        if dist is not None:
-            tt_ = torch.tensor([b_ms], device=dev)
-            dist.all_reduce(tt_, op=dist.ReduceOp.MAX)
-            b_ms = float(tt_.item())
-        from paper_2103_03074_b200.planner import step_mults
+                a0 = (bb + (args.warmup + args.steps) * Bb) << kb
+                tnb.compute_head_vector(tn, tree, w.sliced, None, slice_range=(a0, a0 + (Bb << kb)),
+                                        precision="single", device=local)  # plan + compile
+                barrier(dist, local)
+                e_t0 = time.perf_counter()
+                for s_ in range(args.steps):
+                    a = a0 + ((s_ + 1) * Bb << kb)
+                    tnb.compute_head_vector(tn, tree, w.sliced, None, slice_range=(a, a + (Bb << kb)),
+                                            precision="single", device=local)
+                barrier(dist, local)
+                be_ms = (time.perf_counter() - e_t0) * 1e3
+            finally:
+                tnb.set_slice_batch(0)
+            batched_slices["e2e_api_slices_per_s"] = world * args.steps * (Bb << kb) / (be_ms / 1e3)
+            E.clear_cache()
+        return batched_slices
 
-        mb, _ = step_mults({n: tn.nodes[n].indices for n in hl}, steps_b, frozenset(reduced_b))
-        sps_b = world * args.steps * Bb * (1 << kb) / (b_ms / 1e3)
-        batched_slices = {"batch_log2": kb, "slices_per_s": sps_b, "max_rank": sc_b,
-                          "executed_flops_per_slice": 8.0 * mb / (1 << kb),
-                          "executed_tflops": sps_b * 8.0 * mb / (1 << kb) / 1e12,
-                          "gemm_tflops": b_gemm_flops / (b_gemm_ms / 1e3) / 1e12 if b_gemm_ms else 0.0,
-                          "speedup_vs_headline": None,
-                          "note": "the reference plan's slices, 2^k aligned slices per contraction "
-                                  "(lowest-mask-bit sliced indices un-sliced, tree re-ordered; "
-                                  "tests/test_gpu_slice_batch.py); executed FLOPs are the batched tree's"}
-        del bp
-        E.clear_cache()
-        # the same through the public API (set_slice_batch; host buffers)
-        tnb.set_slice_batch(kb)
-        try:
-            a0 = (bb + (args.warmup + args.steps) * Bb) << kb
-            tnb.compute_head_vector(tn, tree, w.sliced, None, slice_range=(a0, a0 + (Bb << kb)),
-                                    precision="single", device=local)  # plan + compile
-            barrier(dist, local)
-            e_t0 = time.perf_counter()
-            for s_ in range(args.steps):
-                a = a0 + ((s_ + 1) * Bb << kb)
-                tnb.compute_head_vector(tn, tree, w.sliced, None, slice_range=(a, a + (Bb << kb)),
-                                        precision="single", device=local)
-            barrier(dist, local)
-            be_ms = (time.perf_counter() - e_t0) * 1e3
-        finally:
-            tnb.set_slice_batch(0)
-        batched_slices["e2e_api_slices_per_s"] = world * args.steps * (Bb << kb) / (be_ms / 1e3)
-        E.clear_cache()
+    batched_slices = _run_leg("batched_slices", _leg_batched_slices)
 
     # ---- optional: cross-slice reuse (TNB_FLAG_REUSE_SLICES) -- reported beside the
     # headline, NOT as it: it skips re-computing results whose mask bits did not change
@@ -630,11 +664,11 @@ def run_ours(args):
         "xeb_partial_subset": float((2.0 ** 53 / amps_total.numel())
                                     * float((amps_total.abs().double() ** 2).sum()) - 1.0),
     }
-    if reordered is not None:
+    if reordered and "unavailable" not in reordered:
         reordered["speedup_vs_headline"] = reordered["slices_per_s"] / value
-    if batched_slices is not None:
+    if batched_slices and "unavailable" not in batched_slices:
         batched_slices["speedup_vs_headline"] = batched_slices["slices_per_s"] / value
-    if opt_plan is not None:
+    if opt_plan and "unavailable" not in opt_plan:
         # time for ALL 2^n_e head slices, reference plan vs co-optimised plan
         ref_log2 = w.n_e - math.log2(value)
         opt_plan["reference_plan_all_slices_head_s_log2"] = ref_log2
