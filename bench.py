@@ -431,7 +431,14 @@ def run_ours(args):
         if args.reordered and os.path.isdir(os.path.join(ROOT, "tests", "golden", ro_name)):
             wr = tnb.load_workload(ro_name)
             assert wr.sliced == w.sliced
-            rp = E.head_program(wr.tn, wr.tree, wr.sliced, "single", device=local)
+            # the re-ordered tree with its small steps clustered, as set_reorder runs it
+            from paper_2103_03074_b200.planner import cluster_small_steps
+
+            _hl, _hs, _, _, _cut = E._split(wr.tn, wr.tree)
+            _steps = cluster_small_steps({n: wr.tn.nodes[n].indices for n in _hl}, _hs,
+                                         frozenset(wr.sliced))
+            rp = E.get_program(E._leaf_entries(wr.tn, _hl), E._steps_tuples(_steps), list(wr.sliced),
+                               sorted(_cut), "single", local)
             rp.set_timing(2)
             Sr = args.reordered_slices
             rb = rank * (args.warmup + args.steps) * Sr

@@ -35,7 +35,7 @@ import numpy as np
 from . import _lib
 from .errors import (ProvenanceMismatch, RangeGap, RangeOutOfBounds, RangeOverlap,
                      ShapeMismatch)
-from .planner import greedy_steps, split, step_mults
+from .planner import cluster_small_steps, greedy_steps, split, step_mults
 from .provenance import circuit_sha, normalize_s1, order_sha256, provenance_hash
 from .types import AmplitudeTable, EngineStats, HeadVector
 
@@ -103,6 +103,8 @@ def _exec_head_steps(tn, tree, head_leaves, head_steps, sliced):
         if list(plan.sliced_indices) != list(sliced):
             raise ShapeMismatch("re-ordering changed the sliced set")
         hit = new_tree.head_steps()
+        if os.environ.get("TNB_CLUSTER", "1") != "0":
+            hit = cluster_small_steps(sets, hit, frozenset(sliced))
         _reorder_cache[key] = hit
     return hit
 

@@ -25,10 +25,11 @@ here: ``slice_range`` must be 2^k-aligned).
 from __future__ import annotations
 
 import hashlib
+import os
 
 from . import engine as E
 from .errors import RangeOutOfBounds, ShapeMismatch
-from .planner import step_mults
+from .planner import cluster_small_steps, step_mults
 from .provenance import normalize_s1, provenance_hash
 from .types import HeadVector
 
@@ -44,7 +45,7 @@ def batched_plan(tn, tree, sliced_indices, k: int, reorder: bool = True, max_ran
     reduced = sliced[: len(sliced) - k]
     key = hashlib.sha256(repr((tuple((n, tuple(tn.nodes[n].indices)) for n in head_leaves),
                                tuple(E._steps_tuples(head_steps)), tuple(sliced), k, reorder,
-                               max_rank)).encode()).hexdigest()
+                               max_rank, os.environ.get("TNB_CLUSTER", "1"))).encode()).hexdigest()
     hit = _plans.get(key)
     if hit is not None:
         return hit
@@ -60,6 +61,8 @@ def batched_plan(tn, tree, sliced_indices, k: int, reorder: bool = True, max_ran
         if list(plan.sliced_indices) != reduced:
             raise ShapeMismatch("re-ordering changed the sliced set")
         steps = new_tree.head_steps()
+    if os.environ.get("TNB_CLUSTER", "1") != "0":
+        steps = cluster_small_steps(sets, steps, frozenset(reduced))
     _, sc = step_mults(sets, steps, frozenset(reduced))
     sc = max([sc] + [len(set(tn.nodes[n].indices) - set(reduced)) for n in head_leaves])
     if sc > 32:
