@@ -84,10 +84,17 @@ def set_slice_batch(k: int) -> None:
     _slice_batch = max(0, int(k))
 
 
+_cluster_all = os.environ.get("TNB_CLUSTER_ALL", "0") == "1"
+
+
 def _exec_head_steps(tn, tree, head_leaves, head_steps, sliced):
-    """The head steps the program runs: the caller's, or (set_reorder) the
+    """The head steps the program runs: the caller's (optionally with their
+    tiny steps clustered into waves, TNB_CLUSTER_ALL=1), or (set_reorder) the
     re-ordered ones, never above the caller's largest intermediate."""
     if not _reorder or not head_steps or tree.first_cut is None:
+        if _cluster_all and head_steps:
+            sets = {n: tn.nodes[n].indices for n in head_leaves}
+            return cluster_small_steps(sets, head_steps, frozenset(sliced))
         return head_steps
     key = hashlib.sha256(repr((tuple((n, tuple(tn.nodes[n].indices)) for n in head_leaves),
                                tuple(_steps_tuples(head_steps)), tuple(sliced))).encode()).hexdigest()
@@ -340,7 +347,8 @@ def _leaf_entries(tn, leaf_ids):
 def head_program(tn, tree, sliced_indices, precision="single", device=None, flags=None):
     """The compiled head program (for benchmarks / timing introspection)."""
     head_leaves, head_steps, _, _, cut = _split(tn, tree)
-    return get_program(_leaf_entries(tn, head_leaves), _steps_tuples(head_steps),
+    run_steps = _exec_head_steps(tn, tree, head_leaves, head_steps, list(sliced_indices))
+    return get_program(_leaf_entries(tn, head_leaves), _steps_tuples(run_steps),
                        list(sliced_indices), sorted(cut), precision, device, flags)
 
 
