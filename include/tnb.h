@@ -191,6 +191,22 @@ int tnb_prob_prefix_sums(int32_t device, const double* probs, int64_t n, const i
 int tnb_prob_ks(int32_t device, const double* probs_sorted_asc, int64_t n, double scale,
                 double* out_host);
 
+/* ---- The multi-GPU path's one collective: a sum over ranks of
+   the amplitude (or head-vector) partials of disjoint slice ranges, over
+   NCCL (libnccl.so.2 is dlopen'd on first use; no link-time dependency).
+   One communicator per process/device; `stream` NULL = the legacy stream.
+   Reference interface replaced: the reference has no collective -- partial
+   head vectors travel as TNCUTHV1 files and are summed by reduce_partials
+   (engine.py:398-452, cli.py:417-441). */
+int tnb_nccl_unique_id(uint8_t id_out[128]);
+int tnb_nccl_comm_create(int32_t nranks, const uint8_t id[128], int32_t rank, int32_t device,
+                         void** comm_out);
+int tnb_nccl_comm_destroy(void* comm);
+/* in-place sum of n complex values (complex64 if TNB_SINGLE, complex128
+   otherwise) in device memory; returns after the collective completed. */
+int tnb_allreduce_sum(void* comm, int32_t precision, void* dev_buf, int64_t n_complex,
+                      void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -79,6 +79,10 @@ EXPORTS = {
     "tnb_prob_is_sorted_desc": (i32, [i32, P, i64, C.POINTER(i32)]),
     "tnb_prob_prefix_sums": (i32, [i32, P, i64, C.POINTER(i64), i32, C.POINTER(f64)]),
     "tnb_prob_ks": (i32, [i32, P, i64, f64, C.POINTER(f64)]),
+    "tnb_nccl_unique_id": (i32, [P]),
+    "tnb_nccl_comm_create": (i32, [i32, P, i32, i32, C.POINTER(C.c_void_p)]),
+    "tnb_nccl_comm_destroy": (i32, [C.c_void_p]),
+    "tnb_allreduce_sum": (i32, [C.c_void_p, i32, C.c_void_p, i64, C.c_void_p]),
 }
 
 _lib = None

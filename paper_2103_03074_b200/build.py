@@ -16,7 +16,7 @@ import sys
 PKG = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "libtnb.so")
-SOURCES = ["kernels.cu", "gemm_tc.cu", "program.cu", "analytics.cu", "tnb_api.cu"]
+SOURCES = ["kernels.cu", "gemm_tc.cu", "program.cu", "analytics.cu", "collective.cu", "tnb_api.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xcompiler", "-Wall",
          "-Wno-deprecated-gpu-targets", "-diag-suppress", "177"]
@@ -60,7 +60,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
     objs = [os.path.join(objdir, s.replace(".cu", ".o")) for s in SOURCES]
     if force or jobs or not os.path.exists(LIB):
         tmp = LIB + ".tmp"
-        run([nvcc, *ARCH, "-shared", "-o", tmp, *objs])
+        run([nvcc, *ARCH, "-shared", "-o", tmp, *objs, "-ldl"])
         os.replace(tmp, LIB)
     # host-side plan optimiser (g++)
     from .treeopt import build as build_plan

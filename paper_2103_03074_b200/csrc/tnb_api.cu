@@ -350,4 +350,30 @@ int tnb_prob_ks(int32_t device, const double* probs_sorted_asc, int64_t n, doubl
   });
 }
 
+int tnb_nccl_unique_id(uint8_t id_out[128]) {
+  return guarded([&] {
+    if (!id_out) throw Error(TNB_ERR_ARG, "null id buffer");
+    nccl_unique_id(id_out);
+  });
+}
+
+int tnb_nccl_comm_create(int32_t nranks, const uint8_t id[128], int32_t rank, int32_t device,
+                         void** comm_out) {
+  return guarded([&] {
+    if (!id || !comm_out) throw Error(TNB_ERR_ARG, "null NCCL argument");
+    *comm_out = nccl_comm_create(nranks, id, rank, device);
+  });
+}
+
+int tnb_nccl_comm_destroy(void* comm) {
+  return guarded([&] { nccl_comm_destroy(comm); });
+}
+
+int tnb_allreduce_sum(void* comm, int32_t precision, void* dev_buf, int64_t n_complex, void* stream) {
+  return guarded([&] {
+    if (precision != TNB_SINGLE && precision != TNB_DOUBLE) throw Error(TNB_ERR_ARG, "bad precision");
+    nccl_allreduce_sum(comm, precision, dev_buf, n_complex, stream);
+  });
+}
+
 }  // extern "C"

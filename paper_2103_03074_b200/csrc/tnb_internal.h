@@ -240,4 +240,10 @@ void tc_launch_gemm(const TcGemmPlan* p, cudaStream_t s);
 int64_t tc_workspace_elems(int64_t M, int64_t Np, int64_t Kp, int num_sms);
 int tc_splits(int64_t M, int64_t Np, int64_t Kp, int num_sms);
 
+// collective.cu: NCCL (dlopen'd) sum over ranks of complex partials
+void nccl_unique_id(uint8_t* out128);
+void* nccl_comm_create(int nranks, const uint8_t* id128, int rank, int device);
+void nccl_comm_destroy(void* comm);
+void nccl_allreduce_sum(void* comm, int precision, void* buf, int64_t n_complex, void* stream);
+
 }  // namespace tnb

@@ -136,3 +136,58 @@ def sharded_amplitudes(tn, tree, sliced_indices, s1, slice_range=None, precision
     dist.all_reduce(flat, group=group)
     amps = torch.view_as_complex(flat.reshape(-1, 2)).cpu().numpy()
     return dataclasses.replace(tab, amplitudes=amps.astype(np.asarray(tab.amplitudes).dtype))
+
+
+class NcclComm:
+    """The C-ABI collective (``tnb_allreduce_sum``, include/tnb.h) for callers
+    that do not run torch.distributed: one communicator per process/device.
+    The 128-byte NCCL id is created on rank 0 and shared by the caller
+    (``unique_id()``; e.g. over any side channel or a gloo broadcast)."""
+
+    def __init__(self, nranks: int, uid: bytes, rank: int, device: int = 0):
+        import ctypes as C
+
+        from . import _lib
+
+        if len(uid) != 128:
+            raise ValueError("NCCL unique id must be 128 bytes")
+        self._lib = _lib
+        buf = C.create_string_buffer(uid, 128)
+        out = C.c_void_p()
+        _lib.check(_lib.load().tnb_nccl_comm_create(nranks, C.addressof(buf), rank, device,
+                                                    C.byref(out)))
+        self.handle = out
+
+    @staticmethod
+    def unique_id() -> bytes:
+        import ctypes as C
+
+        from . import _lib
+
+        buf = C.create_string_buffer(128)
+        _lib.check(_lib.load().tnb_nccl_unique_id(C.addressof(buf)))
+        return buf.raw
+
+    def allreduce_sum(self, tensor, stream=None) -> None:
+        """In-place sum over ranks of a complex64/complex128 CUDA tensor."""
+        import torch
+
+        if not tensor.is_cuda or not tensor.is_contiguous():
+            raise ValueError("allreduce_sum needs a contiguous CUDA tensor")
+        prec = {torch.complex64: self._lib.TNB_SINGLE, torch.complex128: self._lib.TNB_DOUBLE}
+        if tensor.dtype not in prec:
+            raise ValueError("allreduce_sum takes complex64 or complex128")
+        s = stream.cuda_stream if stream is not None else None
+        self._lib.check(self._lib.load().tnb_allreduce_sum(self.handle, prec[tensor.dtype],
+                                                           tensor.data_ptr(), tensor.numel(), s))
+
+    def close(self) -> None:
+        if self.handle:
+            self._lib.check(self._lib.load().tnb_nccl_comm_destroy(self.handle))
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:  # noqa: BLE001
+            pass

@@ -30,3 +30,25 @@ def test_gpu_partials_through_files_reduce_bit_exactly(gpu, workloads, tmp_path,
     lines = (tmp_path / "amps.tsv").read_text().splitlines()
     assert len(lines) == 2 + (1 << len(tab.open_qubits))
     assert lines[2].split("\t")[0] == tab.bitstring(0)
+
+
+@pytest.mark.gpu
+def test_c_abi_nccl_allreduce_single_rank(gpu):
+    """tnb_allreduce_sum over a 1-rank communicator (the only NCCL shape a
+    1-GPU box allows): the collective path runs and leaves the sum intact."""
+    import torch
+
+    from paper_2103_03074_b200.distributed import NcclComm
+
+    uid = NcclComm.unique_id()
+    comm = NcclComm(1, uid, 0, 0)
+    x = (torch.randn(1 << 20, dtype=torch.complex64, device="cuda"))
+    ref = x.clone()
+    comm.allreduce_sum(x)
+    torch.cuda.synchronize()
+    assert torch.equal(x, ref)
+    y = torch.randn(1000, dtype=torch.complex128, device="cuda")
+    yr = y.clone()
+    comm.allreduce_sum(y, stream=torch.cuda.current_stream())
+    assert torch.equal(y, yr)
+    comm.close()
