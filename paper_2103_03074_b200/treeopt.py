@@ -200,7 +200,7 @@ def select_slices_b200(tn, tree, target_space: int, *, objective: str = "mults",
                        polish_k: int = 12, slice_repeats: int = 2, threads: int = 0,
                        seed: int = 0, time_budget_s: float = 60.0,
                        initial_slices=None, gemm_flops: float = 4.1e14,
-                       hbm_bytes: float = 4.0e12, step_s: float = 5e-6, stats: dict | None = None,
+                       hbm_bytes: float | None = None, step_s: float = 5e-6, stats: dict | None = None,
                        restarts: int = 1, keep_slices: bool = False):
     """Drop-in for ``tncut.slicing.select_slices`` (slicing.py:76-196).
 
@@ -229,6 +229,8 @@ def select_slices_b200(tn, tree, target_space: int, *, objective: str = "mults",
         if stats is not None:
             stats.update(best[1], restarts=restarts)
         return best[0]
+    if hbm_bytes is None:  # model bandwidth (bytes/s); TNB_MODEL_BW overrides
+        hbm_bytes = float(os.environ.get("TNB_MODEL_BW", "4.0e12"))
     if keep_slices and not initial_slices:
         raise ValueError("keep_slices needs initial_slices (the sliced set to keep)")
     hp = head_problem(tn, tree)
