@@ -359,12 +359,23 @@ def compute_head_vector(tn, tree, sliced_indices, s1, slice_range=None, precisio
         n_all = 1 << len(sliced_indices)
         a0, b0 = slice_range if slice_range is not None else (0, n_all)
         k = min(_slice_batch, len(sliced_indices))
-        if k and 0 <= a0 < b0 <= n_all and a0 % (1 << k) == 0 and b0 % (1 << k) == 0:
-            from .slice_batch import compute_head_vector_slice_batched
+        from .slice_batch import compute_head_vector_slice_batched
 
-            return compute_head_vector_slice_batched(tn, tree, sliced_indices, s1, slice_range,
-                                                     batch_log2=k, precision=precision, mode=mode,
-                                                     stats=stats, device=device)
+        # the widest aligned block that fits (rank <= 32, device memory);
+        # otherwise the per-slice path below
+        while k and 0 <= a0 < b0 <= n_all:
+            if a0 % (1 << k) == 0 and b0 % (1 << k) == 0:
+                try:
+                    return compute_head_vector_slice_batched(
+                        tn, tree, sliced_indices, s1, slice_range, batch_log2=k,
+                        precision=precision, mode=mode, stats=stats, device=device)
+                except ShapeMismatch:
+                    pass
+                except RuntimeError as exc:
+                    if "out of memory" not in str(exc):
+                        raise
+                    clear_cache()
+            k -= 1
     s1 = normalize_s1(tn, s1)
     tn = tn.repin(s1)
     sliced_indices = list(sliced_indices)

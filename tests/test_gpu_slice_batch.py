@@ -85,3 +85,20 @@ def test_co_optimised_plan_blocks_match_per_slice(gpu, workloads):
                                   precision="single")
     tnb.clear_cache()
     assert rel_l2(hv.data, ref.data) < TOL
+
+
+def test_public_api_falls_back_to_narrower_blocks(gpu, workloads):
+    """C5_32 (rank-32 plan): 2^4 blocks would need rank > 32, so the API
+    takes the widest block that fits (or the per-slice path) silently."""
+    import gc
+
+    w = workloads("c5_32")
+    try:
+        tnb.set_slice_batch(4)
+        hv = tnb.compute_head_vector(w.tn, w.tree, w.sliced, None, slice_range=(0, 16),
+                                     precision="single")
+    finally:
+        tnb.set_slice_batch(0)
+    tnb.clear_cache()
+    gc.collect()
+    assert hv.slice_range == (0, 16) and np.isfinite(hv.data).all()
