@@ -178,6 +178,8 @@ def run_ours(args):
     from paper_2103_03074_b200.planner import split
 
     world, rank, local, dist = setup_dist(args)
+    if world > 1:  # host planning threads per rank (the plan legs run treeopt on every rank)
+        os.environ.setdefault("TNB_PLAN_THREADS", str(max(1, HOST_CORES // world)))
     torch.cuda.set_device(local)
     tnb.set_device(local)
     w = tnb.load_workload(args.workload)

@@ -248,7 +248,7 @@ def select_slices_b200(tn, tree, target_space: int, *, objective: str = "mults",
     opt.keep_top = int(keep_top)
     opt.reconf_k = int(reconf_k)
     opt.polish_k = int(polish_k)
-    opt.threads = int(threads)
+    opt.threads = int(threads) if threads else int(os.environ.get("TNB_PLAN_THREADS", "0") or 0)
     opt.objective = _objective(objective)
     opt.seed = int(seed)
     opt.gemm_flops = float(gemm_flops)
