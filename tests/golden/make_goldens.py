@@ -144,10 +144,10 @@ def make_golden(name):
             out[f"head_fixed_{a}_{b}"] = tengine.compute_head_vector(
                 tn, tree, sliced, None, slice_range=(a, b), precision="double").data
     else:
-        ranges = {"s8": [(0, 4), (0, 1), (4, 8)], "s8_opt": [(0, 4), (0, 1)], "c4_opt": [(0, 1)], "c4_opt_b200": [(0, 1)], "c4_opt31_b200": [(0, 1)], "m12": [(0, 1)], "c2": [(0, 1)],
+        ranges = {"s8": [(0, 4), (0, 1), (4, 8)], "s8_opt": [(0, 4), (0, 1)], "c4_opt": [(0, 1)], "c4_opt_b200": [(0, 1)], "c4_opt31_b200": [(0, 1)], "c2_opt_b200": [(0, 1)], "c3_opt_b200": [(0, 1)], "m12": [(0, 1)], "c2": [(0, 1)],
                   "c3": [(0, 1)], "c4": [(0, 1)], "c5_26": [(0, 2)], "c5_28": [(0, 1)],
                   "c5_n21": [(0, 1)]}[name]
-        stride = {"s8_opt": 32, "c4_opt": 64, "c4_opt_b200": 64, "c4_opt31_b200": 64, "s8": 32, "m12": 64, "c2": 1, "c3": 4, "c4": 64, "c5_26": 64, "c5_28": 64,
+        stride = {"s8_opt": 32, "c4_opt": 64, "c4_opt_b200": 64, "c4_opt31_b200": 64, "c2_opt_b200": 1, "c3_opt_b200": 4, "s8": 32, "m12": 64, "c2": 1, "c3": 4, "c4": 64, "c5_26": 64, "c5_28": 64,
                   "c5_n21": 64}[name]
         for (a, b) in ranges:
             st = tengine.EngineStats()
@@ -166,7 +166,7 @@ def make_golden(name):
                 out[f"head_double_{a}_{b}_sub"], out[f"head_double_{a}_{b}_norm2"] = sub(pd.data, stride)
             if (a, b) == ranges[0]:
                 full = dataclasses.replace(p, slice_range=(0, 1 << n_e))
-                amp_stride = {"s8_opt": 1, "c4_opt": 16, "c4_opt_b200": 16, "c4_opt31_b200": 16, "s8": 1, "m12": 256, "c2": 1, "c3": 16, "c4": 16, "c5_26": 16,
+                amp_stride = {"s8_opt": 1, "c4_opt": 16, "c4_opt_b200": 16, "c4_opt31_b200": 16, "c2_opt_b200": 1, "c3_opt_b200": 16, "s8": 1, "m12": 256, "c2": 1, "c3": 16, "c4": 16, "c5_26": 16,
                               "c5_28": 16, "c5_n21": 32}[name]
                 if name in ("s8", "c2", "s8_opt"):
                     t1 = time.time()

@@ -39,6 +39,9 @@ PLANS = {
     # fewer, bigger slices), then the B200 polish
     "c4_opt31": ("c4", 31, "mults", {"restarts": 16}),
     "c4_opt31_b200": ("c4_opt31", 31, "b200", {"trials": 0, "keep_top": 0, "slice_repeats": 1}, "c4"),
+    # C2 (m=12, t=2^28) and C3 (m=14, t=2^30): co-optimised + B200 polish
+    "c2_opt_b200": ("c2", 28, "b200", {"restarts": 4}),
+    "c3_opt_b200": ("c3", 30, "b200", {"restarts": 4}),
     # the reference plan's OWN sliced set (same slices, same partial head
     # vectors), head tree re-ordered: exact DP, then the B200 polish
     "c4_reordered": ("c4", 30, "b200", {"keep_slices": True}),
