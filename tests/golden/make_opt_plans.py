@@ -42,6 +42,9 @@ PLANS = {
     # C2 (m=12, t=2^28) and C3 (m=14, t=2^30): co-optimised + B200 polish
     "c2_opt_b200": ("c2", 28, "b200", {"restarts": 4}),
     "c3_opt_b200": ("c3", 30, "b200", {"restarts": 4}),
+    # a second, independent C3 plan (other seeds): its full slice sum must
+    # equal c3_opt_b200's (plan independence of the complete contraction)
+    "c3_opt_b200_alt": ("c3", 30, "b200", {"restarts": 2, "seed": 100}),
     # the reference plan's OWN sliced set (same slices, same partial head
     # vectors), head tree re-ordered: exact DP, then the B200 polish
     "c4_reordered": ("c4", 30, "b200", {"keep_slices": True}),
