@@ -42,6 +42,7 @@ PLANS = {
     # C2 (m=12, t=2^28) and C3 (m=14, t=2^30): co-optimised + B200 polish
     "c2_opt_b200": ("c2", 28, "b200", {"restarts": 4}),
     "c3_opt_b200": ("c3", 30, "b200", {"restarts": 4}),
+    "c2_opt_b200_alt": ("c2", 28, "b200", {"restarts": 2, "seed": 100}),
     # a second, independent C3 plan (other seeds): its full slice sum must
     # equal c3_opt_b200's (plan independence of the complete contraction)
     "c3_opt_b200_alt": ("c3", 30, "b200", {"restarts": 2, "seed": 100}),

@@ -115,3 +115,27 @@ def test_c5_32_reordered_matches_given_tree(gpu, workloads):
     b = tnb.compute_head_vector(r.tn, r.tree, r.sliced, None, slice_range=(0, 1), precision="single")
     tnb.clear_cache()
     assert rel_l2(a.data, b.data) < TOL
+
+
+def test_c2_complete_contraction_is_plan_independent(gpu, workloads):
+    """ALL slices of two independently co-optimised C2 plans (different
+    trees and sliced sets): the complete head sums give the same 2^10
+    amplitudes and XEB (a finished 53-qubit m=12 answer, ~1 min)."""
+    import gc
+
+    amps = []
+    try:
+        tnb.set_slice_batch(3)
+        for name in ("c2_opt_b200", "c2_opt_b200_alt"):
+            w = workloads(name)
+            hv = tnb.compute_head_vector(w.tn, w.tree, w.sliced, None, precision="single")
+            assert hv.slice_range == (0, 1 << w.n_e)
+            tab = tnb.compute_tail_amplitudes(w.tn, w.tree, hv, precision="single")
+            amps.append(tab.amplitudes.astype(np.complex128))
+            tnb.clear_cache()
+            gc.collect()
+    finally:
+        tnb.set_slice_batch(0)
+    assert rel_l2(amps[1], amps[0]) < TOL
+    p0, p1 = np.abs(amps[0]) ** 2, np.abs(amps[1]) ** 2
+    assert abs(O.xeb(p0, 53) - O.xeb(p1, 53)) < 1e-3

@@ -24,7 +24,7 @@ from paper_2103_03074_b200 import treeopt
 from paper_2103_03074_b200.planner import split, step_mults
 
 OPT = {"c1_opt": "c1", "s8_opt": "s8", "c4_opt": "c4", "c4_opt_b200": "c4", "c4_reordered": "c4",
-       "c4_opt31": "c4", "c4_opt31_b200": "c4", "c2_opt_b200": "c2", "c3_opt_b200": "c3",
+       "c4_opt31": "c4", "c4_opt31_b200": "c4", "c2_opt_b200": "c2", "c2_opt_b200_alt": "c2", "c3_opt_b200": "c3",
        "c3_opt_b200_alt": "c3",
        "c5_26_reordered": "c5_26", "c5_28_reordered": "c5_28", "c5_32_reordered": "c5_32"}
 
