@@ -66,6 +66,18 @@ int tnbp_tree_cost(int n_leaves, const int* leaf_ptr, const int* leaf_idx, int n
                    const int* children, const int* sliced, int n_sliced, int objective,
                    double* out_stats);
 
+/* Pairwise order of a whole (small) network, no slicing: a deterministic
+ * size-reduction greedy, then every subtree of <= opt->polish_k operands
+ * re-optimised exactly under opt->objective (the whole order when
+ * n_leaves <= polish_k), intermediates kept <= max(opt->target_log2, the
+ * greedy's largest).  Used for the head-absorbed tail (the reference orders
+ * its tail with the greedy of ordering.py:256-285 and contracts it per
+ * pinned block, engine.py:348-377).  Open legs (one endpoint) stay open.
+ * out_children: (n-1)*2 ints, SSA post-order as in tnbp_optimize.
+ * out_stats[3] = {log2 model cost, max rank, log2 multiplications}. */
+int tnbp_order(int n_leaves, const int* leaf_ptr, const int* leaf_idx, int n_index,
+               const tnbp_options* opt, int* out_children, double* out_stats);
+
 const char* tnbp_last_error(void);
 
 #ifdef __cplusplus

@@ -113,9 +113,10 @@ def compute_head_vectors_batched(tn, tree, sliced_indices, s1_list, slice_range=
         raise RangeOutOfBounds(f"range [{a},{b}) outside [0,{total})")
     cut = sorted(cut)
     # root axes: the varying qubits (major, MSB first), then the cut ids
-    prog = E.get_program(E._leaf_entries(tnb, head_leaves), E._steps_tuples(head_steps),
-                         sliced_indices, list(q_ix) + cut, precision, device)
-    data = prog.run_range(a, b, mode)
+    entries = E._leaf_entries(tnb, head_leaves)
+    prog = E.get_program(entries, E._steps_tuples(head_steps), sliced_indices, list(q_ix) + cut,
+                         precision, device, upload=False)
+    data = prog.run(entries, a, b, mode)
     if stats is not None:
         from .planner import step_mults
 

@@ -491,6 +491,64 @@ int tnbp_tree_cost(int n_leaves, const int* leaf_ptr, const int* leaf_idx, int n
   return 0;
 }
 
+int tnbp_order(int n_leaves, const int* leaf_ptr, const int* leaf_idx, int n_index,
+               const tnbp_options* opt, int* out_children, double* out_stats) {
+  try {
+    if (n_leaves < 2) { g_err = "need at least two leaves"; return 1; }
+    if (n_index > W * 64) { g_err = "more than 2048 distinct indices"; return 1; }
+    Net net;
+    net.n = n_leaves;
+    net.nidx = n_index;
+    net.leaf.resize(n_leaves);
+    std::vector<int> deg(n_index, 0);
+    for (int i = 0; i < n_leaves; ++i) {
+      net.leaf[i].clear();
+      for (int p = leaf_ptr[i]; p < leaf_ptr[i + 1]; ++p) {
+        int ix = leaf_idx[p];
+        if (ix < 0 || ix >= n_index) { g_err = "index id out of range"; return 1; }
+        net.leaf[i].set(ix);
+        ++deg[ix];
+      }
+    }
+    for (int ix = 0; ix < n_index; ++ix)
+      if (deg[ix] > 2) { g_err = "index with more than two endpoints"; return 1; }
+    net.sliceable.clear();
+    auto t0 = std::chrono::steady_clock::now();
+    // deterministic size-reduction greedy (no sampling), then exact subset-DP
+    // re-optimisation of every subtree of <= polish_k operands under the
+    // chosen cost model; with n_leaves <= polish_k the whole order is exact.
+    std::mt19937_64 rng(opt->seed);
+    Tree t = greedy_tree(net, rng, 1.0, 0.0);
+    Model m{opt->objective, opt->gemm_flops, opt->hbm_bytes, opt->step_s};
+    BS none;
+    none.clear();
+    Eval e;
+    evaluate(net, t, none, m, e);
+    int cap = std::max(e.sc, opt->target_log2);
+    reconf(net, t, none, std::min(opt->polish_k, n_leaves), cap, m, e, 8, opt->time_budget_s, t0);
+    std::vector<int> post;
+    postorder(t, post);
+    std::vector<int> newid(2 * n_leaves - 1, -1);
+    for (int i = 0; i < n_leaves; ++i) newid[i] = i;
+    for (int i = 0; i < (int)post.size(); ++i) newid[post[i]] = n_leaves + i;
+    for (int i = 0; i < (int)post.size(); ++i) {
+      int v = post[i];
+      out_children[2 * i] = newid[t.L[v - n_leaves]];
+      out_children[2 * i + 1] = newid[t.R[v - n_leaves]];
+    }
+    Model mm{0, 1, 1, 0};
+    Eval e2;
+    evaluate(net, t, none, mm, e2);
+    out_stats[0] = std::log2(e.cost);
+    out_stats[1] = e.sc;
+    out_stats[2] = std::log2(e2.cost);
+    return 0;
+  } catch (const std::exception& ex) {
+    g_err = ex.what();
+    return 3;
+  }
+}
+
 int tnbp_optimize(int n_leaves, const int* leaf_ptr, const int* leaf_idx, int n_index,
                   const unsigned char* sliceable, const int* init_children, const int* init_sliced,
                   int n_init_sliced, const tnbp_options* opt, int* out_children, int* out_sliced,

@@ -33,9 +33,9 @@ import threading
 import numpy as np
 
 from . import _lib
-from .errors import (ProvenanceMismatch, RangeGap, RangeOutOfBounds, RangeOverlap,
+from .errors import (BlockTooWide, ProvenanceMismatch, RangeGap, RangeOutOfBounds, RangeOverlap,
                      ShapeMismatch)
-from .planner import cluster_small_steps, greedy_steps, split, step_mults
+from .planner import cluster_small_steps, split, step_mults
 from .provenance import circuit_sha, normalize_s1, order_sha256, provenance_hash
 from .types import AmplitudeTable, EngineStats, HeadVector
 
@@ -51,6 +51,38 @@ _flags = 0
 def set_device(device: int) -> None:
     global _default_device
     _default_device = int(device)
+
+
+_thread_devices = False
+_thread_local = threading.local()
+_thread_counter = [0]
+_thread_lock = threading.Lock()
+
+
+def set_thread_devices(on: bool) -> None:
+    """Bind each calling thread to its own device, round-robin over the
+    visible GPUs (first call of a thread picks the next one).  The
+    reference's ``cli run --threads T`` fans ranges out over T threads
+    (cli.py:367-380); with this on, those threads spread over the box's
+    GPUs instead of queueing on device 0.  Off: every call uses
+    ``set_device``'s device."""
+    global _thread_devices
+    _thread_devices = bool(on)
+
+
+def _resolve_device(device):
+    if device is not None:
+        return int(device)
+    if not _thread_devices:
+        return _default_device
+    dev = getattr(_thread_local, "device", None)
+    if dev is None:
+        n = max(1, _lib.device_count())
+        with _thread_lock:
+            dev = (_default_device + _thread_counter[0]) % n
+            _thread_counter[0] += 1
+        _thread_local.device = dev
+    return dev
 
 
 _reorder = os.environ.get("TNB_REORDER", "0") not in ("", "0")
@@ -180,6 +212,20 @@ class Program:
     def update_leaves(self, leaves) -> None:
         """Upload leaves whose values changed (repin), topology unchanged --
         one batched, staged upload through tnb_program_set_leaves."""
+        with self.lock:
+            self._update_leaves(leaves)
+
+    def run(self, leaves, a: int, b: int, mode: str = "fixed", out=None):
+        """Upload ``leaves`` and run [a, b) as ONE critical section: programs
+        are cached per topology and shared between threads (the reference's
+        ``cli run --threads`` fans compute_head_vector out over disjoint
+        ranges, cli.py:367-380), so two callers with different s1 must not
+        interleave their uploads with each other's runs."""
+        with self.lock:
+            self._update_leaves(leaves)
+            return self._run_range(a, b, mode, out)
+
+    def _update_leaves(self, leaves) -> None:
         pos_list, datas = [], []
         for nid, _, d in leaves:
             pos = self.leaf_pos[nid]
@@ -210,12 +256,17 @@ class Program:
             flat.ctypes.data_as(C.POINTER(C.c_double))))
 
     def set_leaf_device(self, pos: int, dev_ptr: int) -> None:
-        _lib.check(self.lib.tnb_program_set_leaf_device(self.handle, pos, C.c_void_p(dev_ptr)))
-        self._leaf_data[pos] = None  # unknown host copy: force upload next time
+        with self.lock:
+            _lib.check(self.lib.tnb_program_set_leaf_device(self.handle, pos, C.c_void_p(dev_ptr)))
+            self._leaf_data[pos] = None  # unknown host copy: force upload next time
 
     def run_range(self, a: int, b: int, mode: str = "fixed", out=None) -> np.ndarray:
         """Host result (numpy) unless ``out`` is a device pointer (int)."""
         with self.lock:
+            return self._run_range(a, b, mode, out)
+
+    def _run_range(self, a, b, mode, out):
+        if True:
             if out is None:
                 res = _host_array(self.info.out_elems, self.dtype)
                 _lib.check(self.lib.tnb_program_run_range(
@@ -281,8 +332,12 @@ def _signature(leaves, steps, sliced, out_order, precision, device, flags) -> st
     return h.hexdigest()
 
 
-def get_program(leaves, steps, sliced, out_order, precision, device=None, flags=None) -> Program:
-    device = _default_device if device is None else device
+def get_program(leaves, steps, sliced, out_order, precision, device=None, flags=None,
+                upload: bool = True) -> Program:
+    """The cached program for this topology; ``upload`` puts ``leaves``' values
+    on it (single-threaded callers).  Engine calls pass upload=False and run
+    through ``Program.run`` so upload and run are one critical section."""
+    device = _resolve_device(device)
     flags = _flags if flags is None else flags
     key = _signature(leaves, steps, sliced, out_order, precision, device, flags)
     with _cache_lock:
@@ -305,7 +360,8 @@ def get_program(leaves, steps, sliced, out_order, precision, device=None, flags=
             _cache[key] = prog
         else:
             _cache[key] = _cache.pop(key)  # LRU touch
-    prog.update_leaves(leaves)
+    if upload:
+        prog.update_leaves(leaves)
     return prog
 
 
@@ -317,19 +373,26 @@ def clear_cache() -> None:
 _split_cache: dict = {}
 
 
+def _topology_key(tn, tree) -> tuple:
+    """What ``split`` and the tail order depend on: the tree's steps and every
+    node's index list -- not leaf values, so every ``repin`` of a network
+    (one per s1) shares one entry."""
+    return (tuple((s.lhs, s.rhs, s.out) for s in tree.steps), tree.first_cut,
+            tuple((nid, tuple(tn.nodes[nid].indices)) for nid in sorted(tn.nodes)))
+
+
 def _split(tn, tree):
-    """planner.split memoised per (network, tree) object pair: the split only
-    depends on the topology, and repeated calls on the same objects (slice
-    ranges, tail after head) are common.  The cache holds references to both
-    objects, so an id is never reused while its entry lives."""
-    key = (id(tn), id(tree), len(tree.steps))
+    """planner.split memoised per topology (``_topology_key``): repeated calls
+    (slice ranges, tail after head, an s1 sweep) reuse one split."""
+    key = _topology_key(tn, tree)
     hit = _split_cache.get(key)
-    if hit is not None and hit[0] is tn and hit[1] is tree:
-        return hit[2]
+    if hit is not None:
+        return hit
     res = split(tn, tree)
-    if len(_split_cache) >= 16:
-        _split_cache.pop(next(iter(_split_cache)))
-    _split_cache[key] = (tn, tree, res)
+    with _cache_lock:
+        if len(_split_cache) >= 16:
+            _split_cache.pop(next(iter(_split_cache)))
+        _split_cache[key] = res
     return res
 
 
@@ -369,7 +432,7 @@ def compute_head_vector(tn, tree, sliced_indices, s1, slice_range=None, precisio
                     return compute_head_vector_slice_batched(
                         tn, tree, sliced_indices, s1, slice_range, batch_log2=k,
                         precision=precision, mode=mode, stats=stats, device=device)
-                except ShapeMismatch:
+                except BlockTooWide:
                     pass
                 except RuntimeError as exc:
                     if "out of memory" not in str(exc):
@@ -400,9 +463,10 @@ def compute_head_vector(tn, tree, sliced_indices, s1, slice_range=None, precisio
         data = _degenerate_sum(b - a, dtype, mode)
     else:
         run_steps = _exec_head_steps(tn, tree, head_leaves, head_steps, sliced_indices)
-        prog = get_program(_leaf_entries(tn, head_leaves), _steps_tuples(run_steps),
-                           sliced_indices, sorted(cut), precision, device)
-        data = prog.run_range(a, b, mode)
+        entries = _leaf_entries(tn, head_leaves)
+        prog = get_program(entries, _steps_tuples(run_steps), sliced_indices, sorted(cut),
+                           precision, device, upload=False)
+        data = prog.run(entries, a, b, mode)
         if stats is not None:
             sets = {nid: tn.nodes[nid].indices for nid in head_leaves}
             mults, _ = step_mults(sets, head_steps, frozenset(sliced_indices))
@@ -429,20 +493,26 @@ _tail_plan_cache: dict = {}
 
 
 def tail_plan(tn, tree, cut, head_id=None):
-    """Leaves + greedy steps of the head-absorbed tail network (memoised per
-    (network, tree, cut) like ``_split``: the order depends on the topology only)."""
+    """Leaves + pairwise order of the head-absorbed tail network, memoised per
+    topology (the order does not depend on leaf values).  The order comes
+    from the native planner (``treeopt.order_network``: greedy, then exact
+    subset-DP re-optimisation under the B200 time model), intermediates
+    capped at 2^31 elements where the network allows."""
     _, _, tail_leaves, _, _ = _split(tn, tree)
     hid = (max(tn.nodes) + 1) if head_id is None else head_id
-    key = (id(tn), id(tree), tuple(cut), hid)
+    key = (tuple((nid, tuple(tn.nodes[nid].indices)) for nid in tail_leaves), tuple(cut), hid)
     hit = _tail_plan_cache.get(key)
-    if hit is not None and hit[0] is tn and hit[1] is tree:
-        return tail_leaves, hid, hit[2]
+    if hit is not None:
+        return tail_leaves, hid, hit
+    from .treeopt import order_network
+
     sets = {nid: frozenset(tn.nodes[nid].indices) for nid in tail_leaves}
     sets[hid] = frozenset(cut)
-    steps = greedy_steps(sets, hid + 1)
-    if len(_tail_plan_cache) >= 16:
-        _tail_plan_cache.pop(next(iter(_tail_plan_cache)))
-    _tail_plan_cache[key] = (tn, tree, steps)
+    steps = order_network(sets, hid + 1, cap_log2=31)
+    with _cache_lock:
+        if len(_tail_plan_cache) >= 16:
+            _tail_plan_cache.pop(next(iter(_tail_plan_cache)))
+        _tail_plan_cache[key] = steps
     return tail_leaves, hid, steps
 
 
@@ -501,8 +571,8 @@ def _tail(tn, tree, head, space_cap, precision, stats, device):
     entries.append((hid, list(head.cut_order), np.asarray(head.data).reshape(-1)))
     out_order = [tn.open_output_indices[q] for q in open_qubits]
     # cache keyed on topology only: the head leaf is re-uploaded when it changes
-    prog = get_program(entries, steps, [], out_order, precision, device)
-    amps = prog.run_range(0, 1, "fixed")
+    prog = get_program(entries, steps, [], out_order, precision, device, upload=False)
+    amps = prog.run(entries, 0, 1, "fixed")
     return _make_table(tn, tree, head, amps.astype(dtype, copy=False), open_qubits, precision)
 
 
@@ -540,8 +610,8 @@ def contract_tree(tn, tree, slice_assignment, dtype=np.complex128, stats=None, d
     mask = 0
     for ix in pinned:
         mask = (mask << 1) | (int(slice_assignment[ix]) & 1)
-    prog = get_program(leaves, steps, pinned, root_ids, precision, device)
-    out = prog.run_range(mask, mask + 1, "fixed")
+    prog = get_program(leaves, steps, pinned, root_ids, precision, device, upload=False)
+    out = prog.run(leaves, mask, mask + 1, "fixed")
     if stats is not None:
         mults, _ = step_mults({nid: ix for nid, ix, _ in leaves}, steps, frozenset(pinned))
         stats.multiplications += mults

@@ -42,5 +42,11 @@ except Exception:  # tncut not installed (e.g. the GPU box)
         """Slicing every contracted index still misses the space target (errors.py:77-78)."""
 
 
-__all__ = ["TncutError", "ShapeMismatch", "RangeOutOfBounds", "RangeGap", "RangeOverlap",
+class BlockTooWide(ShapeMismatch):
+    """A batched-slice block would need intermediates above the executor's
+    rank limit (slice_batch.batched_plan); callers fall back to narrower
+    blocks.  A ShapeMismatch subclass, so reference handlers still match."""
+
+
+__all__ = ["BlockTooWide", "TncutError", "ShapeMismatch", "RangeOutOfBounds", "RangeGap", "RangeOverlap",
            "ProvenanceMismatch", "CannotReachCap"]

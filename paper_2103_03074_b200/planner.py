@@ -2,11 +2,11 @@
 
 * ``split`` restates the engine's head/tail split (engine.py:171-185) and
   ``cut_indices`` (ordering.py:372-380) on duck-typed networks/trees.
-* ``greedy_steps`` restates the reference's deterministic greedy pair
-  order (ordering.py:256-285: minimise (result rank, union rank, ids)); the
-  executor uses it to order the head-absorbed tail network, which the
-  reference never builds (it contracts the tail per pinned block and takes
-  a GEMV with the head vector instead, engine.py:358-377).
+* ``step_mults`` is the engine's exact multiplication counter
+  (engine.py:138-140) evaluated analytically from index sets;
+  ``cluster_small_steps`` re-orders a step list so the executor can batch
+  its tiny steps.  (The head-absorbed tail is ordered by the native
+  planner, ``treeopt.order_network``.)
 """
 
 from __future__ import annotations
@@ -31,37 +31,6 @@ def split(tn, tree):
     if tn.open_output_indices:
         return [], [], sorted(tree.leaves), list(tree.steps), []
     return sorted(tree.leaves), list(tree.steps), [], [], []
-
-
-def greedy_steps(index_sets: dict, next_out: int) -> list:
-    """Greedy pairwise order over {id: frozenset(indices)} -> [(lhs, rhs, out)]."""
-    sets = {k: frozenset(v) for k, v in index_sets.items()}
-    live = sorted(sets)
-    steps = []
-
-    def key(i, j):
-        a, b = sets[i], sets[j]
-        return (len(a ^ b), len(a | b), i, j)
-
-    pairs = {}
-    for x, i in enumerate(live):
-        for j in live[x + 1:]:
-            pairs[(i, j)] = key(i, j)
-    while len(live) > 1:
-        (i, j) = min(pairs, key=lambda p: pairs[p])
-        out = next_out
-        next_out += 1
-        sets[out] = sets[i] ^ sets[j]
-        steps.append((i, j, out))
-        live.remove(i)
-        live.remove(j)
-        for p in [p for p in pairs if i in p or j in p]:
-            del pairs[p]
-        for other in live:
-            pair = (other, out) if other < out else (out, other)
-            pairs[pair] = key(*pair)
-        live.append(out)
-    return steps
 
 
 def step_mults(leaf_sets: dict, steps, removed=frozenset()) -> tuple:

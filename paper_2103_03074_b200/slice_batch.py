@@ -28,7 +28,7 @@ import hashlib
 import os
 
 from . import engine as E
-from .errors import RangeOutOfBounds, ShapeMismatch
+from .errors import BlockTooWide, RangeOutOfBounds, ShapeMismatch
 from .planner import cluster_small_steps, step_mults
 from .provenance import normalize_s1, provenance_hash
 from .types import HeadVector
@@ -47,6 +47,8 @@ def batched_plan(tn, tree, sliced_indices, k: int, reorder: bool = True, max_ran
                                tuple(E._steps_tuples(head_steps)), tuple(sliced), k, reorder,
                                max_rank, os.environ.get("TNB_CLUSTER", "1"))).encode()).hexdigest()
     hit = _plans.get(key)
+    if isinstance(hit, BlockTooWide):  # negative results are memoised too
+        raise hit
     if hit is not None:
         return hit
     sets = {n: tn.nodes[n].indices for n in head_leaves}
@@ -66,7 +68,8 @@ def batched_plan(tn, tree, sliced_indices, k: int, reorder: bool = True, max_ran
     _, sc = step_mults(sets, steps, frozenset(reduced))
     sc = max([sc] + [len(set(tn.nodes[n].indices) - set(reduced)) for n in head_leaves])
     if sc > 32:
-        raise ShapeMismatch(f"un-slicing {k} indices needs rank-{sc} intermediates (> 32)")
+        _plans[key] = BlockTooWide(f"un-slicing {k} indices needs rank-{sc} intermediates (> 32)")
+        raise _plans[key]
     _plans[key] = (steps, reduced, sc)
     return _plans[key]
 
@@ -101,9 +104,10 @@ def compute_head_vector_slice_batched(tn, tree, sliced_indices, s1, slice_range=
         if len(eps) != 2 or any(e not in hs for e in eps):
             raise ShapeMismatch(f"sliced index {ix} is not internal to the head")
     steps, reduced, _ = batched_plan(tn, tree, sliced, k, reorder, max_rank)
-    prog = E.get_program(E._leaf_entries(tn, head_leaves), E._steps_tuples(steps), reduced,
-                         sorted(cut), precision, device)
-    data = prog.run_range(a >> k, b >> k, mode)
+    entries = E._leaf_entries(tn, head_leaves)
+    prog = E.get_program(entries, E._steps_tuples(steps), reduced, sorted(cut), precision, device,
+                         upload=False)
+    data = prog.run(entries, a >> k, b >> k, mode)
     if stats is not None:
         sets = {n: tn.nodes[n].indices for n in head_leaves}
         mults, _ = step_mults(sets, head_steps, frozenset(sliced))

@@ -61,7 +61,8 @@ class Options(ctypes.Structure):  # tnb_plan.h: tnbp_options
     ]
 
 
-EXPORTS = ("tnbp_optimize", "tnbp_tree_cost", "tnbp_default_options", "tnbp_last_error")
+EXPORTS = ("tnbp_optimize", "tnbp_order", "tnbp_tree_cost", "tnbp_default_options",
+           "tnbp_last_error")
 
 
 def build(force: bool = False) -> str:
@@ -93,6 +94,8 @@ def load():
                                       ctypes.POINTER(ctypes.c_double)]
         lib.tnbp_tree_cost.argtypes = [ctypes.c_int, ip, ip, ctypes.c_int, ip, ip, ctypes.c_int,
                                        ctypes.c_int, ctypes.POINTER(ctypes.c_double)]
+        lib.tnbp_order.argtypes = [ctypes.c_int, ip, ip, ctypes.c_int, ctypes.POINTER(Options), ip,
+                                   ctypes.POINTER(ctypes.c_double)]
         lib.tnbp_default_options.argtypes = [ctypes.POINTER(Options)]
         lib.tnbp_last_error.restype = ctypes.c_char_p
         _lib = lib
@@ -170,6 +173,52 @@ def head_problem(tn, tree) -> HeadProblem:
         ssa[s.out] = len(head_leaves) + i
     return HeadProblem(head_leaves, index_ids, np.asarray(ptr, np.int32),
                        np.asarray(idx, np.int32), sliceable, np.asarray(ch, np.int32))
+
+
+def order_network(index_sets: dict, next_out: int, *, cap_log2: int = 30,
+                  objective: str = "b200", exact_k: int = 14, stats: dict | None = None) -> list:
+    """Pairwise order of a whole small network {leaf id: indices} ->
+    [(lhs, rhs, out)] with out ids next_out, next_out + 1, ... (``tnbp_order``).
+
+    A deterministic size-reduction greedy, then every subtree of <= exact_k
+    operands re-optimised exactly under the B200 time model (the whole order
+    when the network has <= exact_k leaves), never creating a tensor above
+    max(cap_log2, the greedy's largest).  Indices with one endpoint stay
+    open.  Used for the head-absorbed tail, which the reference never builds
+    (its blocked tail is ordered by ordering.py:256-285's greedy)."""
+    ids = sorted(index_sets)
+    if len(ids) < 2:
+        return []
+    dense: dict = {}
+    ptr = [0]
+    idx = []
+    for nid in ids:
+        for ix in index_sets[nid]:
+            idx.append(dense.setdefault(ix, len(dense)))
+        ptr.append(len(idx))
+    lp, li = np.asarray(ptr, np.int32), np.asarray(idx or [0], np.int32)
+    opt = Options()
+    lib = load()
+    lib.tnbp_default_options(ctypes.byref(opt))
+    opt.target_log2 = int(cap_log2)
+    opt.polish_k = int(exact_k)
+    opt.objective = _objective(objective)
+    opt.time_budget_s = 30.0
+    n = len(ids)
+    ch = np.zeros(2 * (n - 1), np.int32)
+    st = (ctypes.c_double * 3)()
+    rc = lib.tnbp_order(n, _ptr(lp), _ptr(li), len(dense), ctypes.byref(opt), _ptr(ch), st)
+    if rc:
+        raise ValueError(lib.tnbp_last_error().decode())
+    if stats is not None:
+        stats.update(log2_cost=st[0], sc=int(st[1]), log2_mults=st[2])
+    names = list(ids)
+    steps = []
+    for i in range(n - 1):
+        out = next_out + i
+        steps.append((names[ch[2 * i]], names[ch[2 * i + 1]], out))
+        names.append(out)
+    return steps
 
 
 def tree_cost(tn, tree, sliced, objective: str = "mults") -> tuple:
