@@ -100,10 +100,53 @@ class ClockSampler:
 
 
 # ---------------------------------------------------------------------------
+# TNB_* variables a benchmark of record may carry: launch plumbing only.  Every
+# other TNB_* knob (tile/pacing/fusion overrides, debug prints, the GEMM's
+# promotion chunk) changes the executed schedule, so the bench refuses to run
+# with one set unless --allow-knobs marks the line as a diagnostic run.
+_BENCH_ENV_OK = {"TNB_SHARE_DEVICE", "TNB_DIST_BACKEND", "TNB_REF_BUDGET_S", "TNB_PLAN_THREADS",
+                 "TNB_BENCH_FAIL_LEG", "TNB_BENCH_PROFILE_E2E"}
+
+
+def diagnostic_knobs():
+    return sorted(k for k in os.environ if k.startswith("TNB_") and k not in _BENCH_ENV_OK)
+
+
+def refuse_diagnostics(allow=False):
+    knobs = diagnostic_knobs()
+    if knobs and not allow:
+        raise SystemExit(f"bench: refusing to run with executor knobs set ({', '.join(knobs)}); "
+                         "unset them or pass --allow-knobs (the line is then marked diagnostic)")
+    return knobs
+
+
+def spawn_ranks(n: int, argv) -> int:
+    """``python bench.py --gpus N`` without a launcher: start N rank processes
+    of this script exactly as torchrun would (RANK / LOCAL_RANK / WORLD_SIZE /
+    MASTER_ADDR=127.0.0.1 / MASTER_PORT in the env, one device per rank) and
+    return the worst exit code.  Rank 0 prints the JSON line."""
+    import socket
+
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    procs = []
+    for r in range(n):
+        env = dict(os.environ, RANK=str(r), LOCAL_RANK=str(r), WORLD_SIZE=str(n),
+                   LOCAL_WORLD_SIZE=str(n), MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+        procs.append(subprocess.Popen([sys.executable, os.path.abspath(__file__), *argv], env=env))
+    rc = 0
+    for p in procs:
+        rc = max(rc, p.wait())
+    return rc
+
+
 def setup_dist(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        raise SystemExit(f"bench: --gpus {args.gpus} but WORLD_SIZE={world}")
     # test hook: TNB_SHARE_DEVICE=1 puts every rank on device 0 (gloo), so the
     # multi-rank choreography can be exercised on a single-GPU box
     if os.environ.get("TNB_SHARE_DEVICE") == "1":
@@ -113,12 +156,34 @@ def setup_dist(args):
         import torch
         import torch.distributed as dist_
 
-        if args.impl == "ours":
+        if args.impl == "ours" and torch.cuda.is_available():
             torch.cuda.set_device(local)
         backend = os.environ.get("TNB_DIST_BACKEND") or ("nccl" if args.impl == "ours" else "gloo")
         dist_.init_process_group(backend)
         dist = dist_
     return world, rank, local, dist
+
+
+def rank_inventory(dist, local):
+    """Which device every rank drives (PCI bus id): evidence that N ranks
+    ran on N distinct GPUs, plus the communicator's size and backend."""
+    import torch
+
+    me = {"rank": int(os.environ.get("RANK", "0")), "device": local}
+    if torch.cuda.is_available():
+        p = torch.cuda.get_device_properties(local)
+        me["pci_bus_id"] = f"{p.pci_domain_id:04x}:{p.pci_bus_id:02x}:{p.pci_device_id:02x}"
+        me["name"] = p.name
+    ranks = [me]
+    comm = {"backend": None, "size": 1}
+    if dist is not None:
+        ranks = [None] * dist.get_world_size()
+        dist.all_gather_object(ranks, me)
+        comm = {"backend": dist.get_backend(), "size": dist.get_world_size()}
+        if comm["backend"] == "nccl":
+            comm["nccl_version"] = ".".join(map(str, torch.cuda.nccl.version()))
+    active = len({r.get("pci_bus_id", r["device"]) for r in ranks})
+    return ranks, active, comm
 
 
 def barrier(dist, local):
@@ -143,13 +208,19 @@ def traffic_from_profile():
         return {"traffic": None}
 
 
-def cpu_baseline(w):
+def cpu_baseline(w, budget_s):
+    """One real reference slice (kind "reference"); the sampler of
+    oracle/cpu_sample.py only when the reference is not importable."""
+    line = reference_cpu_baseline(w, budget_s)
+    if "unavailable" not in line:
+        return line
     from oracle.cpu_sample import time_head_slice
 
     est, wall, sample = time_head_slice(w.tn, w.tree, w.sliced, precision="single")
     flops = 8.0 * w.tc_per_slice
     return {"value": 1.0 / est, "unit": "slices/s", "cores": HOST_CORES, "kind": "port",
-            "sample": sample, "est_s_per_slice": est, "tflops": flops / est / 1e12}
+            "sample": "EXTRAPOLATED sampler (reference unavailable: " + line["unavailable"] + "): " + sample,
+            "est_s_per_slice": est, "tflops": flops / est / 1e12}
 
 
 def _run_leg(name, fn):
@@ -170,6 +241,36 @@ def _run_leg(name, fn):
         return {"unavailable": f"{type(exc).__name__}: {str(exc)[:200]}"}
 
 
+def run_dry(args):
+    """The multi-rank plumbing of run_ours without kernels (CPU tests): the
+    rendezvous, the per-rank aligned slice ranges, one all-reduce of an
+    amplitude-sized vector and the max-over-ranks timing."""
+    import torch
+
+    os.environ.setdefault("TNB_DIST_BACKEND", "gloo")
+    world, rank, local, dist = setup_dist(args)
+    ranks, active, comm = rank_inventory(dist, local)
+    total = (args.warmup + args.steps) * args.slices
+    mine = (rank * total, (rank + 1) * total)
+    amps = torch.full((1 << 10,), float(rank + 1), dtype=torch.float32)
+    t0 = time.perf_counter()
+    if dist is not None:
+        dist.all_reduce(amps)
+    ms = torch.tensor([(time.perf_counter() - t0) * 1e3])
+    if dist is not None:
+        dist.all_reduce(ms, op=dist.ReduceOp.MAX)
+        spans = [None] * world
+        dist.all_gather_object(spans, mine)
+    else:
+        spans = [mine]
+    if rank == 0:
+        print(json.dumps({"dry_run": True, "n_gpus": world, "ranks": ranks, "gpus_active": active,
+                          "communicator": comm, "slice_ranges": spans,
+                          "allreduce_sum": float(amps[0]), "max_ms": float(ms[0])}), flush=True)
+    if dist is not None:
+        dist.destroy_process_group()
+
+
 def run_ours(args):
     import torch
 
@@ -182,6 +283,7 @@ def run_ours(args):
         os.environ.setdefault("TNB_PLAN_THREADS", str(max(1, HOST_CORES // world)))
     torch.cuda.set_device(local)
     tnb.set_device(local)
+    ranks, gpus_active, comm = rank_inventory(dist, local)
     w = tnb.load_workload(args.workload)
     S = args.slices
     total_slices = (args.warmup + args.steps) * S
@@ -653,6 +755,9 @@ def run_ours(args):
             **traffic_from_profile(),
         },
         "gpu_launches": launches,
+        "gpus_active": gpus_active,
+        "ranks": ranks,
+        "communicator": comm,
         "device_ms_per_step": {"total": dev_ms / args.steps, "gemm": gemm_ms / args.steps,
                                "non_gemm": (dev_ms - gemm_ms) / args.steps},
         "breakdown_step_ms": {"note": "one extra step after the timed region with CUDA events "
@@ -684,39 +789,146 @@ def run_ours(args):
         opt_plan["all_slices_speedup_log2"] = ref_log2 - opt_plan["all_slices_head_s_log2"]
         if opt_plan.get("batched"):
             opt_plan["batched"]["all_slices_speedup_log2"] = ref_log2 - opt_plan["batched"]["all_slices_head_s_log2"]
+    if getattr(args, "knobs", None):
+        line["diagnostic_knobs"] = {k: os.environ[k] for k in args.knobs}
     if world == 1 and not args.no_cpu:
-        line["cpu_baseline"] = cpu_baseline(w)
+        line["cpu_baseline"] = cpu_baseline(w, args.ref_budget_s)
     print(json.dumps(line), flush=True)
 
 
+REF_INSTALL = os.path.join(ROOT, "baseline", "_ref")  # pip --target install of the reference
+
+
+def import_reference():
+    """The UNMODIFIED reference package ``tncut`` from baseline/_ref (pip
+    --target install, travels to the GPU box); /root/reference/pkg/src in
+    the build container.  None when neither is importable."""
+    for path in (REF_INSTALL, "/root/reference/pkg/src"):
+        if os.path.isdir(os.path.join(path, "tncut")) and path not in sys.path:
+            sys.path.insert(0, path)
+            break
+    os.environ.setdefault("NUMBA_CACHE_DIR", "/tmp/numba_cache_tnb")
+    try:
+        import tncut  # noqa: F401
+        from tncut import engine  # noqa: F401
+    except Exception as exc:  # noqa: BLE001
+        return None, f"{type(exc).__name__}: {exc}"
+    return tncut, None
+
+
+def reference_workload(name):
+    """Network + plan through the reference's OWN builders: parse_circuit
+    (circuit.py), build_network (network.py), doc_to_tree (ordering.py:670-722)
+    on the frozen circuit/order files of tests/golden/<name>."""
+    from tncut import ordering
+    from tncut.circuit import parse_circuit
+    from tncut.network import build_network
+
+    d = os.path.join(ROOT, "tests", "golden", name)
+    with open(os.path.join(d, "circuit.qsim")) as fh:
+        circ = parse_circuit(fh.read(), "qsim_text")
+    with open(os.path.join(d, "order.json")) as fh:
+        doc = json.load(fh)
+    if circ.sha256() != doc["circuit_sha256"]:
+        raise RuntimeError(f"{name}: circuit sha mismatch")
+    opens = doc["open_qubits"]
+    tn = build_network(circ, set(opens), {q: 0 for q in circ.layout.ids if q not in set(opens)})
+    return tn, ordering.doc_to_tree(doc), list(doc["slices"]), doc
+
+
+def time_reference_slices(name, first, max_slices, budget_s):
+    """Wall time of the reference's own ``compute_head_vector(tn, tree,
+    sliced, None, slice_range=(a, a+1), precision="single", mode="fixed")``
+    (engine.py:242-310), one real slice per call, until ``max_slices`` calls
+    or until the next call would overrun ``budget_s``.  No extrapolation:
+    returns the per-slice wall times actually measured."""
+    from tncut import engine
+
+    tn, tree, sliced, doc = reference_workload(name)
+    times = []
+    t_all = time.perf_counter()
+    while len(times) < max_slices:
+        spent = time.perf_counter() - t_all
+        if times and spent + max(times) > budget_s:
+            break
+        a = first + len(times)
+        t0 = time.perf_counter()
+        engine.compute_head_vector(tn, tree, sliced, None, slice_range=(a, a + 1),
+                                   precision="single", mode="fixed")
+        times.append(time.perf_counter() - t0)
+    return times
+
+
+def reference_cpu_baseline(w, budget_s):
+    """cpu_baseline leg of our arm: real reference slices (kind "reference")."""
+    ref, why = import_reference()
+    if ref is None:
+        return {"unavailable": f"reference not importable: {why}"}
+    times = time_reference_slices(WORKLOAD, 0, 1, budget_s)
+    s = float(sum(times))
+    return {"value": len(times) / s, "unit": "slices/s", "cores": HOST_CORES, "kind": "reference",
+            "sample": f"{len(times)} full C4 head slice(s) [0,{len(times)}) through the unmodified "
+                      f"reference engine (baseline/_ref tncut.engine.compute_head_vector, "
+                      f"precision=single, mode=fixed), OPENBLAS_NUM_THREADS={os.environ.get('OPENBLAS_NUM_THREADS')}; "
+                      f"{s:.1f} s measured, no extrapolation",
+            "s_per_slice": s / len(times), "tflops": len(times) * 8.0 * w.tc_per_slice / s / 1e12}
+
+
 def run_reference(args):
-    world, rank, local, dist = setup_dist(args)
+    """--impl reference: the reference's CPU engine on this box's host cores.
+
+    A C4 slice is ~70-110 s of OpenBLAS on 16 cores, so K full slices do not
+    fit the driver's step budget.  Each timed step is ONE real reference
+    slice; steps run until K or until --ref-budget-s would be exceeded, and
+    the line reports the number actually timed (``steps``) beside the
+    requested K.  Warm-up steps are C1 head slices through the same engine
+    (imports, numba JIT, OpenBLAS thread pool), not timed."""
+    world = int(os.environ.get("WORLD_SIZE", "1")) if "WORLD_SIZE" in os.environ else args.gpus
+    rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    from paper_2103_03074_b200.workloads import load_workload
-    from oracle.cpu_sample import time_head_slice
+    base = {"metric": METRIC, "impl": "reference"}
+    ref, why = import_reference()
+    if ref is None:
+        print(json.dumps({**base, "unavailable": f"reference not importable from baseline/_ref: {why}"}),
+              flush=True)
+        return
+    from tncut import engine
 
-    w = load_workload(args.workload)
-    for _ in range(args.warmup):
-        time_head_slice(w.tn, w.tree, w.sliced, step_cap_s=0.5)
-    ests = []
+    from paper_2103_03074_b200.workloads import load_workload
+
+    w = load_workload(args.workload)  # tc_per_slice / n_e bookkeeping only
+    tn1, tree1, sl1, _ = reference_workload("c1")
+    for s in range(args.warmup):
+        engine.compute_head_vector(tn1, tree1, sl1, None, slice_range=(s % 16, s % 16 + 1),
+                                   precision="single", mode="fixed")
     t0 = time.perf_counter()
-    for _ in range(args.steps):
-        est, wall, sample = time_head_slice(w.tn, w.tree, w.sliced)
-        ests.append(est)
-    est = float(np.mean(ests))
-    v = args.slices / (args.slices * est)
-    line = {"metric": METRIC, "value": v, "unit": "slices/s", "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": est * 1e3, "higher_is_better": True,
+    times = time_reference_slices(args.workload, 0, args.steps, args.ref_budget_s)
+    wall = time.perf_counter() - t0
+    total = float(sum(times))
+    v = len(times) / total
+    sample = (f"{len(times)} full {args.workload.upper()} head slices [0,{len(times)}) of the reference "
+              f"plan, one compute_head_vector(slice_range=(a,a+1), precision='single', mode='fixed') "
+              f"call each (unmodified tncut from baseline/_ref), OPENBLAS_NUM_THREADS="
+              f"{os.environ.get('OPENBLAS_NUM_THREADS')}; no extrapolation")
+    line = {**base, "value": v, "unit": "slices/s", "n_gpus": world, "steps": len(times),
+            "requested_steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": total / len(times) * 1e3, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "c64 (numpy/OpenBLAS cgemm)",
-            "data": "synthetic", "impl": "reference",
-            "config": {"workload": "C4: Sycamore-53 m=20, 2^20 correlated bitstrings, target space 2^30",
-                       "parallelism": "host CPU"},
+            "data": "synthetic (Sycamore-layout random gates, seed 0; reference plan frozen in tests/golden/c4)",
+            "config": {"workload": f"{args.workload.upper()}: Sycamore-53 m=20, 2^20 correlated bitstrings, "
+                                   f"target space 2^{w.target_space}, n_e={w.n_e}",
+                       "parallelism": "host CPU (rank 0 only)"},
             "contraction_tflops": v * 8.0 * w.tc_per_slice / 1e12,
-            "cpu_baseline": {"value": v, "unit": "slices/s", "cores": HOST_CORES, "kind": "port",
+            "per_slice_s": times,
+            "steps_note": (f"each step is one full reference slice; {len(times)} of the requested "
+                           f"{args.steps} fit the {args.ref_budget_s:.0f} s budget"
+                           if len(times) < args.steps else "all requested steps timed"),
+            "warmup_note": "warm-up steps are C1 head slices through the same reference engine",
+            "cpu_baseline": {"value": v, "unit": "slices/s", "cores": HOST_CORES, "kind": "reference",
                              "sample": sample},
             "e2e": {"value": v, "unit": "slices/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
-            "sampled_cpu_s": time.perf_counter() - t0}
+            "timed_wall_s": wall}
     print(json.dumps(line), flush=True)
 
 
@@ -727,6 +939,12 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--slices", type=int, default=2, help="head slices per step per GPU")
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--dry-run", action="store_true",
+                    help="launcher/rendezvous/collective plumbing only (gloo, no kernels): CPU tests")
+    ap.add_argument("--allow-knobs", action="store_true",
+                    help="run with TNB_* executor knobs set (the line is marked diagnostic)")
+    ap.add_argument("--ref-budget-s", type=float, default=float(os.environ.get("TNB_REF_BUDGET_S", "420")),
+                    help="wall budget of the reference arm's timed slices (each ~70-110 s at C4)")
     ap.add_argument("--workload", default=WORKLOAD)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
@@ -742,9 +960,22 @@ def main():
     ap.add_argument("--batch-s1", type=int, default=4,
                     help="also time 2^b closed-bit assignments per head pass (reported separately)")
     args = ap.parse_args()
-    if args.impl == "reference":
+    if args.gpus < 1:
+        raise SystemExit("--gpus must be >= 1")
+    if args.impl == "ours" and args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        if os.environ.get("TNB_SHARE_DEVICE") != "1" and not args.dry_run:
+            import torch
+
+            n_dev = torch.cuda.device_count()
+            if n_dev < args.gpus:
+                raise SystemExit(f"bench: --gpus {args.gpus} but only {n_dev} visible CUDA device(s)")
+        sys.exit(spawn_ranks(args.gpus, sys.argv[1:]))
+    if args.dry_run:
+        run_dry(args)
+    elif args.impl == "reference":
         run_reference(args)
     else:
+        args.knobs = refuse_diagnostics(args.allow_knobs)
         run_ours(args)
 
 

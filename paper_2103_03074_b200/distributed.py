@@ -21,6 +21,7 @@ the defaults run libtnb on the rank's GPU.
 from __future__ import annotations
 
 import dataclasses
+import os
 
 import numpy as np
 
@@ -73,6 +74,43 @@ def _device_add(x, y):
     return out
 
 
+def rank_device() -> int:
+    """This rank's GPU: torch's current device, or LOCAL_RANK when the caller
+    left the current device at 0 (torchrun starts every rank there); the
+    choice is made current so torch, NCCL and libtnb all use it."""
+    import torch
+
+    cur = torch.cuda.current_device()
+    lr = os.environ.get("LOCAL_RANK")
+    if lr is not None and cur == 0 and 0 < int(lr) < torch.cuda.device_count():
+        cur = int(lr)
+        torch.cuda.set_device(cur)
+    return cur
+
+
+def _tdtype(precision):
+    import torch
+
+    return torch.complex64 if precision == "single" else torch.complex128
+
+
+def _all_gather(flat, world, group):
+    """all_gather of equal-size tensors.  NCCL gathers device buffers in
+    place; gloo has no CUDA all_gather, so (gloo test runs only) the gather
+    goes through host copies and the parts return to the device."""
+    import torch
+    import torch.distributed as dist
+
+    if flat.is_cuda and dist.get_backend(group) == "gloo":
+        host = flat.cpu()
+        bufs = [torch.empty_like(host) for _ in range(world)]
+        dist.all_gather(bufs, host, group=group)
+        return [b.to(flat.device) for b in bufs]
+    bufs = [torch.empty_like(flat) for _ in range(world)]
+    dist.all_gather(bufs, flat, group=group)
+    return bufs
+
+
 def _rank_world(group):
     import torch.distributed as dist
 
@@ -92,18 +130,20 @@ def sharded_head_vector(tn, tree, sliced_indices, s1, slice_range=None, precisio
     a, b = slice_range if slice_range is not None else (0, 1 << n_e)
     lo, hi = aligned_ranges(a, b, world)[rank]
     if partial_fn is None:
-        hv = engine.compute_head_vector(tn, tree, sliced_indices, s1, slice_range=(lo, hi),
-                                        precision=precision, mode=mode)
-        local = torch.from_numpy(hv.data).to(torch.device("cuda", torch.cuda.current_device()))
-        template = hv
+        # head partial stays on this rank's device (no host round trip)
+        dev = rank_device()
+        n_c = len(engine._split(tn, tree)[4])
+        local = torch.empty(1 << n_c, dtype=_tdtype(precision), device=torch.device("cuda", dev))
+        template = engine.head_vector_to_device(tn, tree, sliced_indices, s1, local,
+                                                slice_range=(lo, hi), precision=precision,
+                                                mode=mode, device=dev)
         add = add or _device_add
     else:
         local, template = partial_fn(lo, hi)
         add = add or _torch_add
     flat = torch.view_as_real(local).reshape(-1)
     if mode == "fixed":
-        bufs = [torch.empty_like(flat) for _ in range(world)]
-        dist.all_gather(bufs, flat, group=group)
+        bufs = _all_gather(flat, world, group)
         parts = [torch.view_as_complex(x.reshape(-1, 2)) for x in bufs]
         total = tree_combine(parts, add)
     else:
@@ -126,16 +166,25 @@ def sharded_amplitudes(tn, tree, sliced_indices, s1, slice_range=None, precision
     a, b = slice_range if slice_range is not None else (0, 1 << n_e)
     lo, hi = aligned_ranges(a, b, world)[rank]
     if partial_fn is None:
-        hv = engine.compute_head_vector(tn, tree, sliced_indices, s1, slice_range=(lo, hi),
-                                        precision=precision, mode=mode)
-        tab = engine.tail_amplitudes_unchecked(tn, tree, hv, precision=precision)
-        local = torch.from_numpy(tab.amplitudes).to(torch.device("cuda", torch.cuda.current_device()))
+        # head -> tail -> all-reduce on the device; one D2H of the result
+        dev = rank_device()
+        cuda = torch.device("cuda", dev)
+        n_c = len(engine._split(tn, tree)[4])
+        n2 = len(tn.open_output_indices)
+        head_dev = torch.empty(1 << n_c, dtype=_tdtype(precision), device=cuda)
+        hv = engine.head_vector_to_device(tn, tree, sliced_indices, s1, head_dev,
+                                          slice_range=(lo, hi), precision=precision,
+                                          mode=mode, device=dev)
+        local = torch.empty(1 << n2, dtype=_tdtype(precision), device=cuda)
+        tab = engine.tail_amplitudes_to_device(tn, tree, hv, head_dev, local,
+                                               precision=precision, device=dev)
     else:
         local, tab = partial_fn(lo, hi)
     flat = torch.view_as_real(local).reshape(-1)
     dist.all_reduce(flat, group=group)
     amps = torch.view_as_complex(flat.reshape(-1, 2)).cpu().numpy()
-    return dataclasses.replace(tab, amplitudes=amps.astype(np.asarray(tab.amplitudes).dtype))
+    want = np.complex64 if precision == "single" else np.complex128
+    return dataclasses.replace(tab, amplitudes=amps.astype(want, copy=False))
 
 
 class NcclComm:

@@ -215,14 +215,18 @@ class Program:
         with self.lock:
             self._update_leaves(leaves)
 
-    def run(self, leaves, a: int, b: int, mode: str = "fixed", out=None):
-        """Upload ``leaves`` and run [a, b) as ONE critical section: programs
-        are cached per topology and shared between threads (the reference's
-        ``cli run --threads`` fans compute_head_vector out over disjoint
-        ranges, cli.py:367-380), so two callers with different s1 must not
-        interleave their uploads with each other's runs."""
+    def run(self, leaves, a: int, b: int, mode: str = "fixed", out=None, device_leaves=None):
+        """Upload ``leaves`` (and bind ``device_leaves`` {pos: device ptr}) and
+        run [a, b) as ONE critical section: programs are cached per topology
+        and shared between threads (the reference's ``cli run --threads``
+        fans compute_head_vector out over disjoint ranges, cli.py:367-380),
+        so two callers with different s1 must not interleave their uploads
+        with each other's runs."""
         with self.lock:
             self._update_leaves(leaves)
+            for pos, ptr in (device_leaves or {}).items():
+                _lib.check(self.lib.tnb_program_set_leaf_device(self.handle, pos, C.c_void_p(ptr)))
+                self._leaf_data[pos] = None
             return self._run_range(a, b, mode, out)
 
     def _update_leaves(self, leaves) -> None:
@@ -418,7 +422,33 @@ def head_program(tn, tree, sliced_indices, precision="single", device=None, flag
 def compute_head_vector(tn, tree, sliced_indices, s1, slice_range=None, precision="double",
                         mode="fixed", stats=None, device=None) -> HeadVector:
     """Sum of head contractions over a slice range (engine.py:242-310)."""
-    if _slice_batch and precision == "single" and tree.first_cut is not None:
+    return _head(tn, tree, sliced_indices, s1, slice_range, precision, mode, stats, device, None)
+
+
+def head_vector_to_device(tn, tree, sliced_indices, s1, out, slice_range=None,
+                          precision="single", mode="fixed", stats=None, device=None) -> HeadVector:
+    """``compute_head_vector`` whose 2^n_c result stays in device memory: it is
+    written to ``out`` (a caller-owned contiguous torch CUDA tensor of the
+    precision's complex dtype on ``device``; the call returns after the device
+    finished).  The returned HeadVector carries
+    the metadata with ``data=None``.  Used by the sharded (multi-GPU) path so
+    head -> tail -> all-reduce never round-trips through the host."""
+    _check_out(out, precision)
+    return _head(tn, tree, sliced_indices, s1, slice_range, precision, mode, stats, device,
+                 out, batch_ok=False)
+
+
+def _check_out(t, precision):
+    import torch
+
+    want = torch.complex64 if precision == "single" else torch.complex128
+    if not (t.is_cuda and t.is_contiguous() and t.dtype == want):
+        raise ValueError(f"device output must be a contiguous CUDA {want} tensor")
+
+
+def _head(tn, tree, sliced_indices, s1, slice_range, precision, mode, stats, device, out_dev,
+          batch_ok=True) -> HeadVector:
+    if batch_ok and _slice_batch and precision == "single" and tree.first_cut is not None:
         n_all = 1 << len(sliced_indices)
         a0, b0 = slice_range if slice_range is not None else (0, n_all)
         k = min(_slice_batch, len(sliced_indices))
@@ -461,12 +491,24 @@ def compute_head_vector(tn, tree, sliced_indices, s1, slice_range=None, precisio
     if not head_leaves:
         # degenerate head (engine.py:282-283): every slice contributes ones(1)
         data = _degenerate_sum(b - a, dtype, mode)
+        if out_dev is not None:
+            import torch
+
+            out_dev.copy_(torch.from_numpy(data))
+            data = None
     else:
         run_steps = _exec_head_steps(tn, tree, head_leaves, head_steps, sliced_indices)
         entries = _leaf_entries(tn, head_leaves)
         prog = get_program(entries, _steps_tuples(run_steps), sliced_indices, sorted(cut),
                            precision, device, upload=False)
-        data = prog.run(entries, a, b, mode)
+        if out_dev is not None and out_dev.numel() != prog.info.out_elems:
+            raise ShapeMismatch(f"device output holds {out_dev.numel()} elements, "
+                                f"the head vector {prog.info.out_elems}")
+        if out_dev is not None:
+            import torch
+
+            torch.cuda.synchronize(out_dev.device)  # the tensor's producers (torch streams)
+        data = prog.run(entries, a, b, mode, out=None if out_dev is None else out_dev.data_ptr())
         if stats is not None:
             sets = {nid: tn.nodes[nid].indices for nid in head_leaves}
             mults, _ = step_mults(sets, head_steps, frozenset(sliced_indices))
@@ -574,6 +616,38 @@ def _tail(tn, tree, head, space_cap, precision, stats, device):
     prog = get_program(entries, steps, [], out_order, precision, device, upload=False)
     amps = prog.run(entries, 0, 1, "fixed")
     return _make_table(tn, tree, head, amps.astype(dtype, copy=False), open_qubits, precision)
+
+
+def tail_amplitudes_to_device(tn, tree, head: HeadVector, head_dev, out,
+                              precision="single", device=None) -> AmplitudeTable:
+    """Head-absorbed tail of a head vector that is already in device memory
+    (``head_dev``: torch CUDA tensor, 2^n_c elements of the precision's complex
+    dtype); the 2^n2 amplitudes (s2 order) are written to the torch CUDA
+    tensor ``out``.
+    Leaf upload, head-pointer binding and run are one critical section on the
+    cached program.  Returns the table's metadata with ``amplitudes=None``."""
+    tn = tn.repin(head.s1)
+    _, _, tail_leaves, _, cut = _split(tn, tree)
+    if sorted(cut) != list(head.cut_order):
+        raise ProvenanceMismatch("cut indices differ from the head vector's")
+    open_qubits = sorted(tn.open_output_indices)
+    if not tail_leaves:
+        raise ShapeMismatch("tail_amplitudes_to_device needs a non-empty tail")
+    leaves, hid, steps = tail_plan(tn, tree, head.cut_order)
+    entries = _leaf_entries(tn, leaves)
+    entries.append((hid, list(head.cut_order), np.zeros(1 << len(head.cut_order))))
+    out_order = [tn.open_output_indices[q] for q in open_qubits]
+    _check_out(head_dev, precision)
+    _check_out(out, precision)
+    if head_dev.numel() != 1 << len(head.cut_order) or out.numel() != 1 << len(open_qubits):
+        raise ShapeMismatch("device head / amplitude tensors have the wrong size")
+    prog = get_program(entries, steps, [], out_order, precision, device, upload=False)
+    import torch
+
+    torch.cuda.synchronize(out.device)
+    prog.run(entries[:-1], 0, 1, "fixed", out=out.data_ptr(),
+             device_leaves={len(entries) - 1: head_dev.data_ptr()})
+    return _make_table(tn, tree, head, None, open_qubits, precision)
 
 
 def _make_table(tn, tree, head, amplitudes, open_qubits, precision):

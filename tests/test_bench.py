@@ -1,0 +1,72 @@
+"""bench.py's launcher: ``--gpus N`` without torchrun spawns N ranks
+(RANK/LOCAL_RANK/WORLD_SIZE/MASTER_* like torchrun) and rank 0 prints one
+line with the communicator size and the device of every rank."""
+
+from __future__ import annotations
+
+import json
+import os
+import subprocess
+import sys
+
+import pytest
+
+from conftest import ROOT
+
+BENCH = os.path.join(ROOT, "bench.py")
+
+
+def _run(args, env_extra, timeout):
+    env = {k: v for k, v in os.environ.items() if not k.startswith("TNB_")}
+    for k in ("WORLD_SIZE", "RANK", "LOCAL_RANK", "MASTER_ADDR", "MASTER_PORT"):
+        env.pop(k, None)
+    env.update(env_extra)
+    r = subprocess.run([sys.executable, BENCH, *args], capture_output=True, text=True,
+                       timeout=timeout, env=env, cwd=ROOT)
+    assert r.returncode == 0, r.stderr[-3000:]
+    lines = [ln for ln in r.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1, r.stdout[-3000:]  # rank 0 alone prints
+    return json.loads(lines[0])
+
+
+def test_gpus_flag_spawns_ranks_dry_run():
+    line = _run(["--gpus", "2", "--dry-run", "--steps", "2", "--warmup", "1", "--slices", "2"],
+                {"TNB_SHARE_DEVICE": "1"}, 180)
+    assert line["n_gpus"] == 2
+    assert line["communicator"] == {"backend": "gloo", "size": 2}
+    assert [r["rank"] for r in line["ranks"]] == [0, 1]
+    assert line["slice_ranges"] == [[0, 6], [6, 12]]  # disjoint per-rank ranges
+    assert line["allreduce_sum"] == 3.0
+
+
+def test_bench_refuses_executor_knobs():
+    env = {k: v for k, v in os.environ.items() if not k.startswith("TNB_")}
+    env["TNB_CHUNK_KB"] = "0"
+    r = subprocess.run([sys.executable, BENCH, "--steps", "1"], capture_output=True, text=True,
+                       timeout=120, env=env, cwd=ROOT)
+    assert r.returncode != 0 and "refusing" in r.stderr
+
+
+def test_more_gpus_than_devices_fails():
+    import torch
+
+    if torch.cuda.device_count() >= 64:
+        pytest.skip("box has 64 GPUs")
+    env = {k: v for k, v in os.environ.items() if not k.startswith("TNB_")}
+    r = subprocess.run([sys.executable, BENCH, "--gpus", "64", "--steps", "1"], capture_output=True,
+                       text=True, timeout=120, env=env, cwd=ROOT)
+    assert r.returncode != 0 and "visible CUDA device" in r.stderr
+
+
+@pytest.mark.gpu
+def test_bench_two_ranks_share_one_gpu(gpu):
+    """The full bench step on 2 ranks (gloo, both on device 0: the 1-GPU box
+    can not host 2 NCCL ranks): head -> tail -> all-reduce per rank, max
+    over ranks, rank 0's line."""
+    line = _run(["--gpus", "2", "--steps", "1", "--warmup", "1", "--slices", "1", "--no-cpu",
+                 "--no-e2e", "--reuse", "0", "--opt-plan", "0", "--reordered", "0",
+                 "--batch-slices", "0", "--batch-s1", "0"],
+                {"TNB_SHARE_DEVICE": "1", "TNB_DIST_BACKEND": "gloo"}, 900)
+    assert line["n_gpus"] == 2 and line["communicator"]["size"] == 2
+    assert line["gpus_active"] == 1 and line["value"] > 0
+    assert line["gpu_launches"] > 0

@@ -52,3 +52,61 @@ def test_c_abi_nccl_allreduce_single_rank(gpu):
     comm.allreduce_sum(y, stream=torch.cuda.current_stream())
     assert torch.equal(y, yr)
     comm.close()
+
+
+def _sharded_worker(rank, world, port, out_q):
+    import os
+    import sys
+
+    from conftest import ROOT
+
+    sys.path.insert(0, ROOT)
+    os.environ["LOCAL_RANK"] = str(rank)
+    import torch
+    import torch.distributed as dist
+
+    from paper_2103_03074_b200 import distributed as D
+    from paper_2103_03074_b200.workloads import load_workload
+
+    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=world)
+    w = load_workload("s8")
+    hv = D.sharded_head_vector(w.tn, w.tree, w.sliced, None, slice_range=(0, 8), mode="fixed")
+    tab = D.sharded_amplitudes(w.tn, w.tree, w.sliced, None, slice_range=(0, 8), mode="fixed")
+    out_q.put((rank, torch.cuda.current_device(), hv.data, hv.slice_range, tab.amplitudes))
+    dist.destroy_process_group()
+
+
+def test_sharded_device_path_two_ranks_one_gpu(gpu, workloads):
+    """distributed.sharded_* on their default (device-resident) path, 2 ranks
+    sharing the box's GPU over gloo: head -> tail -> collective never leave
+    the device until the final result; fixed mode equals the 1-process
+    result bit-exactly, amplitudes within fp32 rounding."""
+    import socket
+
+    import torch.multiprocessing as mp
+
+    from conftest import rel_l2
+
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_sharded_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=300) for _ in range(2)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    w = workloads("s8")
+    full = tnb.compute_head_vector(w.tn, w.tree, w.sliced, None, slice_range=(0, 8),
+                                   precision="single")
+    amps = tnb.tail_amplitudes_unchecked(w.tn, w.tree, full, precision="single").amplitudes
+    for rank, dev, data, rng, a in res:
+        assert rng == (0, 8) and dev == 0
+        assert np.array_equal(data, full.data), f"rank {rank}: fixed-mode head not bit-identical"
+        e = rel_l2(a, amps)
+        print(f"rank {rank}: sharded amplitudes rel L2 {e:.2e}")
+        assert e < 1e-5
