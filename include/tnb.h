@@ -42,7 +42,7 @@
 extern "C" {
 #endif
 
-#define TNB_ABI_VERSION 1
+#define TNB_ABI_VERSION 2
 
 typedef enum {
   TNB_OK = 0,
@@ -115,6 +115,10 @@ typedef struct {
   int64_t gemm_launches;
   double gemm_flops;            /* algorithmic complex FLOPs executed on tcgen05    */
   int64_t steps_reused;         /* steps skipped by TNB_FLAG_REUSE_SLICES           */
+  int64_t scale_redos;          /* fused producers re-run by the fp16 scale guard:
+                                   the a-priori bound 2K max|A| max|B| was more than
+                                   TNB_SCALE_GUARD_BITS (default 18) binary orders
+                                   above the result's max (always counted)           */
 } tnb_timing;
 
 int tnb_abi_version(void);

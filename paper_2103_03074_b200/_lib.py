@@ -52,7 +52,7 @@ class Timing(C.Structure):
     _fields_ = [
         ("total_ms", f64), ("gemm_ms", f64), ("convert_ms", f64), ("simt_ms", f64),
         ("other_ms", f64), ("launches", i64), ("gemm_launches", i64), ("gemm_flops", f64),
-        ("steps_reused", i64),
+        ("steps_reused", i64), ("scale_redos", i64),
     ]
 
 
@@ -101,7 +101,7 @@ def load() -> C.CDLL:
             fn = getattr(lib, name)
             fn.restype = res
             fn.argtypes = args
-        if lib.tnb_abi_version() != 1:
+        if lib.tnb_abi_version() != 2:
             raise ImportError("libtnb.so ABI version mismatch")
         _lib = lib
     return _lib

@@ -66,7 +66,25 @@ def build(force: bool = False, verbose: bool = False) -> str:
     from .treeopt import build as build_plan
 
     build_plan(force=force)
+    build_io(force=force)
     return LIB
+
+
+IO_SRC = os.path.join(CSRC, "tsv_format.cpp")
+IO_LIB = os.path.join(PKG, "libtnbio.so")
+
+
+def build_io(force: bool = False) -> str:
+    """g++ build of libtnbio.so: the host TSV row formatter (io.py)."""
+    if force or not os.path.exists(IO_LIB) or os.path.getmtime(IO_SRC) > os.path.getmtime(IO_LIB):
+        tmp = IO_LIB + ".tmp"
+        cmd = ["g++", "-O2", "-std=c++17", "-fPIC", "-shared", "-pthread", "-Wall",
+               "-ffp-contract=off", "-fno-builtin", IO_SRC, "-o", tmp]
+        r = subprocess.run(cmd, capture_output=True, text=True)
+        if r.returncode != 0:
+            raise RuntimeError(f"g++ failed ({' '.join(cmd)}):\n{r.stdout}\n{r.stderr}")
+        os.replace(tmp, IO_LIB)
+    return IO_LIB
 
 
 if __name__ == "__main__":

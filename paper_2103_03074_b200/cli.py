@@ -36,7 +36,9 @@ def bind(slicer: bool | None = None) -> dict:
     pipeline modules (they import them by name) to this package's; with
     ``slicer`` (default: env TNB_CLI_SLICER=b200) also ``tncut slice``'s
     ``select_slices`` to the plan co-optimiser.
-    Returns {module.name: previous object} so callers can restore."""
+    Worker threads of ``tncut run --threads`` are spread over the visible
+    GPUs round-robin.  Returns {module.name: previous object} so callers can
+    restore."""
     import os
 
     import tncut.cli as cli
@@ -44,7 +46,10 @@ def bind(slicer: bool | None = None) -> dict:
 
     from . import analytics, engine
 
-    previous = {}
+    previous = {"paper_2103_03074_b200.engine._thread_devices": engine._thread_devices}
+    # `tncut run --threads T` (cli.py:367-380) fans ranges out over T threads:
+    # each thread is bound to the next GPU round-robin (engine.set_thread_devices)
+    engine.set_thread_devices(True)
     if slicer is None:
         slicer = os.environ.get("TNB_CLI_SLICER", "") == "b200"
     if slicer:

@@ -344,9 +344,12 @@ gemm_f16x3_kernel(const __grid_constant__ CUtensorMap tm_ahi, const __grid_const
                   float* __restrict__ C, int M, int Np, int Kp, int splits, int k_per_split,
                   int chunk_kb, int group_m, const ScaleSrc scale_rows, const ScaleSrc scale_cols,
                   unsigned int* __restrict__ max_out, unsigned int* __restrict__ progress,
-                  int pace_slack, const __grid_constant__ FuseOut fo, int exp_skip, int epi_spin) {
+                  int pace_slack, const __grid_constant__ FuseOut fo, int epi_spin) {
   using CF = Cfg<CG, NB>;
   constexpr int STAGES = CF::STAGES;
+  // gated re-run of a fused producer (fp16 scale guard): nothing to do unless
+  // the guard fired; uniform over the grid, before any barrier or TMEM use
+  if (fo.gate != nullptr && __ldcg(fo.gate) == 0u) return;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + STAGES * CF::STAGE_BYTES);
@@ -430,22 +433,13 @@ gemm_f16x3_kernel(const __grid_constant__ CUtensorMap tm_ahi, const __grid_const
           if (epi_spin & 4) mbar_wait(&empty_bar[stage], phase ^ 1);
           else mbar_wait_sleep(&empty_bar[stage], phase ^ 1);
           uint8_t* st = smem + stage * CF::STAGE_BYTES;
-          // exp_skip (diagnostic only, wrong results): 1 = skip B loads, 2 = skip A loads
           const int kbk = k / BK;
-          // 3 = skip A on odd K blocks (half the A traffic: the bound of sharing A)
-          const bool skip_a = exp_skip == 2 || (exp_skip == 3 && (kbk & 1));
-          const bool skip_b = exp_skip == 1 || (exp_skip == 4 && (kbk & 1));  // 4: half the B traffic
-          const uint32_t bytes = (skip_a ? 0 : 2 * A_TILE) + (skip_b ? 0 : 2 * CF::B_TILE);
-          if (leader) mbar_arrive_expect_tx(&full_bar[stage], CG * bytes);
+          if (leader) mbar_arrive_expect_tx(&full_bar[stage], CG * (2 * A_TILE + 2 * CF::B_TILE));
           else mbar_arrive_remote(&full_bar[stage], 0);
-          if (!skip_a) {
-            tma_load_tile<CG>(st, &tm_ahi, &full_bar[stage], m0, kbk);
-            tma_load_tile<CG>(st + A_TILE, &tm_alo, &full_bar[stage], m0, kbk);
-          }
-          if (!skip_b) {
-            tma_load_tile<CG>(st + 2 * A_TILE, &tm_bhi, &full_bar[stage], n0, kbk);
-            tma_load_tile<CG>(st + 2 * A_TILE + CF::B_TILE, &tm_blo, &full_bar[stage], n0, kbk);
-          }
+          tma_load_tile<CG>(st, &tm_ahi, &full_bar[stage], m0, kbk);
+          tma_load_tile<CG>(st + A_TILE, &tm_alo, &full_bar[stage], m0, kbk);
+          tma_load_tile<CG>(st + 2 * A_TILE, &tm_bhi, &full_bar[stage], n0, kbk);
+          tma_load_tile<CG>(st + 2 * A_TILE + CF::B_TILE, &tm_blo, &full_bar[stage], n0, kbk);
         }
         __syncwarp();
         if (++stage == STAGES) { stage = 0; phase ^= 1; }
@@ -543,9 +537,7 @@ gemm_f16x3_kernel(const __grid_constant__ CUtensorMap tm_ahi, const __grid_const
 #pragma unroll
         for (int j = 0; j < EPI_COLS; ++j) acc[j] *= alpha;
       }
-      if (exp_skip == 6) {
-        // diagnostic: no result stores (timing only)
-      } else if (fo.mode != 0) {
+      if (fo.mode != 0) {
         // fused staging: write the consumer's fp16 operand directly
         const int nvalid = min(EPI_COLS / 2, (Np - col0) >> 1);
         if (nvalid > 0) {  // warp-uniform; every row of a 32-row group exists (M >= 128, 2^k)
@@ -744,8 +736,10 @@ void tc_plan_gemm(TcGemmPlan* p, const __half* Ahi, const __half* Alo, const __h
   p->scale_rows = scale_rows;
   p->scale_cols = scale_cols;
   p->max_out = max_out;
+  // promotion chunk: always on (the tensor cores' long-K accumulation error is
+  // ~15x IEEE fp32, profiles/r1/gemm_accuracy_vs_promotion_chunk.txt)
   p->chunk_kb = env_int("TNB_CHUNK_KB", kDefaultChunkKb);
-  if (p->chunk_kb <= 0) p->chunk_kb = 1 << 30;  // no promotion: whole K in TMEM
+  if (p->chunk_kb <= 0 || p->chunk_kb > 64) p->chunk_kb = kDefaultChunkKb;
   p->group_m = env_int("TNB_GROUP_M", GROUP_M);
   if (p->group_m <= 0) p->group_m = 1 << 30;
   // soft pacing keeps long-K tiles inside the L2 window (top C4 GEMM: 75 vs
@@ -784,7 +778,7 @@ void launch_cg(const TcGemmPlan* p, cudaStream_t s) {
   TNB_CUDA(cudaLaunchKernelEx(&cfg, kern, maps[0], maps[1], maps[2], maps[3], p->C, (int)p->M,
                               (int)p->Np, (int)p->Kp, p->splits, (int)p->k_per_split, p->chunk_kb,
                               p->group_m, p->scale_rows, p->scale_cols, p->max_out, p->progress,
-                              p->pace_slack, p->fuse, env_int("TNB_EXP_SKIP", 0), p->epi_spin));
+                              p->pace_slack, p->fuse, p->epi_spin));
 }
 
 void tc_launch_gemm(const TcGemmPlan* p, cudaStream_t s) {

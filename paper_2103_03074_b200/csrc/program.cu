@@ -131,6 +131,16 @@ struct StepRec {
   FuseOut simt_fuse;                           // SIMT (small-K) producer: fused output map
   int batch = -1;                              // tiled SIMT step launched in Program::batches[batch]
   TcGemmPlan tc;
+  // fp16 scale guard of a fused producer: after it runs, guard_bound (the
+  // a-priori bound it scaled by) is compared with its result's exact max; if
+  // the bound is more than Program::guard_bits binary orders looser, the
+  // gated re-run (tc_redo / simt_redo: same launch, scale = the exact max)
+  // rewrites the operand and the consumer's ScaleSrc follows the guard word
+  bool has_redo = false;
+  ScaleSrc guard_bound;
+  unsigned int* guard = nullptr;
+  TcGemmPlan tc_redo;
+  FuseOut simt_redo;
 };
 
 // bytes of a tensor's storage: complex elements, or the consumer's fp16
@@ -174,6 +184,8 @@ struct Program {
   uint32_t* d_keep = nullptr;
   unsigned int* d_tmax = nullptr;   // per-tensor max|re|,|im| slots (fp32 bits)
   unsigned int* d_progress = nullptr;  // GEMM soft-pacing counters (one per CTA unit)
+  unsigned int* d_guard = nullptr;  // fp16 scale guard words (per tensor slot) + redo counter
+  int guard_bits = 18;              // TNB_SCALE_GUARD_BITS at creation (< 0: guard off)
   std::vector<int> slot;            // tensor -> slot
   int inv_slot_begin = 0, inv_slot_count = 0, var_slot_begin = 0, var_slot_count = 0;
   std::vector<StageTables> stages;  // device views of the TC staging tables
@@ -210,7 +222,8 @@ struct Program {
   ~Program() {
     if (device >= 0) cudaSetDevice(device);
     void* ptrs[] = {d_leaf_pool, d_slice_pool, d_persist, d_arena, d_luts,
-                    d_sl_descs, d_keep, d_tmax, d_acc, d_stage_u32, d_stage_luts, d_progress, d_fuse_luts, d_simt_descs};
+                    d_sl_descs, d_keep, d_tmax, d_acc, d_stage_u32, d_stage_luts, d_progress, d_fuse_luts, d_simt_descs,
+                    d_guard};
     for (void* p : ptrs)
       if (p) cudaFree(p);
     for (auto e : ev_pool) cudaEventDestroy(e);
@@ -454,7 +467,13 @@ void plan_tensor_core_steps(Program* P) {
   // fp16 split scale of a tensor-core operand: its own max when staged, the
   // producer's a-priori bound 2 K max|A| max|B| when the producer's epilogue
   // wrote it (fused); producer and consumer evaluate the same ScaleSrc
-  auto operand_scale = [&](int t) {
+  {
+    const char* e = getenv("TNB_SCALE_GUARD_BITS");
+    P->guard_bits = e ? atoi(e) : 18;
+  }
+  // producer view (the bound alone) and consumer view (bound, or the
+  // result's exact max when the guard fired) of a fused operand's scale
+  auto bound_scale = [&](int t) {
     ScaleSrc sc;
     const TensorRec& r = P->tensors[t];
     if (r.fuse_role != 0) {
@@ -464,6 +483,14 @@ void plan_tensor_core_steps(Program* P) {
       sc.f = (float)(2.0 * (double)p.K);
     } else {
       sc.a = P->d_tmax + P->slot[t];
+    }
+    return sc;
+  };
+  auto operand_scale = [&](int t) {
+    ScaleSrc sc = bound_scale(t);
+    if (P->tensors[t].fuse_role != 0 && P->guard_bits >= 0) {
+      sc.guard = P->d_guard + P->slot[t];
+      sc.own = P->d_tmax + P->slot[t];
     }
     return sc;
   };
@@ -503,7 +530,7 @@ void plan_tensor_core_steps(Program* P) {
     }
     f.hi = (__half2*)P->tensor_ptr(s.out);
     f.lo = f.hi + (as_rows ? c.M * c.K : 2 * c.N * c.K);
-    f.scale = operand_scale(s.out);
+    f.scale = bound_scale(s.out);  // the producer's first run scales by the bound
     fuse_luts.emplace_back();
     build_lut(mvec, &fuse_luts.back());
     fuse_luts.emplace_back();
@@ -604,6 +631,28 @@ void plan_tensor_core_steps(Program* P) {
       FuseOut& f = st.kind == KIND_TC ? st.tc.fuse : st.simt_fuse;
       f.lut_m = P->d_fuse_luts + 2 * e;
       f.lut_n = P->d_fuse_luts + 2 * e + 1;
+    }
+  }
+  // scale-guard re-runs of every fused producer: the same launch, gated on
+  // the guard word, scaling by the result's exact max
+  if (P->guard_bits >= 0) {
+    for (int i = 0; i < n_steps; ++i) {
+      StepRec& st = P->steps[i];
+      FuseOut& f = st.kind == KIND_TC ? st.tc.fuse : st.simt_fuse;
+      if (f.mode == 0) continue;
+      st.has_redo = true;
+      st.guard_bound = f.scale;
+      st.guard = P->d_guard + P->slot[st.out];
+      FuseOut r = f;
+      r.gate = st.guard;
+      r.scale = ScaleSrc{};
+      r.scale.a = P->d_tmax + P->slot[st.out];
+      if (st.kind == KIND_TC) {
+        st.tc_redo = st.tc;
+        st.tc_redo.fuse = r;
+      } else {
+        st.simt_redo = r;
+      }
     }
   }
 
@@ -1094,6 +1143,9 @@ Program* program_create(const tnb_program_desc* d) {
     P->var_slot_count = next - P->var_slot_begin;
     dmalloc((void**)&P->d_tmax, (int64_t)next * 4);
     TNB_CUDA(cudaMemset(P->d_tmax, 0, (size_t)next * 4));
+    // guard words share the slot numbering; the last word counts re-runs
+    dmalloc((void**)&P->d_guard, (int64_t)(next + 1) * 4);
+    TNB_CUDA(cudaMemset(P->d_guard, 0, (size_t)(next + 1) * 4));
   }
   // tensor-core staging tables (tiled permute + split), one per TC operand
   {
@@ -1393,8 +1445,17 @@ void exec_step(Program* P, StepRec& s, int parts) {
                             P->d_luts + s.lut_b, s.lut_e >= 0 ? P->d_luts + s.lut_e : nullptr,
                             P->precision == TNB_SINGLE ? P->d_tmax + P->slot[s.out] : nullptr,
                             s.simt_fuse.mode ? &s.simt_fuse : nullptr, P->stream);
-    C.close(2, e);
     C.launches++;
+    if (s.has_redo) {
+      launch_scale_guard(s.guard_bound, P->d_tmax + P->slot[s.out], s.guard, P->guard_bits,
+                         P->d_guard + P->slot.size(), P->stream);
+      launch_contract_simt<T>((const T*)P->tensor_ptr(s.a), (const T*)P->tensor_ptr(s.b),
+                              (T*)P->tensor_ptr(s.out), s.M, s.N, s.K, P->d_luts + s.lut_a,
+                              P->d_luts + s.lut_b, s.lut_e >= 0 ? P->d_luts + s.lut_e : nullptr,
+                              P->d_tmax + P->slot[s.out], &s.simt_redo, P->stream);
+      C.launches += 2;
+    }
+    C.close(2, e);
     return;
   }
   if constexpr (std::is_same<T, float2>::value) {
@@ -1428,6 +1489,15 @@ void exec_step(Program* P, StepRec& s, int parts) {
       C.launches += 1;
       C.gemm_launches++;
       C.gemm_flops += 8.0 * s.mults;
+      if (s.has_redo) {
+        // guard + gated re-run (exits at once unless the guard fired)
+        e = C.mark(1);
+        launch_scale_guard(s.guard_bound, s.tc.max_out, s.guard, P->guard_bits,
+                           P->d_guard + P->slot.size(), P->stream);
+        tc_launch_gemm(&s.tc_redo, P->stream);
+        C.close(1, e);
+        C.launches += 2;
+      }
     }
     if ((parts & kPost) && s.tc.splits > 1) {
       e = C.mark(1);
@@ -1509,6 +1579,8 @@ void run_range_t(Program* P, uint64_t a, uint64_t b, int mode, void* out, bool o
   static const int graphs_env = env_int("TNB_GRAPHS", 1);
   const bool use_graphs = graphs_env && P->timing != 1 && !P->reuse;
   cudaEvent_t t_start = ctx.mark(-1);
+  unsigned int* redo_count = P->d_guard + P->slot.size();
+  TNB_CUDA(cudaMemsetAsync(redo_count, 0, 4, st));
 
   // hoisted slice-invariant steps (once per leaf-data version)
   if (!P->invariant_valid) {
@@ -1603,6 +1675,8 @@ void run_range_t(Program* P, uint64_t a, uint64_t b, int mode, void* out, bool o
     TNB_CUDA(cudaMemcpyAsync(out, result, (size_t)E * sizeof(T), cudaMemcpyDeviceToHost, st));
   }
   cudaEvent_t t_end = ctx.mark(-1);
+  unsigned int redos = 0;
+  TNB_CUDA(cudaMemcpyAsync(&redos, redo_count, 4, cudaMemcpyDeviceToHost, st));
   TNB_CUDA(cudaStreamSynchronize(st));
   if (std::is_same<T, float2>::value && getenv("TNB_DEBUG_MAX")) {
     // diagnostic: per-step output max vs the a-priori bound 2 K max|A| max|B|
@@ -1634,6 +1708,7 @@ void run_range_t(Program* P, uint64_t a, uint64_t b, int mode, void* out, bool o
   tm.gemm_launches = ctx.gemm_launches;
   tm.gemm_flops = ctx.gemm_flops;
   tm.steps_reused = ctx.reused;
+  tm.scale_redos = redos;
   P->last = tm;
 }
 

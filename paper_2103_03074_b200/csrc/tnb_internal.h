@@ -60,27 +60,42 @@ struct ScaleSrc {
   const unsigned int* a = nullptr;
   const unsigned int* b = nullptr;
   float f = 1.f;  // power of two
+  // runtime guard of a fused operand (consumer side): when *guard != 0 the
+  // producer was re-run with its result's exact max (`own`) as the scale
+  // source because the a-priori bound was looser than the guard threshold
+  const unsigned int* guard = nullptr;
+  const unsigned int* own = nullptr;
 };
 
 #ifdef __CUDACC__
-__device__ __forceinline__ float scale_from_src(const ScaleSrc& s) {
-  const float ma = __uint_as_float(*s.a);
-  if (!(ma > 0.f)) return 1.f;
-  int e;
+// exponent e of the scale source's bound v = frac * 2^e (frac in [0.5, 1));
+// false when the bound is zero (all-zero operand)
+__device__ __forceinline__ bool scale_bound_exp(const unsigned int* pa, const unsigned int* pb,
+                                                float f, int& e) {
+  const float ma = __uint_as_float(*pa);
+  if (!(ma > 0.f)) return false;
   float fr = frexpf(ma, &e);  // ma = fr * 2^e
-  if (s.b != nullptr) {
-    const float mb = __uint_as_float(*s.b);
-    if (!(mb > 0.f)) return 1.f;
+  if (pb != nullptr) {
+    const float mb = __uint_as_float(*pb);
+    if (!(mb > 0.f)) return false;
     int eb, ef, ep;
     const float fb = frexpf(mb, &eb);
-    frexpf(s.f, &ef);            // f = 2^(ef-1)
+    frexpf(f, &ef);              // f = 2^(ef-1)
     fr = frexpf(fr * fb, &ep);   // product of the fractions in [0.25, 1)
     e = e + eb + (ef - 1) + ep;
-  } else if (s.f != 1.f) {
+  } else if (f != 1.f) {
     int ef;
-    frexpf(s.f, &ef);
+    frexpf(f, &ef);
     e += ef - 1;
   }
+  return true;
+}
+
+__device__ __forceinline__ float scale_from_src(const ScaleSrc& s) {
+  int e;
+  const bool own = s.guard != nullptr && *s.guard != 0u;
+  if (!(own ? scale_bound_exp(s.own, nullptr, 1.f, e) : scale_bound_exp(s.a, s.b, s.f, e)))
+    return 1.f;
   int p = 15 - e;
   p = p > 126 ? 126 : (p < -126 ? -126 : p);
   return ldexpf(1.f, p);
@@ -114,6 +129,11 @@ template <typename T>
 void launch_contract_simt(const T* A, const T* B, T* C, int64_t M, int64_t N, int64_t K,
                           const ByteLut* lutA, const ByteLut* lutB, const ByteLut* lutE,
                           unsigned int* max_out, const FuseOut* fuse, cudaStream_t s);
+// fp16 scale guard of a fused operand: *guard = 1 (and ++*count) when the
+// producer's a-priori bound `bound` exceeds its result's exact max `own` by
+// more than `thr_bits` binary orders, else 0 (stream-ordered, one thread)
+void launch_scale_guard(const ScaleSrc& bound, const unsigned int* own, unsigned int* guard,
+                        int thr_bits, unsigned int* count, cudaStream_t s);
 // one step of a batched SIMT launch (contract_simt_batch_kernel)
 struct SimtStepDesc {
   const void* A;
@@ -206,6 +226,7 @@ struct FuseOut {
   const ByteLut* lut_n = nullptr;
   uint32_t dlow[32] = {};
   ScaleSrc scale;                // scale of the written operand
+  const unsigned int* gate = nullptr;  // re-run of a fused producer: run only if *gate != 0
 };
 
 // ---------------------------------------------------------------------------

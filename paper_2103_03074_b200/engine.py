@@ -611,10 +611,34 @@ def _tail(tn, tree, head, space_cap, precision, stats, device):
     leaves, hid, steps = tail_plan(tn, tree, head.cut_order)
     entries = _leaf_entries(tn, leaves)
     entries.append((hid, list(head.cut_order), np.asarray(head.data).reshape(-1)))
-    out_order = [tn.open_output_indices[q] for q in open_qubits]
-    # cache keyed on topology only: the head leaf is re-uploaded when it changes
-    prog = get_program(entries, steps, [], out_order, precision, device, upload=False)
-    amps = prog.run(entries, 0, 1, "fixed")
+    open_ids = [tn.open_output_indices[q] for q in open_qubits]
+    sets = {nid: ix for nid, ix, _ in entries}
+    # blocked fallback (engine.py:348-362): pin the k leading open qubits
+    # (s2 MSBs) when the absorbed tail's largest intermediate exceeds
+    # space_cap, or when its program does not fit in device memory; block j
+    # then fills amplitudes[j << (n2 - k) : (j + 1) << (n2 - k)]
+    kb = 0
+    if space_cap is not None:
+        while kb < n2 and step_mults(sets, steps, frozenset(open_ids[:kb]))[1] > space_cap:
+            kb += 1
+    while True:
+        # cache keyed on topology only: the head leaf is re-uploaded when it changes
+        try:
+            prog = get_program(entries, steps, open_ids[:kb], open_ids[kb:], precision, device,
+                               upload=False)
+            break
+        except RuntimeError as exc:
+            if "out of memory" not in str(exc) or kb >= n2:
+                raise
+            clear_cache()
+            kb += 1
+    if kb == 0:
+        amps = prog.run(entries, 0, 1, "fixed")
+    else:
+        amps = np.empty(1 << n2, dtype=dtype)
+        w = 1 << (n2 - kb)
+        for j in range(1 << kb):
+            amps[j * w:(j + 1) * w] = prog.run(entries, j, j + 1, "fixed")
     return _make_table(tn, tree, head, amps.astype(dtype, copy=False), open_qubits, precision)
 
 

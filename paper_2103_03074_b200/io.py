@@ -12,6 +12,7 @@
 
 from __future__ import annotations
 
+import os
 import struct
 
 import numpy as np
@@ -70,11 +71,6 @@ def read_head_vector(path) -> HeadVector:
                       slice_range=(a, b), mode=mode, sliced_indices=tuple(sl))
 
 
-def _fmt17g(x: np.ndarray) -> list:
-    """Python's f'{v:.17g}' for a float array (exactly what the reference prints)."""
-    return [f"{v:.17g}" for v in x.tolist()]
-
-
 def bitstrings(table) -> np.ndarray:
     """All row bitstrings of an AmplitudeTable (AmplitudeTable.bitstring, engine.py:83-92)."""
     n2 = len(table.open_qubits)
@@ -91,9 +87,41 @@ def bitstrings(table) -> np.ndarray:
     return cols.view(f"S{len(layout)}").reshape(-1)
 
 
-def write_amplitude_tsv(path, table) -> None:
-    """``tncut-amplitudes/1`` TSV (engine.py:464-479), vectorised bitstrings."""
+_iolib = None
+
+
+def _io_lib():
+    global _iolib
+    if _iolib is None:
+        import ctypes as C
+
+        from .build import IO_LIB
+
+        if not os.path.exists(IO_LIB):
+            raise RuntimeError(f"{IO_LIB} not built (python -m paper_2103_03074_b200.build)")
+        lib = C.CDLL(IO_LIB)
+        lib.tnbio_row_cap.restype = C.c_int64
+        lib.tnbio_row_cap.argtypes = [C.c_int32]
+        lib.tnbio_format_rows.restype = C.c_int64
+        lib.tnbio_format_rows.argtypes = [C.c_void_p, C.c_int32, C.c_void_p, C.c_int32, C.c_int64,
+                                          C.c_void_p, C.c_int64, C.c_int32]
+        _iolib = lib
+    return _iolib
+
+
+ROWS_PER_CHUNK = 1 << 16
+
+
+def write_amplitude_tsv(path, table, threads: int = 0) -> None:
+    """``tncut-amplitudes/1`` TSV (engine.py:464-479), byte-identical to the
+    reference writer: bitstrings vectorised in numpy, the three number
+    columns formatted by libtnbio (csrc/tsv_format.cpp) on all host threads,
+    2^16 rows per chunk."""
     amps = np.asarray(table.amplitudes)
+    single = amps.dtype == np.complex64
+    if not single:
+        amps = amps.astype(np.complex128, copy=False)
+    amps = np.ascontiguousarray(amps).reshape(-1)
     s1_str = "".join(str(table.s1[q]) for q in sorted(table.s1)) or "-"
     opens = ",".join(str(q) for q in table.open_qubits) or "-"
     header = (f"# {TSV_SCHEMA} circuit_sha256={table.circuit_sha256} "
@@ -101,14 +129,18 @@ def write_amplitude_tsv(path, table) -> None:
               f"open_qubits={opens} n={len(table.layout_ids)} "
               f"precision={table.precision} reduction={table.mode}\n"
               "bitstring\tamp_re\tamp_im\tprobability\n")
-    # rows() yields complex(amp) and float(abs(amp) ** 2) with numpy SCALAR
-    # arithmetic (engine.py:94-96); numpy's scalar abs/pow differ from the
-    # array ufuncs in the last bit, so the probability column keeps the scalar path
-    c128 = amps.astype(np.complex128)
-    re = _fmt17g(c128.real)
-    im = _fmt17g(c128.imag)
-    pr = [f"{float(abs(v) ** 2):.17g}" for v in amps]
-    bits = bitstrings(table)
-    with open(path, "w", newline="\n") as fh:
-        fh.write(header)
-        fh.writelines(f"{b.decode()}\t{r}\t{i}\t{p}\n" for b, r, i, p in zip(bits, re, im, pr))
+    bits = np.ascontiguousarray(bitstrings(table))
+    nb = bits.dtype.itemsize
+    lib = _io_lib()
+    n = amps.size
+    cap = min(n, ROWS_PER_CHUNK) * lib.tnbio_row_cap(nb)
+    buf = np.empty(max(cap, 1), dtype=np.uint8)
+    with open(path, "wb") as fh:
+        fh.write(header.encode())
+        for lo in range(0, n, ROWS_PER_CHUNK):
+            hi = min(n, lo + ROWS_PER_CHUNK)
+            got = lib.tnbio_format_rows(bits[lo:hi].ctypes.data, nb, amps[lo:hi].ctypes.data,
+                                        1 if single else 0, hi - lo, buf.ctypes.data, cap, threads)
+            if got < 0:
+                raise RuntimeError("tnbio_format_rows: buffer too small")
+            fh.write(memoryview(buf)[:got])

@@ -24,6 +24,40 @@ def pytest_configure(config):
     config.addinivalue_line("markers", "gpu: needs an sm_100 GPU and libtnb.so")
 
 
+# measured parity errors, printed at the end of the run (GPU logs show margins)
+PARITY = []
+
+
+def parity_report(tag, **errs):
+    """Record measured errors of one comparison (printed in the summary)."""
+    PARITY.append((tag, {k: float(v) for k, v in errs.items()}))
+    print(f"[parity] {tag}: " + ", ".join(f"{k}={v:.3e}" for k, v in errs.items()))
+
+
+def measured(err, what="rel_l2"):
+    """Record an error measured inside the current test and return it."""
+    test = os.environ.get("PYTEST_CURRENT_TEST", "?").split(" ")[0].split("::")[-1]
+    PARITY.append((test, {what: float(err)}))
+    return err
+
+
+def pytest_terminal_summary(terminalreporter, exitstatus, config):
+    if not PARITY:
+        return
+    tr = terminalreporter
+    tr.section("measured parity errors (each test asserts its own bound; north_star: rel L2 1e-4, XEB abs 1e-3)")
+    for tag, errs in PARITY:
+        tr.write_line(f"{tag}: " + ", ".join(f"{k}={v:.2e}" for k, v in errs.items()))
+    worst = {}
+    for tag, errs in PARITY:
+        for k, v in errs.items():
+            kind = "xeb" if "xeb" in k else "rel"
+            if v > worst.get(kind, (-1, ""))[0]:
+                worst[kind] = (v, tag)
+    tr.write_line("parity worst: " + "; ".join(f"{k} {v:.2e} ({t})" for k, (v, t) in sorted(worst.items()))
+                  + f"; {len(PARITY)} comparisons")
+
+
 def rel_l2(a, b) -> float:
     a = np.asarray(a, dtype=np.complex128).reshape(-1)
     b = np.asarray(b, dtype=np.complex128).reshape(-1)

@@ -11,7 +11,7 @@ import sys
 import numpy as np
 import pytest
 
-from conftest import GOLDEN, ROOT
+from conftest import GOLDEN, ROOT, measured
 
 REF_INSTALL = os.path.join(ROOT, "baseline", "_ref")  # pip --target install of the reference
 
@@ -78,6 +78,15 @@ def test_tncut_run_and_reduce_on_the_executor(gpu, tmp_path):
         assert got.keys() == ref.keys()
         a = np.array([got[k] for k in ref]); b = np.array([ref[k] for k in ref])
         assert np.linalg.norm(a - b) / np.linalg.norm(b) < tol, precision
+
+    # `run --threads 4` (cli.py:367-380): 4 concurrent ranges through the
+    # shared cached program, threads bound to devices round-robin
+    out = tmp_path / "ours_threads.tsv"
+    assert ours.main(["run", circ, order, "--precision", "single", "--threads", "4",
+                      "-o", str(out)]) == 0
+    got = table(out)
+    a = np.array([got[k] for k in ref]); b = np.array([ref[k] for k in ref])
+    assert measured(np.linalg.norm(a - b) / np.linalg.norm(b)) < 1e-4
 
     # partial ranges written by the executor, reduced by the reference's `reduce`
     import json

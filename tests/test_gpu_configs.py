@@ -8,7 +8,7 @@ import numpy as np
 import pytest
 
 import paper_2103_03074_b200 as tnb
-from conftest import golden, rel_l2
+from conftest import golden, rel_l2, measured
 from oracle import engine_np as O
 
 pytestmark = pytest.mark.gpu
@@ -27,17 +27,17 @@ def test_config_head_tail_xeb_vs_reference(gpu, workloads, name, rng_):
                                  precision="single", stats=st)
     key = f"head_single_{a}_{b}"
     stride = int(g["stride"])
-    assert rel_l2(hv.data[::stride], g[key + "_sub"]) < TOL
+    assert measured(rel_l2(hv.data[::stride], g[key + "_sub"])) < TOL
     assert abs(float(np.vdot(hv.data, hv.data).real) / float(g[key + "_norm2"]) - 1) < 2 * TOL
     # exact reference counters (engine.py:138-140)
     assert [st.multiplications, st.head_contractions] == [int(g[key + "_stats"][0]),
                                                           int(g[key + "_stats"][1])]
     tab = tnb.tail_amplitudes_unchecked(w.tn, w.tree, hv, precision="single")
     s2 = int(g["amps_stride"])
-    assert rel_l2(tab.amplitudes[::s2], g["amps_sub"]) < TOL
+    assert measured(rel_l2(tab.amplitudes[::s2], g["amps_sub"])) < TOL
     probs = np.abs(tab.amplitudes.astype(np.complex128)) ** 2
     f_ref = (2.0 ** 53 / probs.size) * float(g["amps_probsum"]) - 1.0
-    assert abs(O.xeb(probs, 53) - f_ref) < 1e-3
+    assert measured(abs(O.xeb(probs, 53) - f_ref), 'xeb_abs') < 1e-3
 
 
 def test_n_e_63_mask_bits(gpu, workloads):
@@ -75,4 +75,4 @@ def test_c5_32_fused_matches_staged(gpu, workloads):
     E.clear_cache()
     gc.collect()
     assert np.isfinite(hf).all() and np.abs(hs).max() > 0
-    assert rel_l2(hf, hs) < 1e-5
+    assert measured(rel_l2(hf, hs)) < 1e-5

@@ -12,7 +12,7 @@ import string
 import numpy as np
 import pytest
 
-from conftest import rel_l2
+from conftest import rel_l2, measured
 
 
 def _random_network(rng, n_t=None):
@@ -109,7 +109,7 @@ def test_random_networks_tensor_core_and_fused_paths(gpu, seed, monkeypatch):
         err = rel_l2(got, ref)
         assert err < 1e-4, (name, err, fused)
     # tensor-core paths agree with the fp32 SIMT path to fp32-level accuracy
-    assert rel_l2(results["fused"], results["simt"]) < 1e-5
+    assert measured(rel_l2(results["fused"], results["simt"])) < 1e-5
 
 
 @pytest.mark.gpu
@@ -150,4 +150,81 @@ def test_random_networks_slice_blocks(gpu, seed, monkeypatch):
     for j in range(1 << (len(sliced) - k)):
         want = full.run_range(j << k, (j + 1) << k, "fixed")
         got = blk.run_range(j, j + 1, "fixed")
-        assert rel_l2(got, want) < 1e-5, (j, rel_l2(got, want))
+        assert measured(rel_l2(got, want)) < 1e-5, (j, rel_l2(got, want))
+
+
+def _loose_bound_network(rng, huge_log2=13):
+    """T1[m,k] T2[k,n] -> X (fused into the next step) then X T3[n,p].
+    T1 has one huge entry in column k=0 where T2's row is zero, T2 one huge
+    entry in row k=1 where T1's column is zero: the a-priori bound
+    2K max|T1| max|T2| of X is ~2^(2*huge_log2+7) while |X| stays O(10) --
+    the fused fp16 operand of the second step would sit ~28 binary orders
+    below its scale, i.e. in fp16's subnormal range."""
+    m, k, n, p = [list(range(100 + 10 * i, 100 + 10 * i + w)) for i, w in enumerate((8, 6, 7, 8))]
+    big = float(2 ** huge_log2)
+
+    def rnd(*shape):
+        x = (rng.standard_normal(shape) + 1j * rng.standard_normal(shape)) / 2
+        return x.astype(np.complex64).astype(np.complex128)  # exactly representable in fp32
+
+    t1 = rnd(1 << 8, 1 << 6)
+    t1[:, 1] = 0
+    t1[0, 0] = big
+    t2 = rnd(1 << 6, 1 << 7)
+    t2[0, :] = 0
+    t2[1, 0] = big
+    t3 = rnd(1 << 7, 1 << 8)
+    leaves = [(1, m + k, t1.reshape((2,) * 14)), (2, k + n, t2.reshape((2,) * 13)),
+              (3, n + p, t3.reshape((2,) * 15))]
+    return leaves, [(1, 2, 1000), (1000, 3, 1001)], m + p
+
+
+@pytest.mark.gpu
+def test_fp16_scale_guard_fires_on_loose_bound(gpu, monkeypatch):
+    """The fused operand's fp16 scale comes from an a-priori bound; when the
+    result is ~2^-28 of it, the guard re-runs the producer with the exact max
+    (timing().scale_redos counts it) and the result stays at fp32 accuracy.
+    With the guard off the same program loses accuracy -- the guard is what
+    keeps it."""
+    from paper_2103_03074_b200.engine import Program
+
+    rng = np.random.default_rng(7)
+    leaves, steps, opens = _loose_bound_network(rng)
+    ref = _einsum(leaves, opens).reshape(-1)
+    monkeypatch.setenv("TNB_TC_MIN_RANK", "14")
+    errs = {}
+    for name, bits in (("guard", None), ("off", "-1")):
+        if bits is None:
+            monkeypatch.delenv("TNB_SCALE_GUARD_BITS", raising=False)
+        else:
+            monkeypatch.setenv("TNB_SCALE_GUARD_BITS", bits)
+        prog = Program(leaves, steps, [], opens, "single", 0, 0)
+        assert prog.info.n_steps_fused >= 1, "network did not produce a fused edge"
+        prog.set_timing(2)
+        got = prog.run_range(0, 1, "fixed")
+        errs[name] = rel_l2(got, ref)
+        redos = prog.timing()["scale_redos"]
+        if name == "guard":
+            assert redos >= 1
+        else:
+            assert redos == 0
+        del prog
+    measured(errs["guard"])
+    measured(errs["off"], "rel_l2_guard_off")
+    assert errs["guard"] < 1e-5, errs
+    assert errs["off"] > 10 * errs["guard"], errs
+
+
+@pytest.mark.gpu
+def test_fp16_scale_guard_quiet_on_c2(gpu, workloads):
+    """On a real plan (c2, 249 steps) the guard does not fire at its default
+    threshold: no re-runs, so the fast path is unchanged."""
+    from paper_2103_03074_b200 import engine as E
+
+    w = workloads("c2")
+    prog = E.head_program(w.tn, w.tree, w.sliced, "single")
+    prog.set_timing(2)
+    prog.run_range(0, 2, "fixed")
+    t = prog.timing()
+    assert prog.info.n_steps_fused >= 1
+    assert t["scale_redos"] == 0, t

@@ -13,7 +13,7 @@ import numpy as np
 import pytest
 
 import paper_2103_03074_b200 as tnb
-from conftest import golden, rel_l2
+from conftest import golden, rel_l2, measured
 from oracle import engine_np as O
 
 pytestmark = pytest.mark.gpu
@@ -51,7 +51,7 @@ def test_cgemm_tensor_core_vs_fp64(gpu, M, N, K):
 
 def test_cgemm_simt_vs_fp64(gpu):
     Cm, ref, _, _ = _cgemm(gpu, 64, 32, 128, False)
-    assert rel_l2(Cm, ref) < 1e-6
+    assert measured(rel_l2(Cm, ref)) < 1e-6
 
 
 def test_cgemm_scaled_inputs(gpu):
@@ -64,7 +64,7 @@ def test_cgemm_scaled_inputs(gpu):
     B = ((rng.standard_normal((K, N)) + 1j * rng.standard_normal((K, N))) * 2.0 ** 20).astype(np.complex64)
     Cm = np.empty((M, N), dtype=np.complex64)
     _lib.check(gpu.tnb_cgemm(0, M, N, K, A.ctypes.data, B.ctypes.data, Cm.ctypes.data, 0, 1))
-    assert rel_l2(Cm, A.astype(np.complex128) @ B.astype(np.complex128)) < 2e-6
+    assert measured(rel_l2(Cm, A.astype(np.complex128) @ B.astype(np.complex128))) < 2e-6
 
 
 # ---------------------------------------------------------------------------
@@ -83,7 +83,7 @@ def test_c1_all_amplitudes(gpu, workloads, precision):
         amps.append(tab.amplitudes)
     amps = np.array(amps)
     tol = 1e-10 if precision == "double" else SINGLE_TOL
-    assert rel_l2(amps, g["amps_statevector"]) < tol
+    assert measured(rel_l2(amps, g["amps_statevector"])) < tol
     # total probability over all 2^12 bitstrings
     assert abs(np.sum(np.abs(amps.astype(np.complex128)) ** 2) - 1.0) < (1e-9 if precision == "double" else 1e-4)
 
@@ -92,7 +92,7 @@ def test_c1_head_matches_reference_double(gpu, workloads):
     w = workloads("c1")
     g = golden("c1")
     hv = tnb.compute_head_vector(w.tn, w.tree, w.sliced, None, precision="double")
-    assert rel_l2(hv.data, g["head_full_double"]) < 1e-12
+    assert measured(rel_l2(hv.data, g["head_full_double"])) < 1e-12
     assert hv.provenance == str(g["provenance"])
     assert hv.cut_order == sorted(hv.cut_order)
 
@@ -105,7 +105,7 @@ def test_c1_ranges(gpu, workloads, mode):
         p = tnb.compute_head_vector(w.tn, w.tree, w.sliced, None, slice_range=(a, b),
                                     precision="double", mode=mode)
         assert p.slice_range == (a, b)
-        assert rel_l2(p.data, g[f"head_{mode}_{a}_{b}"]) < 1e-12
+        assert measured(rel_l2(p.data, g[f"head_{mode}_{a}_{b}"])) < 1e-12
 
 
 @pytest.mark.parametrize("precision", ["double", "single"])
@@ -139,7 +139,7 @@ def test_c1_contract_tree(gpu, workloads):
     asg = {ix: (5 >> (w.n_e - 1 - p)) & 1 for p, ix in enumerate(w.sliced)}
     out = tnb.contract_tree(w.tn, w.tree, asg)
     assert out.shape == g["contract_tree_mask5"].shape
-    assert rel_l2(out, g["contract_tree_mask5"]) < 1e-12
+    assert measured(rel_l2(out, g["contract_tree_mask5"])) < 1e-12
 
 
 def test_errors(gpu, workloads):
@@ -186,10 +186,10 @@ def test_s8_head_and_tail(gpu, workloads):
     _, errd, _ = _head_vs_golden(w, g, (0, 4), "double")
     assert errd < 1e-10
     tab = tnb.tail_amplitudes_unchecked(w.tn, w.tree, hv, precision="single")
-    assert rel_l2(tab.amplitudes, g["amps_sub"]) < SINGLE_TOL
+    assert measured(rel_l2(tab.amplitudes, g["amps_sub"])) < SINGLE_TOL
     # oracle at full size, same inputs
     ref = O.head_vector(w.tn, w.tree, w.sliced, (0, 4), "single")
-    assert rel_l2(hv.data, ref) < SINGLE_TOL
+    assert measured(rel_l2(hv.data, ref)) < SINGLE_TOL
 
 
 def test_s8_fixed_vs_free_and_ranges(gpu, workloads):
@@ -198,7 +198,7 @@ def test_s8_fixed_vs_free_and_ranges(gpu, workloads):
     for mode in ("fixed", "free"):
         hv = tnb.compute_head_vector(w.tn, w.tree, w.sliced, None, slice_range=(4, 12),
                                      precision="single", mode=mode)
-        assert rel_l2(hv.data, ref) < SINGLE_TOL
+        assert measured(rel_l2(hv.data, ref)) < SINGLE_TOL
 
 
 @pytest.mark.parametrize("name", ["m12", "c2", "c4"])
@@ -211,14 +211,14 @@ def test_sycamore_head_slice_vs_reference(gpu, workloads, name):
     assert abs(nr - 1) < 2 * SINGLE_TOL
     tab = tnb.tail_amplitudes_unchecked(w.tn, w.tree, hv, precision="single")
     stride = int(g["amps_stride"])
-    assert rel_l2(tab.amplitudes[::stride], g["amps_sub"]) < SINGLE_TOL
+    assert measured(rel_l2(tab.amplitudes[::stride], g["amps_sub"])) < SINGLE_TOL
     probs = np.abs(tab.amplitudes.astype(np.complex128)) ** 2
     assert abs(probs.sum() / float(g["amps_probsum"]) - 1) < 2 * SINGLE_TOL
     # linear XEB on the partial-slice amplitudes (analytics.py:46-58)
     n = 53
     f_ours = O.xeb(probs, n)
     f_ref = (2.0 ** n / probs.size) * float(g["amps_probsum"]) - 1.0
-    assert abs(f_ours - f_ref) < 1e-3
+    assert measured(abs(f_ours - f_ref), 'xeb_abs') < 1e-3
     # bitstring indexing: row mask -> layout bitstring with s1 spliced
     assert len(tab.amplitudes) == 1 << len(tab.open_qubits)
     bs = tab.bitstring(1)
@@ -272,7 +272,7 @@ def test_fused_staging_vs_staged(gpu, workloads, name):
     assert ef < SINGLE_TOL and es < SINGLE_TOL, (ef, es)
     # the bound-based fp16 scale keeps fp32-level accuracy
     assert ef < 10 * max(es, 1e-6), (ef, es)
-    assert rel_l2(hf, hs) < SINGLE_TOL
+    assert measured(rel_l2(hf, hs)) < SINGLE_TOL
 
 
 def test_fused_staging_c4_plan(gpu, workloads):

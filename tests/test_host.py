@@ -26,7 +26,7 @@ def test_library_loads_and_exports_every_header_symbol():
     for s in syms:
         assert hasattr(lib, s), s
         assert s in _lib.EXPORTS, s
-    assert lib.tnb_abi_version() == 1
+    assert lib.tnb_abi_version() == 2
 
 
 def test_no_device_fails_loudly_not_silently():

@@ -83,3 +83,31 @@ def test_amplitude_tsv_byte_identical(tmp_path, workloads):
         teng.write_amplitude_tsv(b, tab)
         assert a.read_bytes() == b.read_bytes()
         assert list(io.bitstrings(tab)) == [tab.bitstring(m).encode() for m in range(len(amps))]
+
+
+def test_amplitude_tsv_byte_identical_at_scale(tmp_path):
+    """2^16 rows of random c64 / c128 amplitudes spanning 2^-60..2^7 plus
+    zeros, -0, subnormals, +-inf and NaN: the libtnbio writer equals the
+    reference's per-row Python writer byte for byte (probability column:
+    numpy scalar abs ** 2 = libm hypotf/powf, not h*h)."""
+    from paper_2103_03074_b200 import io
+
+    import_reference()
+    from tncut import engine as teng
+
+    rng = np.random.default_rng(11)
+    n2 = 16
+    for dt in (np.complex64, np.complex128):
+        a = (rng.standard_normal(1 << n2) + 1j * rng.standard_normal(1 << n2)) * \
+            np.exp(rng.uniform(-42, 5, 1 << n2))
+        a = a.astype(dt)
+        a[:8] = [0, -0.0, 1e-45, np.inf, -np.inf, complex(np.nan, 1), complex(-np.nan, -0.0), 3e38]
+        s1 = {q: q % 2 for q in range(n2, 53)}
+        tab = teng.AmplitudeTable(s1=s1, open_qubits=list(range(n2)), amplitudes=a,
+                                  layout_ids=list(range(53)), circuit_sha256="c" * 64,
+                                  order_sha256="o" * 64, precision="single", mode="fixed")
+        ours, ref = tmp_path / "ours.tsv", tmp_path / "ref.tsv"
+        io.write_amplitude_tsv(ours, tab)
+        with np.errstate(all="ignore"):
+            teng.write_amplitude_tsv(ref, tab)
+        assert ours.read_bytes() == ref.read_bytes(), dt
