@@ -16,6 +16,7 @@ from __future__ import annotations
 import sys
 
 ENGINE_NAMES = ("compute_head_vector", "compute_tail_amplitudes", "reduce_partials", "contract_tree")
+IO_NAMES = ("write_amplitude_tsv",)  # byte-identical, formatted on all host threads (io.py)
 ANALYTICS_NAMES = ("xeb", "histogram", "postselect_curve", "mixed_xeb", "marginal_and_conditional",
                    "ks_to_porter_thomas")
 
@@ -44,7 +45,7 @@ def bind(slicer: bool | None = None) -> dict:
     import tncut.cli as cli
     import tncut.pipeline as pipeline
 
-    from . import analytics, engine
+    from . import analytics, engine, io
 
     previous = {"paper_2103_03074_b200.engine._thread_devices": engine._thread_devices}
     # `tncut run --threads T` (cli.py:367-380) fans ranges out over T threads:
@@ -64,6 +65,10 @@ def bind(slicer: bool | None = None) -> dict:
             if hasattr(mod, name):
                 previous[f"{mod.__name__}.{name}"] = getattr(mod, name)
                 setattr(mod, name, getattr(analytics, name))
+        for name in IO_NAMES:
+            if hasattr(mod, name):
+                previous[f"{mod.__name__}.{name}"] = getattr(mod, name)
+                setattr(mod, name, getattr(io, name))
     return previous
 
 

@@ -49,8 +49,11 @@ struct Cfg {
   static constexpr int B_ROWS = NB / CG;                 // B rows staged by each CTA
   static constexpr int B_TILE = B_ROWS * BK * 2;
   static constexpr int STAGE_BYTES = 2 * A_TILE + 2 * B_TILE;
-  static constexpr int STAGES = CG == 1 ? 4 : 6;
-  static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
+  // ring depth: ~192 KB of stages (6 at NB = 256; deeper for the narrow tiles,
+  // whose short-K steps live on prefetch depth), 4 for single CTAs
+  static constexpr int STAGES = CG == 1 ? 4 : (196608 / STAGE_BYTES > 10 ? 10 : 196608 / STAGE_BYTES);
+  static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 /*align*/ + 512 /*barriers*/;
+  static_assert((2 * STAGES + 2 * (512 / NB)) * 8 + 4 <= 512, "barrier area");
   // instruction descriptor: F32 accum, F16 x F16, K-major both, M = 128*CG, N = NB
   static constexpr uint32_t IDESC =
       (1u << 4) | ((uint32_t)(NB >> 3) << 17) | ((uint32_t)((BM * CG) >> 4) << 24);
@@ -344,19 +347,24 @@ gemm_f16x3_kernel(const __grid_constant__ CUtensorMap tm_ahi, const __grid_const
                   float* __restrict__ C, int M, int Np, int Kp, int splits, int k_per_split,
                   int chunk_kb, int group_m, const ScaleSrc scale_rows, const ScaleSrc scale_cols,
                   unsigned int* __restrict__ max_out, unsigned int* __restrict__ progress,
-                  int pace_slack, const __grid_constant__ FuseOut fo, int epi_spin) {
+                  int pace_slack, const __grid_constant__ FuseOut fo, int epi_spin, int mma_order) {
   using CF = Cfg<CG, NB>;
   constexpr int STAGES = CF::STAGES;
-  // gated re-run of a fused producer (fp16 scale guard): nothing to do unless
-  // the guard fired; uniform over the grid, before any barrier or TMEM use
-  if (fo.gate != nullptr && __ldcg(fo.gate) == 0u) return;
+  // fp16 scale-guard re-run of a fused producer: nothing to do unless the
+  // guard fires (same decision in every CTA, before any barrier or TMEM use)
+  if (fo.redo && !fused_redo_fires(fo)) return;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + STAGES * CF::STAGE_BYTES);
   uint64_t* empty_bar = full_bar + STAGES;
+  // TMEM partial accumulators: as many NB-column buffers as the 512 columns
+  // hold (2 at NB = 256, 8 at NB = 64), so the MMA warp can run NBUF chunks
+  // ahead of the epilogue -- short-K tiles (one or two K blocks) are then no
+  // longer serialised on the epilogue's TMEM read latency
+  constexpr int NBUF = TMEM_COLS / NB;
   uint64_t* pfull_bar = empty_bar + STAGES;
-  uint64_t* pempty_bar = pfull_bar + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(pempty_bar + 2);
+  uint64_t* pempty_bar = pfull_bar + NBUF;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(pempty_bar + NBUF);
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -379,7 +387,7 @@ gemm_f16x3_kernel(const __grid_constant__ CUtensorMap tm_ahi, const __grid_const
       mbar_init(&full_bar[i], CG);          // leader: own arrive(+tx) and the peer's arrive
       mbar_init(&empty_bar[i], 1);          // MMA commit (multicast to both CTAs)
     }
-    for (int i = 0; i < 2; ++i) {
+    for (int i = 0; i < NBUF; ++i) {
       mbar_init(&pfull_bar[i], 1);          // MMA commit (multicast)
       mbar_init(&pempty_bar[i], CG * Epi<NB>::THREADS);  // leader: epilogue threads of both CTAs
     }
@@ -457,9 +465,10 @@ gemm_f16x3_kernel(const __grid_constant__ CUtensorMap tm_ahi, const __grid_const
         const int k_begin = wc.split * k_per_split;
         const int nkb = (min(Kp, k_begin + k_per_split) - k_begin + BK - 1) / BK;
         for (int c0 = 0; c0 < nkb; c0 += chunk_kb, ++gchunk) {
-          const int buf = gchunk & 1;
-          if (epi_spin & 2) mbar_wait(&pempty_bar[buf], ((gchunk >> 1) & 1) ^ 1);
-          else mbar_wait_sleep(&pempty_bar[buf], ((gchunk >> 1) & 1) ^ 1);
+          const int buf = gchunk % NBUF;
+          const uint32_t par = (uint32_t)(gchunk / NBUF) & 1u;
+          if (epi_spin & 2) mbar_wait(&pempty_bar[buf], par ^ 1);
+          else mbar_wait_sleep(&pempty_bar[buf], par ^ 1);
           tc_fence_after();
           const uint32_t tmem_c = tmem_base + buf * NB;
           const int c1 = min(nkb, c0 + chunk_kb);
@@ -476,9 +485,17 @@ gemm_f16x3_kernel(const __grid_constant__ CUtensorMap tm_ahi, const __grid_const
 #pragma unroll
               for (int kk = 0; kk < BK / 16; ++kk) {
                 const uint64_t adv = (uint64_t)(kk * 32) >> 4;  // 16 fp16 = 32 B along K
-                umma_f16<CG, NB>(tmem_c, d_ahi + adv, d_blo + adv, (kb == c0 && kk == 0) ? 0u : 1u);
-                umma_f16<CG, NB>(tmem_c, d_alo + adv, d_bhi + adv, 1u);
-                umma_f16<CG, NB>(tmem_c, d_ahi + adv, d_bhi + adv, 1u);
+                if (mma_order == 0) {
+                  umma_f16<CG, NB>(tmem_c, d_ahi + adv, d_blo + adv, (kb == c0 && kk == 0) ? 0u : 1u);
+                  umma_f16<CG, NB>(tmem_c, d_alo + adv, d_bhi + adv, 1u);
+                  umma_f16<CG, NB>(tmem_c, d_ahi + adv, d_bhi + adv, 1u);
+                } else {
+                  // operand-sharing order: consecutive MMAs keep one operand
+                  // (Ahi, Ahi | Bhi, Bhi) -- fewer operand bit toggles
+                  umma_f16<CG, NB>(tmem_c, d_alo + adv, d_bhi + adv, (kb == c0 && kk == 0) ? 0u : 1u);
+                  umma_f16<CG, NB>(tmem_c, d_ahi + adv, d_bhi + adv, 1u);
+                  umma_f16<CG, NB>(tmem_c, d_ahi + adv, d_blo + adv, 1u);
+                }
               }
               umma_commit<CG>(&empty_bar[stage]);
             }
@@ -507,9 +524,10 @@ gemm_f16x3_kernel(const __grid_constant__ CUtensorMap tm_ahi, const __grid_const
 #pragma unroll
       for (int j = 0; j < EPI_COLS; ++j) acc[j] = 0.f;
       for (int c0 = 0; c0 < nkb; c0 += chunk_kb, ++gchunk) {
-        const int buf = gchunk & 1;
-        if (epi_spin & 1) mbar_wait(&pfull_bar[buf], (gchunk >> 1) & 1);
-        else mbar_wait_sleep(&pfull_bar[buf], (gchunk >> 1) & 1);
+        const int buf = gchunk % NBUF;
+        const uint32_t par = (uint32_t)(gchunk / NBUF) & 1u;
+        if (epi_spin & 1) mbar_wait(&pfull_bar[buf], par);
+        else mbar_wait_sleep(&pfull_bar[buf], par);
         tc_fence_after();
         const uint32_t taddr = tmem_base + ((uint32_t)(q * 32) << 16) + buf * NB + grp * EPI_COLS;
 #pragma unroll
@@ -746,7 +764,14 @@ void tc_plan_gemm(TcGemmPlan* p, const __half* Ahi, const __half* Alo, const __h
   // 343 GB DRAM without it); tiles of few K blocks turn over fast enough for
   // the raster alone, and there the lockstep costs 6-8% of the cycles
   static const int pace_min_kb = env_int("TNB_PACE_MIN_KB", 64);
-  p->pace_slack = kblocks / p->splits >= pace_min_kb ? env_int("TNB_PACE", kDefaultPaceSlack) : 0;
+  // ... and only when the smaller operand does not sit in L2 anyway (a few-MB
+  // B panel is shared by every tile without help)
+  static const int pace_min_mb = env_int("TNB_PACE_MIN_MB", 0);
+  const double small_mb = (double)std::min(M, Np) * (double)Kp * 4.0 / 1048576.0;
+  p->pace_slack = kblocks / p->splits >= pace_min_kb && small_mb >= pace_min_mb
+                      ? env_int("TNB_PACE", kDefaultPaceSlack) : 0;
+  static const int mma_order = env_int("TNB_MMA_ORDER", 0);
+  p->mma_order = mma_order;
   static const int spin = env_int("TNB_EPI_SPIN", -1);
   p->epi_spin = spin >= 0 ? spin : 0;
   const int b_rows = p->nb / p->cta_group;
@@ -778,7 +803,7 @@ void launch_cg(const TcGemmPlan* p, cudaStream_t s) {
   TNB_CUDA(cudaLaunchKernelEx(&cfg, kern, maps[0], maps[1], maps[2], maps[3], p->C, (int)p->M,
                               (int)p->Np, (int)p->Kp, p->splits, (int)p->k_per_split, p->chunk_kb,
                               p->group_m, p->scale_rows, p->scale_cols, p->max_out, p->progress,
-                              p->pace_slack, p->fuse, p->epi_spin));
+                              p->pace_slack, p->fuse, p->epi_spin, p->mma_order));
 }
 
 void tc_launch_gemm(const TcGemmPlan* p, cudaStream_t s) {

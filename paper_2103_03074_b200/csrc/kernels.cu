@@ -229,7 +229,7 @@ contract_smallk_kernel(const T* __restrict__ A, const T* __restrict__ B, T* __re
                        const ByteLut* __restrict__ glb, const ByteLut* __restrict__ gle,
                        unsigned int* __restrict__ max_out, const __grid_constant__ FuseOut fo) {
   using S = typename Scalar<T>::type;
-  if (fo.gate != nullptr && __ldcg(fo.gate) == 0u) return;  // gated re-run (scale guard)
+  if (fo.redo && !fused_redo_fires(fo)) return;  // scale-guard re-run (FuseOut::redo)
   __shared__ uint32_t la[4][256];
   __shared__ uint32_t lb[4][256];
   __shared__ uint32_t fm[4][256];
@@ -532,21 +532,6 @@ stage_async_kernel(const float2* __restrict__ src, StageTables tb, int logK,
   }
 }
 
-// fp16 scale guard (see launch_scale_guard in tnb_internal.h)
-__global__ void scale_guard_kernel(const ScaleSrc bound, const unsigned int* __restrict__ own,
-                                   unsigned int* __restrict__ guard, int thr_bits,
-                                   unsigned int* __restrict__ count) {
-  const float mo = __uint_as_float(__ldcg(own));
-  int eb = 0, eo = 0;
-  unsigned int fire = 0;
-  if (mo > 0.f && scale_bound_exp(bound.a, bound.b, bound.f, eb)) {
-    frexpf(mo, &eo);
-    fire = (eb - eo) > thr_bits ? 1u : 0u;
-  }
-  *guard = fire;
-  if (fire) atomicAdd(count, 1u);
-}
-
 __global__ void splitk_reduce_kernel(const float* __restrict__ ws, int splits, int64_t elems,
                                      float* __restrict__ C, const ScaleSrc scale_rows,
                                      const ScaleSrc scale_cols, unsigned int* __restrict__ max_out) {
@@ -771,12 +756,6 @@ void launch_stage(const float2* src, const StageTables& tb, int64_t K, bool expa
     default: expand ? go(T_{}, std::integral_constant<int, 16>{}) : go(F_{}, std::integral_constant<int, 16>{}); break;
   }
   check_launch("stage");
-}
-
-void launch_scale_guard(const ScaleSrc& bound, const unsigned int* own, unsigned int* guard,
-                        int thr_bits, unsigned int* count, cudaStream_t s) {
-  scale_guard_kernel<<<1, 1, 0, s>>>(bound, own, guard, thr_bits, count);
-  check_launch("scale_guard");
 }
 
 void launch_splitk_reduce(const float* ws, int splits, int64_t elems, float* C,

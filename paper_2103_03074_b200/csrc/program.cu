@@ -131,13 +131,13 @@ struct StepRec {
   FuseOut simt_fuse;                           // SIMT (small-K) producer: fused output map
   int batch = -1;                              // tiled SIMT step launched in Program::batches[batch]
   TcGemmPlan tc;
-  // fp16 scale guard of a fused producer: after it runs, guard_bound (the
-  // a-priori bound it scaled by) is compared with its result's exact max; if
-  // the bound is more than Program::guard_bits binary orders looser, the
-  // gated re-run (tc_redo / simt_redo: same launch, scale = the exact max)
-  // rewrites the operand and the consumer's ScaleSrc follows the guard word
+  // fp16 scale guard of a fused producer: right after it, the re-run launch
+  // (tc_redo / simt_redo, FuseOut::redo) compares the a-priori bound it scaled
+  // by with its result's exact max; if the bound is more than
+  // Program::guard_bits binary orders looser it rewrites the operand scaled
+  // by the exact max, else exits at once.  The decision lands in *guard,
+  // which the consumer's ScaleSrc follows
   bool has_redo = false;
-  ScaleSrc guard_bound;
   unsigned int* guard = nullptr;
   TcGemmPlan tc_redo;
   FuseOut simt_redo;
@@ -578,9 +578,9 @@ void plan_tensor_core_steps(Program* P) {
                  P->num_sms);
     s.tc.progress = P->d_progress;
     if (getenv("TNB_DEBUG_GEMM"))
-      fprintf(stderr, "TNB_GEMM step %d M %lld Np %lld Kp %lld cg %d nb %d splits %d fused_out %d rows_fused %d cols_fused %d\n",
+      fprintf(stderr, "TNB_GEMM step %d M %lld Np %lld Kp %lld cg %d nb %d splits %d fused_out %d rows_fused %d cols_fused %d hoisted %d grid %d\n",
               i, (long long)s.M, (long long)Np, (long long)Kp, s.tc.cta_group, s.tc.nb, s.tc.splits,
-              P->tensors[s.out].fuse_role, (int)s.fuse_rows, (int)s.fuse_cols);
+              P->tensors[s.out].fuse_role, (int)s.fuse_rows, (int)s.fuse_cols, (int)s.hoisted, s.tc.grid);
     if (P->tensors[s.out].fuse_role == 0) continue;
     if (s.tc.splits != 1) throw Error(TNB_ERR_SHAPE, "fused staging planned for a split-K step");
     FuseOut& f = s.tc.fuse;
@@ -641,10 +641,13 @@ void plan_tensor_core_steps(Program* P) {
       FuseOut& f = st.kind == KIND_TC ? st.tc.fuse : st.simt_fuse;
       if (f.mode == 0) continue;
       st.has_redo = true;
-      st.guard_bound = f.scale;
       st.guard = P->d_guard + P->slot[st.out];
       FuseOut r = f;
-      r.gate = st.guard;
+      r.redo = 1;
+      r.guard_bits = P->guard_bits;
+      r.guard_bound = f.scale;
+      r.guard_word = st.guard;
+      r.guard_count = P->d_guard + P->slot.size();
       r.scale = ScaleSrc{};
       r.scale.a = P->d_tmax + P->slot[st.out];
       if (st.kind == KIND_TC) {
@@ -963,8 +966,9 @@ Program* program_create(const tnb_program_desc* d) {
   // staging.  TNB_TC_MIN_RANK (read per program; tests lower it so small
   // random networks exercise the tensor-core and fused-staging paths)
   const int tc_min_rank = env_int("TNB_TC_MIN_RANK", 27);
+  const int tc_min_k = env_int("TNB_TC_MIN_K", 3);  // log2 of the smallest shared dimension
   auto tc_eligible = [&](int na, int nb, int nab) {
-    return use_tc && nab >= 3 && na + nb + nab >= tc_min_rank && std::max(na, nb) >= 7 &&
+    return use_tc && nab >= tc_min_k && na + nb + nab >= tc_min_rank && std::max(na, nb) >= 7 &&
            std::min(na, nb) >= 3;
   };
   OrderPlan op = plan_orders(d, P.get(), use_tc, tc_eligible);
@@ -1447,13 +1451,11 @@ void exec_step(Program* P, StepRec& s, int parts) {
                             s.simt_fuse.mode ? &s.simt_fuse : nullptr, P->stream);
     C.launches++;
     if (s.has_redo) {
-      launch_scale_guard(s.guard_bound, P->d_tmax + P->slot[s.out], s.guard, P->guard_bits,
-                         P->d_guard + P->slot.size(), P->stream);
       launch_contract_simt<T>((const T*)P->tensor_ptr(s.a), (const T*)P->tensor_ptr(s.b),
                               (T*)P->tensor_ptr(s.out), s.M, s.N, s.K, P->d_luts + s.lut_a,
                               P->d_luts + s.lut_b, s.lut_e >= 0 ? P->d_luts + s.lut_e : nullptr,
                               P->d_tmax + P->slot[s.out], &s.simt_redo, P->stream);
-      C.launches += 2;
+      C.launches += 1;
     }
     C.close(2, e);
     return;
@@ -1490,13 +1492,11 @@ void exec_step(Program* P, StepRec& s, int parts) {
       C.gemm_launches++;
       C.gemm_flops += 8.0 * s.mults;
       if (s.has_redo) {
-        // guard + gated re-run (exits at once unless the guard fired)
+        // scale-guard re-run (exits at once unless the guard fires)
         e = C.mark(1);
-        launch_scale_guard(s.guard_bound, s.tc.max_out, s.guard, P->guard_bits,
-                           P->d_guard + P->slot.size(), P->stream);
         tc_launch_gemm(&s.tc_redo, P->stream);
         C.close(1, e);
-        C.launches += 2;
+        C.launches += 1;
       }
     }
     if ((parts & kPost) && s.tc.splits > 1) {

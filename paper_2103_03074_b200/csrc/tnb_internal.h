@@ -129,11 +129,6 @@ template <typename T>
 void launch_contract_simt(const T* A, const T* B, T* C, int64_t M, int64_t N, int64_t K,
                           const ByteLut* lutA, const ByteLut* lutB, const ByteLut* lutE,
                           unsigned int* max_out, const FuseOut* fuse, cudaStream_t s);
-// fp16 scale guard of a fused operand: *guard = 1 (and ++*count) when the
-// producer's a-priori bound `bound` exceeds its result's exact max `own` by
-// more than `thr_bits` binary orders, else 0 (stream-ordered, one thread)
-void launch_scale_guard(const ScaleSrc& bound, const unsigned int* own, unsigned int* guard,
-                        int thr_bits, unsigned int* count, cudaStream_t s);
 // one step of a batched SIMT launch (contract_simt_batch_kernel)
 struct SimtStepDesc {
   const void* A;
@@ -226,8 +221,35 @@ struct FuseOut {
   const ByteLut* lut_n = nullptr;
   uint32_t dlow[32] = {};
   ScaleSrc scale;                // scale of the written operand
-  const unsigned int* gate = nullptr;  // re-run of a fused producer: run only if *gate != 0
+  // fp16 scale guard re-run of a fused producer (redo != 0): every CTA first
+  // decides whether the a-priori bound `guard_bound` exceeds the result's
+  // exact max (scale.a, published by the first run) by more than guard_bits
+  // binary orders; CTA 0 records the decision in *guard_word (read by the
+  // consumer's ScaleSrc) and counts it; without it the launch exits at once
+  int redo = 0;
+  int guard_bits = 18;
+  ScaleSrc guard_bound;
+  unsigned int* guard_word = nullptr;
+  unsigned int* guard_count = nullptr;
 };
+
+#ifdef __CUDACC__
+// the re-run prologue (see FuseOut::redo); true = rewrite the operand
+__device__ __forceinline__ bool fused_redo_fires(const FuseOut& fo) {
+  const float mo = __uint_as_float(__ldcg(fo.scale.a));
+  int eb = 0, eo = 0;
+  bool fire = false;
+  if (mo > 0.f && scale_bound_exp(fo.guard_bound.a, fo.guard_bound.b, fo.guard_bound.f, eb)) {
+    frexpf(mo, &eo);
+    fire = (eb - eo) > fo.guard_bits;
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    *fo.guard_word = fire ? 1u : 0u;
+    if (fire) atomicAdd(fo.guard_count, 1u);
+  }
+  return fire;
+}
+#endif
 
 // ---------------------------------------------------------------------------
 // tcgen05 GEMM (gemm_tc.cu):  C[M][Np] (fp32) = alpha * sum over the three
@@ -242,6 +264,7 @@ struct TcGemmPlan {
   unsigned int* progress = nullptr;  // device [num units]: K-block progress for soft pacing
   int pace_slack = 0;            // K blocks a unit may lead the slowest one (0: off)
   int epi_spin = 0;              // epilogue polls the TMEM-ready barrier instead of sleeping
+  int mma_order = 0;             // order of the three split products per K step
   int64_t k_per_split = 0;       // multiple of the K block
   int grid = 0;
   alignas(64) unsigned char tmap[4][128];  // CUtensorMap x4: Ahi, Alo, Bhi, Blo

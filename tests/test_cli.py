@@ -42,6 +42,9 @@ def test_bind_rebinds_engine_and_analytics_names():
         assert cli.reduce_partials is engine.reduce_partials
         assert pipeline.compute_head_vector is engine.compute_head_vector
         assert cli.xeb is analytics.xeb
+        from paper_2103_03074_b200 import io as ours_io
+
+        assert cli.write_amplitude_tsv is ours_io.write_amplitude_tsv
     finally:
         ours.unbind(prev)
     assert cli.compute_head_vector is not engine.compute_head_vector
