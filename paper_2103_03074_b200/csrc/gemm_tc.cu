@@ -33,11 +33,20 @@ constexpr int EPI_COLS = 64;                 // fp32 register accumulator column
 // skinny ones (Np <= NB), whose 256-wide tiles were >= 75 % padding -- MMA,
 // TMEM and epilogue work on columns that do not exist.  One epilogue warp
 // group (4 lane quadrants) per 64 columns.
+// Narrow tiles get more TMEM partial buffers (the MMA warp runs up to BUFS
+// chunks ahead) and, at NB = 64, two epilogue groups that each own every
+// other tile of the CTA unit: a short-K tile's epilogue is a latency chain
+// (barrier wake-up, tcgen05.ld, stores), so two of them run concurrently.
 template <int NB>
 struct Epi {
   static constexpr int SPLIT = NB / EPI_COLS;     // column groups per TMEM lane quadrant
-  static constexpr int THREADS = 128 * SPLIT;     // epilogue threads
+  static constexpr int GROUPS = NB == 64 ? 2 : 1; // tile-parallel epilogue groups (<= 384
+                                                  // threads: the 64-float accumulators stay in registers)
+  static constexpr int GROUP_THREADS = 128 * SPLIT;
+  static constexpr int THREADS = GROUP_THREADS * GROUPS;  // epilogue threads
   static constexpr int NUM_THREADS = 128 + THREADS;
+  static constexpr int BUFS = 512 / (GROUPS * NB);  // TMEM partial buffers per group (2-4)
+  static_assert(BUFS * GROUPS * NB == 512, "TMEM columns");
 };
 constexpr int TMEM_COLS = 512;
 constexpr int kDefaultChunkKb = 8;           // K blocks (of 32 fp16) per promotion chunk
@@ -52,7 +61,11 @@ struct Cfg {
   // ring depth: ~192 KB of stages (6 at NB = 256; deeper for the narrow tiles,
   // whose short-K steps live on prefetch depth), 4 for single CTAs
   static constexpr int STAGES = CG == 1 ? 4 : (196608 / STAGE_BYTES > 10 ? 10 : 196608 / STAGE_BYTES);
-  static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 /*align*/ + 512 /*barriers*/;
+  // narrow tiles stage the fused-store LUTs in shared memory; at NB = 256 the
+  // extra 8 KB would push the carve-out to the 228 KB step and cost the wide
+  // tiles ~12 % (measured), so they keep reading the LUTs through L1
+  static constexpr int LUT_BYTES = NB < 256 ? 8192 : 0;
+  static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 /*align*/ + 512 /*barriers*/ + LUT_BYTES;
   static_assert((2 * STAGES + 2 * (512 / NB)) * 8 + 4 <= 512, "barrier area");
   // instruction descriptor: F32 accum, F16 x F16, K-major both, M = 128*CG, N = NB
   static constexpr uint32_t IDESC =
@@ -214,6 +227,10 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&r)[16]) {
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
 
+__device__ __forceinline__ uint32_t lut_lookup_s(const uint32_t (*t)[256], uint32_t j) {
+  return t[0][j & 255] | t[1][(j >> 8) & 255] | t[2][(j >> 16) & 255] | t[3][j >> 24];
+}
+
 __device__ __forceinline__ uint32_t lut_lookup(const ByteLut* l, uint32_t j) {
   return __ldg(&l->t[0][j & 255]) | __ldg(&l->t[1][(j >> 8) & 255]) |
          __ldg(&l->t[2][(j >> 16) & 255]) | __ldg(&l->t[3][j >> 24]);
@@ -262,8 +279,8 @@ __device__ __forceinline__ void store_slot(const FuseOut& fo, uint32_t a, const 
 // stage_kernel writes for a staged operand.  `tile` = destination of the
 // warp's (row0, col0) corner.  `fast` is warp-uniform.
 template <int MODE>
-__device__ __forceinline__ void fused_store(const FuseOut& fo, uint32_t tile, float* acc, float so,
-                                            int nvalid, int lane) {
+__device__ __forceinline__ void fused_store(const FuseOut& fo, const uint32_t (*lm)[256], uint32_t tile,
+                                            float* acc, float so, int nvalid, int lane) {
   if (fo.fast && nvalid == EPI_COLS / 2) {
     // butterfly exchanges: slot q = complex 4q..4q+3 = floats 8q..8q+7
 #pragma unroll
@@ -290,7 +307,8 @@ __device__ __forceinline__ void fused_store(const FuseOut& fo, uint32_t tile, fl
 #pragma unroll
     for (int q = 0; q < 8; ++q) store_slot<MODE>(fo, a | fo.slot_w[q], acc + 8 * q, so);
   } else {
-    const uint32_t base = tile | lut_lookup(fo.lut_m, (uint32_t)lane);
+    const uint32_t base = tile | (lm != nullptr ? lut_lookup_s(lm, (uint32_t)lane)
+                                                : lut_lookup(fo.lut_m, (uint32_t)lane));
 #pragma unroll
     for (int j = 0; j < EPI_COLS / 2; ++j) {
       if (j >= nvalid) break;
@@ -347,7 +365,7 @@ gemm_f16x3_kernel(const __grid_constant__ CUtensorMap tm_ahi, const __grid_const
                   float* __restrict__ C, int M, int Np, int Kp, int splits, int k_per_split,
                   int chunk_kb, int group_m, const ScaleSrc scale_rows, const ScaleSrc scale_cols,
                   unsigned int* __restrict__ max_out, unsigned int* __restrict__ progress,
-                  int pace_slack, const __grid_constant__ FuseOut fo, int epi_spin, int mma_order) {
+                  int pace_slack, const __grid_constant__ FuseOut fo, int epi_spin) {
   using CF = Cfg<CG, NB>;
   constexpr int STAGES = CF::STAGES;
   // fp16 scale-guard re-run of a fused producer: nothing to do unless the
@@ -362,9 +380,13 @@ gemm_f16x3_kernel(const __grid_constant__ CUtensorMap tm_ahi, const __grid_const
   // ahead of the epilogue -- short-K tiles (one or two K blocks) are then no
   // longer serialised on the epilogue's TMEM read latency
   constexpr int NBUF = TMEM_COLS / NB;
+  constexpr int GROUPS = Epi<NB>::GROUPS, BUFS = Epi<NB>::BUFS;
   uint64_t* pfull_bar = empty_bar + STAGES;
   uint64_t* pempty_bar = pfull_bar + NBUF;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(pempty_bar + NBUF);
+  // fused-store destination LUTs (rows, cols) staged in shared memory
+  uint32_t (*lut_s)[4][256] = reinterpret_cast<uint32_t (*)[4][256]>(
+      smem + STAGES * CF::STAGE_BYTES + 512);
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -389,7 +411,7 @@ gemm_f16x3_kernel(const __grid_constant__ CUtensorMap tm_ahi, const __grid_const
     }
     for (int i = 0; i < NBUF; ++i) {
       mbar_init(&pfull_bar[i], 1);          // MMA commit (multicast)
-      mbar_init(&pempty_bar[i], CG * Epi<NB>::THREADS);  // leader: epilogue threads of both CTAs
+      mbar_init(&pempty_bar[i], CG * Epi<NB>::GROUP_THREADS);  // leader: one epilogue group of both CTAs
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -404,6 +426,13 @@ gemm_f16x3_kernel(const __grid_constant__ CUtensorMap tm_ahi, const __grid_const
                        smem_u32(tmem_slot)),
                    "r"(TMEM_COLS));
       asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+    }
+  }
+  if (CF::LUT_BYTES > 0 && fo.mode != 0 && warp >= 4) {
+    for (int i = threadIdx.x - 128; i < 2048; i += Epi<NB>::THREADS) {
+      const ByteLut* l = i < 1024 ? fo.lut_m : fo.lut_n;
+      const int j = i & 1023;
+      lut_s[i >> 10][j >> 8][j & 255] = __ldg(&l->t[j >> 8][j & 255]);
     }
   }
   tc_fence_before();
@@ -459,14 +488,21 @@ gemm_f16x3_kernel(const __grid_constant__ CUtensorMap tm_ahi, const __grid_const
       // ===== MMA issuer (leader CTA) =====
       int stage = 0;
       uint32_t phase = 0;
-      int gchunk = 0;
-      for (int w = unit; w < total; w += n_units) {
+      int gcnt[GROUPS];
+#pragma unroll
+      for (int g = 0; g < GROUPS; ++g) gcnt[g] = 0;
+      int tseq = 0;
+      for (int w = unit; w < total; w += n_units, ++tseq) {
         const WorkCoord wc = decode(w, nm, nn, group_m);
         const int k_begin = wc.split * k_per_split;
         const int nkb = (min(Kp, k_begin + k_per_split) - k_begin + BK - 1) / BK;
-        for (int c0 = 0; c0 < nkb; c0 += chunk_kb, ++gchunk) {
-          const int buf = gchunk % NBUF;
-          const uint32_t par = (uint32_t)(gchunk / NBUF) & 1u;
+        const int g = tseq % GROUPS;  // the epilogue group that owns this tile
+        int gc = 0;
+#pragma unroll
+        for (int x = 0; x < GROUPS; ++x) if (x == g) gc = gcnt[x];
+        for (int c0 = 0; c0 < nkb; c0 += chunk_kb, ++gc) {
+          const int buf = g * BUFS + gc % BUFS;
+          const uint32_t par = (uint32_t)(gc / BUFS) & 1u;
           if (epi_spin & 2) mbar_wait(&pempty_bar[buf], par ^ 1);
           else mbar_wait_sleep(&pempty_bar[buf], par ^ 1);
           tc_fence_after();
@@ -485,17 +521,9 @@ gemm_f16x3_kernel(const __grid_constant__ CUtensorMap tm_ahi, const __grid_const
 #pragma unroll
               for (int kk = 0; kk < BK / 16; ++kk) {
                 const uint64_t adv = (uint64_t)(kk * 32) >> 4;  // 16 fp16 = 32 B along K
-                if (mma_order == 0) {
-                  umma_f16<CG, NB>(tmem_c, d_ahi + adv, d_blo + adv, (kb == c0 && kk == 0) ? 0u : 1u);
-                  umma_f16<CG, NB>(tmem_c, d_alo + adv, d_bhi + adv, 1u);
-                  umma_f16<CG, NB>(tmem_c, d_ahi + adv, d_bhi + adv, 1u);
-                } else {
-                  // operand-sharing order: consecutive MMAs keep one operand
-                  // (Ahi, Ahi | Bhi, Bhi) -- fewer operand bit toggles
-                  umma_f16<CG, NB>(tmem_c, d_alo + adv, d_bhi + adv, (kb == c0 && kk == 0) ? 0u : 1u);
-                  umma_f16<CG, NB>(tmem_c, d_ahi + adv, d_bhi + adv, 1u);
-                  umma_f16<CG, NB>(tmem_c, d_ahi + adv, d_blo + adv, 1u);
-                }
+                umma_f16<CG, NB>(tmem_c, d_ahi + adv, d_blo + adv, (kb == c0 && kk == 0) ? 0u : 1u);
+                umma_f16<CG, NB>(tmem_c, d_alo + adv, d_bhi + adv, 1u);
+                umma_f16<CG, NB>(tmem_c, d_ahi + adv, d_bhi + adv, 1u);
               }
               umma_commit<CG>(&empty_bar[stage]);
             }
@@ -505,27 +533,32 @@ gemm_f16x3_kernel(const __grid_constant__ CUtensorMap tm_ahi, const __grid_const
           if (lane == 0) umma_commit<CG>(&pfull_bar[buf]);
           __syncwarp();
         }
+#pragma unroll
+        for (int x = 0; x < GROUPS; ++x) if (x == g) gcnt[x] = gc;
       }
     }
   } else if (warp >= 4) {
     // ===== promotion + epilogue: warp -> TMEM lane quadrant (warp % 4), column group =====
     const int q = warp & 3;
-    const int grp = (warp - 4) >> 2;
+    const int grp = ((warp - 4) >> 2) % Epi<NB>::SPLIT;   // column group
+    const int eg = ((warp - 4) >> 2) / Epi<NB>::SPLIT;    // epilogue group (tiles tseq % GROUPS == eg)
     const float alpha =
         splits == 1 ? 1.f / (scale_from_src(scale_rows) * scale_from_src(scale_cols)) : 1.f;
     const float so = fo.mode != 0 ? scale_from_src(fo.scale) : 1.f;  // fused: consumer's scale
     float vmax = 0.f;  // max |C| of this thread's outputs (scale slot of the result tensor)
-    int gchunk = 0;
-    for (int w = unit; w < total; w += n_units) {
+    int gc = 0;         // chunks of this group's tiles so far
+    int tseq = 0;
+    for (int w = unit; w < total; w += n_units, ++tseq) {
+      if (tseq % GROUPS != eg) continue;
       const WorkCoord wc = decode(w, nm, nn, group_m);
       const int k_begin = wc.split * k_per_split;
       const int nkb = (min(Kp, k_begin + k_per_split) - k_begin + BK - 1) / BK;
       float acc[EPI_COLS];
 #pragma unroll
       for (int j = 0; j < EPI_COLS; ++j) acc[j] = 0.f;
-      for (int c0 = 0; c0 < nkb; c0 += chunk_kb, ++gchunk) {
-        const int buf = gchunk % NBUF;
-        const uint32_t par = (uint32_t)(gchunk / NBUF) & 1u;
+      for (int c0 = 0; c0 < nkb; c0 += chunk_kb, ++gc) {
+        const int buf = eg * BUFS + gc % BUFS;
+        const uint32_t par = (uint32_t)(gc / BUFS) & 1u;
         if (epi_spin & 1) mbar_wait(&pfull_bar[buf], par);
         else mbar_wait_sleep(&pfull_bar[buf], par);
         tc_fence_after();
@@ -559,10 +592,13 @@ gemm_f16x3_kernel(const __grid_constant__ CUtensorMap tm_ahi, const __grid_const
         // fused staging: write the consumer's fp16 operand directly
         const int nvalid = min(EPI_COLS / 2, (Np - col0) >> 1);
         if (nvalid > 0) {  // warp-uniform; every row of a 32-row group exists (M >= 128, 2^k)
-          const uint32_t tile = lut_lookup(fo.lut_m, (uint32_t)row0) | lut_lookup(fo.lut_n, (uint32_t)(col0 >> 1));
+          const uint32_t tile = CF::LUT_BYTES > 0
+              ? lut_lookup_s(lut_s[0], (uint32_t)row0) | lut_lookup_s(lut_s[1], (uint32_t)(col0 >> 1))
+              : lut_lookup(fo.lut_m, (uint32_t)row0) | lut_lookup(fo.lut_n, (uint32_t)(col0 >> 1));
           // (x alpha) so == x (alpha so) exactly: both are powers of two
-          if (fo.mode == 1) fused_store<1>(fo, tile, acc, alpha * so, nvalid, lane);
-          else fused_store<2>(fo, tile, acc, alpha * so, nvalid, lane);
+          const uint32_t (*lm)[256] = CF::LUT_BYTES > 0 ? lut_s[0] : nullptr;
+          if (fo.mode == 1) fused_store<1>(fo, lm, tile, acc, alpha * so, nvalid, lane);
+          else fused_store<2>(fo, lm, tile, acc, alpha * so, nvalid, lane);
         }
       } else if (row0 + 32 <= M && col0 + EPI_COLS <= Np) {
         // full 32-row x 64-column block: transpose float4 chunks inside each
@@ -770,8 +806,6 @@ void tc_plan_gemm(TcGemmPlan* p, const __half* Ahi, const __half* Alo, const __h
   const double small_mb = (double)std::min(M, Np) * (double)Kp * 4.0 / 1048576.0;
   p->pace_slack = kblocks / p->splits >= pace_min_kb && small_mb >= pace_min_mb
                       ? env_int("TNB_PACE", kDefaultPaceSlack) : 0;
-  static const int mma_order = env_int("TNB_MMA_ORDER", 0);
-  p->mma_order = mma_order;
   static const int spin = env_int("TNB_EPI_SPIN", -1);
   p->epi_spin = spin >= 0 ? spin : 0;
   const int b_rows = p->nb / p->cta_group;
@@ -803,7 +837,7 @@ void launch_cg(const TcGemmPlan* p, cudaStream_t s) {
   TNB_CUDA(cudaLaunchKernelEx(&cfg, kern, maps[0], maps[1], maps[2], maps[3], p->C, (int)p->M,
                               (int)p->Np, (int)p->Kp, p->splits, (int)p->k_per_split, p->chunk_kb,
                               p->group_m, p->scale_rows, p->scale_cols, p->max_out, p->progress,
-                              p->pace_slack, p->fuse, p->epi_spin, p->mma_order));
+                              p->pace_slack, p->fuse, p->epi_spin));
 }
 
 void tc_launch_gemm(const TcGemmPlan* p, cudaStream_t s) {
