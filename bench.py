@@ -197,12 +197,14 @@ def barrier(dist, local):
 
 def traffic_from_profile():
     """DRAM bytes per GEMM launch from the committed ncu capture of this bench
-    (scripts/gpu_traffic.sh -> profiles/r1/gemm_traffic.json), else null."""
-    path = os.path.join(ROOT, "profiles", "r1", "gemm_traffic.json")
+    (scripts/make_traffic_json.py -> profiles/r2/gemm_traffic.json), else null."""
+    path = os.path.join(ROOT, "profiles", "r2", "gemm_traffic.json")
     try:
         with open(path) as fh:
             t = json.load(fh)
         return {"traffic": t["dram_bytes_per_launch"], "traffic_unit": "bytes/launch (DRAM read+write)",
+                "traffic_algorithmic": t.get("algorithmic_bytes_per_launch"),
+                "traffic_over_algorithmic": t.get("dram_over_algorithmic"),
                 "traffic_source": t["source"]}
     except Exception:
         return {"traffic": None}

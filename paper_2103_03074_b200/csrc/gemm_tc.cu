@@ -281,7 +281,7 @@ __device__ __forceinline__ void store_slot(const FuseOut& fo, uint32_t a, const 
 template <int MODE>
 __device__ __forceinline__ void fused_store(const FuseOut& fo, const uint32_t (*lm)[256], uint32_t tile,
                                             float* acc, float so, int nvalid, int lane) {
-  if (fo.fast && nvalid == EPI_COLS / 2) {
+  if (fo.fast && nvalid == 4 * fo.nslot) {
     // butterfly exchanges: slot q = complex 4q..4q+3 = floats 8q..8q+7
 #pragma unroll
     for (int j = 0; j < 3; ++j) {
@@ -305,7 +305,8 @@ __device__ __forceinline__ void fused_store(const FuseOut& fo, const uint32_t (*
     for (int b = 0; b < 5; ++b)
       if ((lane >> b) & 1) a |= fo.lane_w[b];
 #pragma unroll
-    for (int q = 0; q < 8; ++q) store_slot<MODE>(fo, a | fo.slot_w[q], acc + 8 * q, so);
+    for (int q = 0; q < 8; ++q)
+      if (q < fo.nslot) store_slot<MODE>(fo, a | fo.slot_w[q], acc + 8 * q, so);
   } else {
     const uint32_t base = tile | (lm != nullptr ? lut_lookup_s(lm, (uint32_t)lane)
                                                 : lut_lookup(fo.lut_m, (uint32_t)lane));

@@ -587,25 +587,28 @@ void plan_tensor_core_steps(Program* P) {
     build_fuse_map(i, s, f, nvec, mvec);
     const int ln = (int)nvec.size();
     // fast path: vector bits n0,n1 -> destination bits 0,1; the lanes take
-    // the 5 thread-local source bits (slot bits n2..n4, lane bits m0..m4)
-    // with the lowest destination bits, swapped in by butterfly exchanges
+    // the 5 thread-local source bits (slot bits n2..n(1+sb), lane bits
+    // m0..m4) with the lowest destination bits, swapped in by butterfly
+    // exchanges.  sb = 3 slot bits (32 complex per thread); sb = 2 for
+    // 16-column results (narrow consumers' operands)
     f.fast = 0;
     static const int fast_env = env_int("TNB_FUSE_FAST", 1);
-    if (fast_env && ln >= 5 && (int)mvec.size() >= 5 && nvec[0] == 0 && nvec[1] == 1) {
-      std::vector<std::pair<int, int>> loc;  // (destination bit, local bit: 0-2 slot, 3-7 lane)
-      for (int j = 0; j < 3; ++j) loc.push_back({nvec[2 + j], j});
-      for (int b = 0; b < 5; ++b) loc.push_back({mvec[b], 3 + b});
+    if (fast_env && ln >= 4 && (int)mvec.size() >= 5 && nvec[0] == 0 && nvec[1] == 1) {
+      const int sb = std::min(3, ln - 2);
+      std::vector<std::pair<int, int>> loc;  // (destination bit, local bit: 0..sb-1 slot, sb.. lane)
+      for (int j = 0; j < sb; ++j) loc.push_back({nvec[2 + j], j});
+      for (int b = 0; b < 5; ++b) loc.push_back({mvec[b], sb + b});
       std::sort(loc.begin(), loc.end());
-      std::vector<char> on_lane(8, 0);
+      std::vector<char> on_lane(sb + 5, 0);
       for (int x = 0; x < 5; ++x) on_lane[loc[x].second] = 1;
-      int dslot[3], dlane[5];
-      for (int j = 0; j < 3; ++j) dslot[j] = nvec[2 + j];
+      int dslot[3] = {0, 0, 0}, dlane[5];
+      for (int j = 0; j < sb; ++j) dslot[j] = nvec[2 + j];
       for (int b = 0; b < 5; ++b) dlane[b] = mvec[b];
       int b = 0;
       for (int j = 0; j < 3; ++j) {
         f.xlane[j] = 0;
-        if (!on_lane[j]) continue;              // slot bit stays in the registers
-        while (on_lane[3 + b]) ++b;             // a lane bit that must leave the lanes
+        if (j >= sb || !on_lane[j]) continue;   // slot bit stays in the registers
+        while (on_lane[sb + b]) ++b;            // a lane bit that must leave the lanes
         f.xlane[j] = 1 << b;
         std::swap(dslot[j], dlane[b]);
         ++b;
@@ -613,10 +616,11 @@ void plan_tensor_core_steps(Program* P) {
       for (int bb = 0; bb < 5; ++bb) f.lane_w[bb] = 1u << dlane[bb];
       for (int q = 0; q < 8; ++q) {
         uint32_t v = 0;
-        for (int j = 0; j < 3; ++j)
+        for (int j = 0; j < sb; ++j)
           if ((q >> j) & 1) v |= 1u << dslot[j];
         f.slot_w[q] = v;
       }
+      f.nslot = 1 << sb;
       f.fast = 1;
     }
     debug_fuse(i, s, f, nvec, mvec);

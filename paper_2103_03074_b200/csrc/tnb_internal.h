@@ -215,6 +215,7 @@ struct FuseOut {
   int xlane[3] = {0, 0, 0};      // lane xor mask exchanged with slot bit j (0: none)
   uint32_t lane_w[5] = {};       // destination weight of lane bit b (after exchanges)
   uint32_t slot_w[8] = {};       // destination offset of slot q (after exchanges)
+  int nslot = 8;                 // fast path: 4-complex slots per thread (8, or 4 at 16 columns)
   __half2* hi = nullptr;
   __half2* lo = nullptr;
   const ByteLut* lut_m = nullptr;
