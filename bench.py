@@ -671,6 +671,35 @@ def run_ours(args):
 
     batched_slices = _run_leg("batched_slices", _leg_batched_slices)
 
+    # ---- optional: double precision (the reference's default, engine.py:248):
+    # the same slices on the fp64 path (SIMT; tcgen05 has no fp64 mode)
+    def _leg_double():
+        if not args.double:
+            return None
+        E.clear_cache()
+        dp = E.head_program(tn, tree, w.sliced, "double", device=local)
+        dp.set_timing(2)
+        d0 = base
+        dp.run_range(d0, d0 + 1, "fixed")  # compile + warm
+        barrier(dist, local)
+        d_ms = 0.0
+        for s_ in range(args.double):
+            dp.run_range(d0 + 1 + s_, d0 + 2 + s_, "fixed")
+            d_ms += dp.timing()["total_ms"]
+        if dist is not None:
+            tt_ = torch.tensor([d_ms], device=dev)
+            dist.all_reduce(tt_, op=dist.ReduceOp.MAX)
+            d_ms = float(tt_.item())
+        sps = world * args.double / (d_ms / 1e3)
+        del dp
+        E.clear_cache()
+        return {"slices_per_s": sps, "contraction_tflops": sps * 8.0 * w.tc_per_slice / 1e12,
+                "slices_per_gpu": args.double,
+                "note": "precision='double' (complex128; the reference's default) on the fp64 SIMT "
+                        "path, same slices and tree as the headline; device time"}
+
+    double_leg = _run_leg("double", _leg_double)
+
     # ---- optional: cross-slice reuse (TNB_FLAG_REUSE_SLICES) -- reported beside the
     # headline, NOT as it: it skips re-computing results whose mask bits did not change
     reuse = None
@@ -775,6 +804,7 @@ def run_ours(args):
         "co_optimised_plan": opt_plan,
         "reordered_same_slices": reordered,
         "batched_slices": batched_slices,
+        "double_precision": double_leg,
         # linear XEB (analytics.py:46-58) of the synthetic partial amplitudes
         # accumulated over every bench step (the fixed slice subset)
         "xeb_partial_subset": float((2.0 ** 53 / amps_total.numel())
@@ -959,6 +989,8 @@ def main():
     ap.add_argument("--reordered-slices", type=int, default=16)
     ap.add_argument("--batch-slices", type=int, default=4,
                     help="also time 2^k-slice blocks per contraction (slice_batch.py; 0 = off)")
+    ap.add_argument("--double", type=int, default=1,
+                    help="also time N head slices in double precision (reported separately; 0 = off)")
     ap.add_argument("--batch-s1", type=int, default=4,
                     help="also time 2^b closed-bit assignments per head pass (reported separately)")
     args = ap.parse_args()
