@@ -144,6 +144,85 @@ __device__ __forceinline__ void simt_tile(const T* __restrict__ A, const T* __re
   if (max_out) block_max_atomic(vmax, max_out);
 }
 
+// Wide tiles for big SIMT steps (the fp64 path): 64x64 outputs per block,
+// 4x4 per thread, K in blocks of 16 staged through shared memory with the
+// same LUT gathers as simt_tile.  Four times the FMAs per shared-memory load
+// of the 32x32 tile (2 vs 0.5 flop/B), so the big complex128 GEMMs of a slice
+// run on the FP64 pipe instead of shared-memory bandwidth.
+template <typename T>
+__global__ void __launch_bounds__(256, 2)
+contract_wide_kernel(const T* __restrict__ A, const T* __restrict__ B, T* __restrict__ C,
+                     int64_t M, int64_t N, int64_t K, const ByteLut* __restrict__ gla,
+                     const ByteLut* __restrict__ glb, unsigned int* __restrict__ max_out) {
+  using S = typename Scalar<T>::type;
+  constexpr int BM = 64, BN = 64, BK = 16;
+  __shared__ uint32_t la[4][256];
+  __shared__ uint32_t lb[4][256];
+  __shared__ T As[BK][BM + 1];
+  __shared__ T Bs[BK][BN + 1];
+  const int tid = threadIdx.x;
+  for (int i = tid; i < 1024; i += 256) {
+    la[i >> 8][i & 255] = gla->t[i >> 8][i & 255];
+    lb[i >> 8][i & 255] = glb->t[i >> 8][i & 255];
+  }
+  const int64_t nbn = (N + BN - 1) / BN;
+  const int64_t m0 = ((int64_t)blockIdx.x / nbn) * BM, n0 = ((int64_t)blockIdx.x % nbn) * BN;
+  const int tx = tid & 15, ty = tid >> 4;
+  S acc_re[4][4], acc_im[4][4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc_re[i][j] = acc_im[i][j] = 0;
+  __syncthreads();
+  for (int64_t k0 = 0; k0 < K; k0 += BK) {
+    // consecutive threads take consecutive k of one row: the canonical
+    // index m*K + k keeps its low (k) bits within a warp's 16-lane runs
+#pragma unroll
+    for (int r = 0; r < (BM * BK) / 256; ++r) {
+      const int i = tid + 256 * r;
+      const int mm = i / BK, kk = i % BK;
+      const int64_t m = m0 + mm, k = k0 + kk;
+      T v; v.x = 0; v.y = 0;
+      if (m < M && k < K) v = A[lut_map(la, (uint32_t)(m * K + k))];
+      As[kk][mm] = v;
+      const int64_t n = n0 + mm;
+      T u; u.x = 0; u.y = 0;
+      if (n < N && k < K) u = B[lut_map(lb, (uint32_t)(n * K + k))];
+      Bs[kk][mm] = u;
+    }
+    __syncthreads();
+#pragma unroll 4
+    for (int kk = 0; kk < BK; ++kk) {
+      T av[4], bv[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) av[i] = As[kk][ty + 16 * i];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) bv[j] = Bs[kk][tx + 16 * j];
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          acc_re[i][j] += av[i].x * bv[j].x - av[i].y * bv[j].y;
+          acc_im[i][j] += av[i].x * bv[j].y + av[i].y * bv[j].x;
+        }
+    }
+    __syncthreads();
+  }
+  float vmax = 0.f;
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int64_t m = m0 + ty + 16 * i, n = n0 + tx + 16 * j;
+      if (m < M && n < N) {
+        T v; v.x = acc_re[i][j]; v.y = acc_im[i][j];
+        C[m * N + n] = v;
+        vmax = fmaxf(vmax, (float)fmax(fabs(v.x), fabs(v.y)));
+      }
+    }
+  if (max_out) block_max_atomic(vmax, max_out);
+}
+
 template <typename T>
 __global__ void __launch_bounds__(256)
 contract_simt_kernel(const T* __restrict__ A, const T* __restrict__ B, T* __restrict__ C,
@@ -597,6 +676,13 @@ void launch_contract_simt(const T* A, const T* B, T* C, int64_t M, int64_t N, in
     return;
   }
   if (fuse && fuse->mode != 0) throw Error(TNB_ERR_SHAPE, "fused output planned for a tiled SIMT step");
+  if (simt_uses_wide(M, N, K)) {
+    const int64_t wb = ((M + 63) / 64) * ((N + 63) / 64);
+    if (wb > 0x7fffffffll) throw Error(TNB_ERR_SHAPE, "SIMT contraction too large");
+    contract_wide_kernel<T><<<(unsigned)wb, 256, 0, s>>>(A, B, C, M, N, K, lutA, lutB, max_out);
+    check_launch("contract_wide");
+    return;
+  }
   const int64_t blocks = ((M + 31) / 32) * ((N + 31) / 32);
   if (blocks > 0x7fffffffll) throw Error(TNB_ERR_SHAPE, "SIMT contraction too large");
   contract_simt_kernel<T><<<(unsigned)blocks, 256, 0, s>>>(A, B, C, M, N, K, lutA, lutB, max_out);

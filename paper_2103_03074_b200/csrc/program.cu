@@ -374,7 +374,7 @@ void plan_simt_batches(Program* P) {
         StepRec& s = P->steps[i];
         if ((int)s.hoisted != seq) continue;  // seq 1: hoisted pass, seq 0: per slice
         const bool cand = s.kind == KIND_SIMT && !simt_uses_smallk(s.M, s.N, s.K) &&
-                          P->tensors[s.out].fuse_role == 0;
+                          !simt_uses_wide(s.M, s.N, s.K) && P->tensors[s.out].fuse_role == 0;
         if (!cand) { close(); continue; }
         bool dep = false;
         for (int m : cur)

@@ -147,6 +147,11 @@ void launch_contract_simt_batch(const SimtStepDesc* descs, int n, int64_t blocks
 inline bool simt_uses_smallk(int64_t M, int64_t N, int64_t K) {
   return K <= 8 && N >= 4 && M * N >= (1 << 16);
 }
+// ... or the 64x64-tile kernel (4x4 outputs per thread; the big steps of the
+// fp64 path, which has no tensor-core mode); never batched
+inline bool simt_uses_wide(int64_t M, int64_t N, int64_t K) {
+  return !simt_uses_smallk(M, N, K) && M >= 64 && N >= 64 && K >= 16;
+}
 
 template <typename T>
 void launch_permute(const T* in, T* out, int64_t elems, const ByteLut* lut, cudaStream_t s);
@@ -265,6 +270,7 @@ struct TcGemmPlan {
   unsigned int* progress = nullptr;  // device [num units]: K-block progress for soft pacing
   int pace_slack = 0;            // K blocks a unit may lead the slowest one (0: off)
   int epi_spin = 0;              // epilogue polls the TMEM-ready barrier instead of sleeping
+  int k_rev = 0;                 // odd rounds of the persistent grid stream K backwards
   int64_t k_per_split = 0;       // multiple of the K block
   int grid = 0;
   alignas(64) unsigned char tmap[4][128];  // CUtensorMap x4: Ahi, Alo, Bhi, Blo
