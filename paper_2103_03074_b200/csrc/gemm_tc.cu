@@ -366,7 +366,7 @@ gemm_f16x3_kernel(const __grid_constant__ CUtensorMap tm_ahi, const __grid_const
                   float* __restrict__ C, int M, int Np, int Kp, int splits, int k_per_split,
                   int chunk_kb, int group_m, const ScaleSrc scale_rows, const ScaleSrc scale_cols,
                   unsigned int* __restrict__ max_out, unsigned int* __restrict__ progress,
-                  int pace_slack, const __grid_constant__ FuseOut fo, int epi_spin, int k_rev) {
+                  int pace_slack, const __grid_constant__ FuseOut fo, int epi_spin) {
   using CF = Cfg<CG, NB>;
   constexpr int STAGES = CF::STAGES;
   // fp16 scale-guard re-run of a fused producer: nothing to do unless the
@@ -456,13 +456,7 @@ gemm_f16x3_kernel(const __grid_constant__ CUtensorMap tm_ahi, const __grid_const
       const int k_end = min(Kp, k_begin + k_per_split);
       const int m0 = wc.mb * BM * CG + (int)rank * BM;
       const int n0 = wc.nb * NB + (int)rank * CF::B_ROWS;
-      // k_rev: every other round of the persistent grid streams K backwards,
-      // so a round starts on the K blocks the previous round (same raster
-      // band, same A panels) left in L2
-      const bool rev = k_rev && (((w - unit) / n_units) & 1);
-      const int nkb_t = (k_end - k_begin + BK - 1) / BK;
-      for (int kb_i = 0; kb_i < nkb_t; ++kb_i, ++issued) {
-        const int k = k_begin + (rev ? nkb_t - 1 - kb_i : kb_i) * BK;
+      for (int k = k_begin; k < k_end; k += BK, ++issued) {
         if (pace && (issued & 15) == 0) {
           if (lane == 0) atomicExch(progress + unit, issued);
           for (;;) {
@@ -813,8 +807,6 @@ void tc_plan_gemm(TcGemmPlan* p, const __half* Ahi, const __half* Alo, const __h
   const double small_mb = (double)std::min(M, Np) * (double)Kp * 4.0 / 1048576.0;
   p->pace_slack = kblocks / p->splits >= pace_min_kb && small_mb >= pace_min_mb
                       ? env_int("TNB_PACE", kDefaultPaceSlack) : 0;
-  static const int k_rev = env_int("TNB_KREV", 0);
-  p->k_rev = k_rev;
   static const int spin = env_int("TNB_EPI_SPIN", -1);
   p->epi_spin = spin >= 0 ? spin : 0;
   const int b_rows = p->nb / p->cta_group;
@@ -846,7 +838,7 @@ void launch_cg(const TcGemmPlan* p, cudaStream_t s) {
   TNB_CUDA(cudaLaunchKernelEx(&cfg, kern, maps[0], maps[1], maps[2], maps[3], p->C, (int)p->M,
                               (int)p->Np, (int)p->Kp, p->splits, (int)p->k_per_split, p->chunk_kb,
                               p->group_m, p->scale_rows, p->scale_cols, p->max_out, p->progress,
-                              p->pace_slack, p->fuse, p->epi_spin, p->k_rev));
+                              p->pace_slack, p->fuse, p->epi_spin));
 }
 
 void tc_launch_gemm(const TcGemmPlan* p, cudaStream_t s) {

@@ -270,7 +270,6 @@ struct TcGemmPlan {
   unsigned int* progress = nullptr;  // device [num units]: K-block progress for soft pacing
   int pace_slack = 0;            // K blocks a unit may lead the slowest one (0: off)
   int epi_spin = 0;              // epilogue polls the TMEM-ready barrier instead of sleeping
-  int k_rev = 0;                 // odd rounds of the persistent grid stream K backwards
   int64_t k_per_split = 0;       // multiple of the K block
   int grid = 0;
   alignas(64) unsigned char tmap[4][128];  // CUtensorMap x4: Ahi, Alo, Bhi, Blo
