@@ -150,7 +150,7 @@ __device__ __forceinline__ void simt_tile(const T* __restrict__ A, const T* __re
 // of the 32x32 tile (2 vs 0.5 flop/B), so the big complex128 GEMMs of a slice
 // run on the FP64 pipe instead of shared-memory bandwidth.
 template <typename T>
-__global__ void __launch_bounds__(256, 2)
+__global__ void __launch_bounds__(256, sizeof(T) == 16 ? 1 : 2)
 contract_wide_kernel(const T* __restrict__ A, const T* __restrict__ B, T* __restrict__ C,
                      int64_t M, int64_t N, int64_t K, const ByteLut* __restrict__ gla,
                      const ByteLut* __restrict__ glb, unsigned int* __restrict__ max_out) {
@@ -174,23 +174,34 @@ contract_wide_kernel(const T* __restrict__ A, const T* __restrict__ B, T* __rest
 #pragma unroll
     for (int j = 0; j < 4; ++j) acc_re[i][j] = acc_im[i][j] = 0;
   __syncthreads();
-  for (int64_t k0 = 0; k0 < K; k0 += BK) {
-    // consecutive threads take consecutive k of one row: the canonical
-    // index m*K + k keeps its low (k) bits within a warp's 16-lane runs
+  // software pipeline: the gathers of K block k0 + BK are in flight (in
+  // registers) while block k0 is multiplied out of shared memory
+  constexpr int LOADS = (BM * BK) / 256;
+  T pa[LOADS], pb[LOADS];
+  auto gather = [&](int64_t k0) {
 #pragma unroll
-    for (int r = 0; r < (BM * BK) / 256; ++r) {
+    for (int r = 0; r < LOADS; ++r) {
+      // consecutive threads take consecutive k of one row: the canonical
+      // index m*K + k keeps its low (k) bits within a warp's 16-lane runs
       const int i = tid + 256 * r;
       const int mm = i / BK, kk = i % BK;
-      const int64_t m = m0 + mm, k = k0 + kk;
-      T v; v.x = 0; v.y = 0;
-      if (m < M && k < K) v = A[lut_map(la, (uint32_t)(m * K + k))];
-      As[kk][mm] = v;
-      const int64_t n = n0 + mm;
-      T u; u.x = 0; u.y = 0;
-      if (n < N && k < K) u = B[lut_map(lb, (uint32_t)(n * K + k))];
-      Bs[kk][mm] = u;
+      const int64_t m = m0 + mm, n = n0 + mm, k = k0 + kk;
+      pa[r].x = 0; pa[r].y = 0;
+      pb[r].x = 0; pb[r].y = 0;
+      if (m < M && k < K) pa[r] = A[lut_map(la, (uint32_t)(m * K + k))];
+      if (n < N && k < K) pb[r] = B[lut_map(lb, (uint32_t)(n * K + k))];
+    }
+  };
+  gather(0);
+  for (int64_t k0 = 0; k0 < K; k0 += BK) {
+#pragma unroll
+    for (int r = 0; r < LOADS; ++r) {
+      const int i = tid + 256 * r;
+      As[i % BK][i / BK] = pa[r];
+      Bs[i % BK][i / BK] = pb[r];
     }
     __syncthreads();
+    if (k0 + BK < K) gather(k0 + BK);
 #pragma unroll 4
     for (int kk = 0; kk < BK; ++kk) {
       T av[4], bv[4];
@@ -220,6 +231,114 @@ contract_wide_kernel(const T* __restrict__ A, const T* __restrict__ B, T* __rest
         vmax = fmaxf(vmax, (float)fmax(fabs(v.x), fabs(v.y)));
       }
     }
+  if (max_out) block_max_atomic(vmax, max_out);
+}
+
+// fp64 tensor-core (DMMA, mma.sync m8n8k4 f64) variant of the wide tile for
+// complex128 steps: same 64x64 output tile, K blocks of 16 gathered through
+// the LUTs into planar (re | im) shared-memory tiles, 8 warps of 32x16
+// outputs, four real products per complex fragment (re += ar br - ai bi,
+// im += ar bi + ai br).  Exact IEEE fp64 products and sums, like the FMA path.
+__device__ __forceinline__ void dmma_8x8x4(double (&d)[2], double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+               : "+d"(d[0]), "+d"(d[1])
+               : "d"(a), "d"(b));
+}
+
+__global__ void __launch_bounds__(256, 1)
+contract_dmma_kernel(const double2* __restrict__ A, const double2* __restrict__ B,
+                     double2* __restrict__ C, int64_t M, int64_t N, int64_t K,
+                     const ByteLut* __restrict__ gla, const ByteLut* __restrict__ glb,
+                     unsigned int* __restrict__ max_out) {
+  constexpr int BM = 64, BN = 64, BK = 16, PAD = 8, LD = BM + PAD;
+  __shared__ uint32_t la[4][256];
+  __shared__ uint32_t lb[4][256];
+  __shared__ double As[2][BK][LD];  // [re|im][k][m]
+  __shared__ double Bs[2][BK][LD];  // [re|im][k][n]
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  for (int i = tid; i < 1024; i += 256) {
+    la[i >> 8][i & 255] = gla->t[i >> 8][i & 255];
+    lb[i >> 8][i & 255] = glb->t[i >> 8][i & 255];
+  }
+  const int64_t nbn = (N + BN - 1) / BN;
+  const int64_t m0 = ((int64_t)blockIdx.x / nbn) * BM, n0 = ((int64_t)blockIdx.x % nbn) * BN;
+  const int wm = (warp >> 2) * 32, wn = (warp & 3) * 16;  // warp tile origin
+  double acc[4][2][2][2];  // [m frag][n frag][re|im][2 values]
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 2; ++j)
+#pragma unroll
+      for (int c = 0; c < 2; ++c) acc[i][j][c][0] = acc[i][j][c][1] = 0.0;
+  __syncthreads();
+  constexpr int LOADS = (BM * BK) / 256;
+  double2 pa[LOADS], pb[LOADS];
+  auto gather = [&](int64_t k0) {
+#pragma unroll
+    for (int r = 0; r < LOADS; ++r) {
+      const int i = tid + 256 * r;
+      const int mm = i / BK, kk = i % BK;
+      const int64_t m = m0 + mm, n = n0 + mm, k = k0 + kk;
+      pa[r] = make_double2(0.0, 0.0);
+      pb[r] = make_double2(0.0, 0.0);
+      if (m < M && k < K) pa[r] = A[lut_map(la, (uint32_t)(m * K + k))];
+      if (n < N && k < K) pb[r] = B[lut_map(lb, (uint32_t)(n * K + k))];
+    }
+  };
+  gather(0);
+  const int fr = lane >> 2, fk = lane & 3;  // fragment row/col and k
+  for (int64_t k0 = 0; k0 < K; k0 += BK) {
+#pragma unroll
+    for (int r = 0; r < LOADS; ++r) {
+      const int i = tid + 256 * r;
+      const int mm = i / BK, kk = i % BK;
+      As[0][kk][mm] = pa[r].x;
+      As[1][kk][mm] = pa[r].y;
+      Bs[0][kk][mm] = pb[r].x;
+      Bs[1][kk][mm] = pb[r].y;
+    }
+    __syncthreads();
+    if (k0 + BK < K) gather(k0 + BK);
+#pragma unroll
+    for (int k4 = 0; k4 < BK; k4 += 4) {
+      double ar[4], ai[4], br[2], bi[2], bn[2];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        ar[i] = As[0][k4 + fk][wm + 8 * i + fr];
+        ai[i] = As[1][k4 + fk][wm + 8 * i + fr];
+      }
+#pragma unroll
+      for (int j = 0; j < 2; ++j) {
+        br[j] = Bs[0][k4 + fk][wn + 8 * j + fr];
+        bi[j] = Bs[1][k4 + fk][wn + 8 * j + fr];
+        bn[j] = -bi[j];
+      }
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {
+          dmma_8x8x4(acc[i][j][0], ar[i], br[j]);
+          dmma_8x8x4(acc[i][j][0], ai[i], bn[j]);
+          dmma_8x8x4(acc[i][j][1], ar[i], bi[j]);
+          dmma_8x8x4(acc[i][j][1], ai[i], br[j]);
+        }
+    }
+    __syncthreads();
+  }
+  float vmax = 0.f;
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 2; ++j)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int64_t m = m0 + wm + 8 * i + fr, n = n0 + wn + 8 * j + 2 * fk + e;
+        if (m < M && n < N) {
+          const double2 v = make_double2(acc[i][j][0][e], acc[i][j][1][e]);
+          C[m * N + n] = v;
+          vmax = fmaxf(vmax, (float)fmax(fabs(v.x), fabs(v.y)));
+        }
+      }
   if (max_out) block_max_atomic(vmax, max_out);
 }
 
@@ -679,6 +798,14 @@ void launch_contract_simt(const T* A, const T* B, T* C, int64_t M, int64_t N, in
   if (simt_uses_wide(M, N, K)) {
     const int64_t wb = ((M + 63) / 64) * ((N + 63) / 64);
     if (wb > 0x7fffffffll) throw Error(TNB_ERR_SHAPE, "SIMT contraction too large");
+    static const int dmma = [] { const char* e = getenv("TNB_DMMA"); return e ? atoi(e) : 1; }();
+    if constexpr (std::is_same<T, double2>::value) {
+      if (dmma) {
+        contract_dmma_kernel<<<(unsigned)wb, 256, 0, s>>>(A, B, C, M, N, K, lutA, lutB, max_out);
+        check_launch("contract_dmma");
+        return;
+      }
+    }
     contract_wide_kernel<T><<<(unsigned)wb, 256, 0, s>>>(A, B, C, M, N, K, lutA, lutB, max_out);
     check_launch("contract_wide");
     return;
