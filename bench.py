@@ -672,7 +672,7 @@ def run_ours(args):
     batched_slices = _run_leg("batched_slices", _leg_batched_slices)
 
     # ---- optional: double precision (the reference's default, engine.py:248):
-    # the same slices on the fp64 path (SIMT; tcgen05 has no fp64 mode)
+    # the same slices on the fp64 path (DMMA / FMA; tcgen05 has no fp64 kind)
     def _leg_double():
         if not args.double:
             return None
@@ -695,8 +695,9 @@ def run_ours(args):
         E.clear_cache()
         return {"slices_per_s": sps, "contraction_tflops": sps * 8.0 * w.tc_per_slice / 1e12,
                 "slices_per_gpu": args.double,
-                "note": "precision='double' (complex128; the reference's default) on the fp64 SIMT "
-                        "path, same slices and tree as the headline; device time"}
+                "note": "precision='double' (complex128; the reference's default) on the fp64 path "
+                        "(DMMA mma.sync m8n8k4 for the big steps, FMA for the rest), same slices and "
+                        "tree as the headline; device time"}
 
     double_leg = _run_leg("double", _leg_double)
 
