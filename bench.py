@@ -186,6 +186,19 @@ def rank_inventory(dist, local):
     return ranks, active, comm
 
 
+def agree_min(dist, dev, v: int) -> int:
+    """The minimum of an integer choice over ranks (plan choices made by
+    time-budgeted host searches can differ between ranks; the legs' later
+    collectives need every rank on the same branch)."""
+    if dist is None:
+        return v
+    import torch
+
+    t = torch.tensor([int(v)], device=dev, dtype=torch.int64)
+    dist.all_reduce(t, op=dist.ReduceOp.MIN)
+    return int(t.item())
+
+
 def barrier(dist, local):
     import torch
 
@@ -503,6 +516,7 @@ def run_ours(args):
                     break
                 except (tnb.ShapeMismatch, tnb.TncutError, ValueError):
                     ko = 0
+            ko = agree_min(dist, dev, ko)  # time-budgeted planning may differ per rank
             if ko:
                 bo = SB.batched_program(wo.tn, wo.tree, wo.sliced, ko, "single", local, max_rank=32)
                 bo.set_timing(2)
@@ -616,6 +630,7 @@ def run_ours(args):
                     kb -= 1
                     if kb == 0:
                         raise
+            kb = agree_min(dist, dev, kb)  # every rank runs the same block width
             bp = SB.batched_program(tn, tree, w.sliced, kb, "single", local)
             bp.set_timing(2)
             Bb = 4  # blocks per step

@@ -70,3 +70,52 @@ def test_bench_two_ranks_share_one_gpu(gpu):
     assert line["n_gpus"] == 2 and line["communicator"]["size"] == 2
     assert line["gpus_active"] == 1 and line["value"] > 0
     assert line["gpu_launches"] > 0
+
+
+@pytest.mark.gpu
+def test_bench_two_ranks_all_legs_c2(gpu):
+    """Every optional leg on 2 ranks (gloo, shared GPU) on the smaller C2
+    plan: the legs' collectives (plan-choice agreement, max-over-ranks
+    times) line up on both ranks and rank 0 prints one complete line."""
+    line = _run(["--gpus", "2", "--workload", "c2", "--steps", "1", "--warmup", "1", "--slices", "1",
+                 "--no-cpu", "--reuse", "1", "--opt-plan", "1", "--opt-slices", "1", "--reordered", "1",
+                 "--reordered-slices", "2", "--batch-slices", "2", "--batch-s1", "2", "--double", "1"],
+                {"TNB_SHARE_DEVICE": "1", "TNB_DIST_BACKEND": "gloo"}, 1500)
+    assert line["n_gpus"] == 2 and line["value"] > 0
+    assert line["e2e"]["value"] > 0
+    for leg in ("batched_s1", "co_optimised_plan", "batched_slices", "double_precision",
+                "cross_slice_reuse"):
+        assert line[leg] is not None and "unavailable" not in line[leg], (leg, line[leg])
+
+
+def test_reference_arm_times_real_reference_slices():
+    """--impl reference: the unmodified reference engine (baseline/_ref or the
+    reference tree) on real slices, no extrapolation (C1 here: fast)."""
+    import importlib.util
+
+    if not (os.path.isdir(os.path.join(ROOT, "baseline", "_ref", "tncut"))
+            or os.path.isdir("/root/reference/pkg/src/tncut")):
+        pytest.skip("reference package not present")
+    if importlib.util.find_spec("numba") is None:
+        pytest.skip("reference dependencies missing")
+    line = _run(["--impl", "reference", "--workload", "c1", "--steps", "3", "--warmup", "1"], {}, 300)
+    assert line["impl"] == "reference" and line["value"] > 0
+    assert line["steps"] == 3 and line["requested_steps"] == 3 and len(line["per_slice_s"]) == 3
+    assert line["cpu_baseline"]["kind"] == "reference"
+    assert line["e2e"]["h2d_bytes_per_step"] == 0
+    assert abs(line["value"] - 3 / sum(line["per_slice_s"])) < 1e-9 * line["value"]
+
+
+def test_reference_arm_budget_caps_the_timed_slices(monkeypatch):
+    """Slices stop once the next one would overrun the budget (the driver's
+    step budget cannot hold K full C4 slices); the line says so."""
+    import importlib.util
+
+    if importlib.util.find_spec("numba") is None or not (
+            os.path.isdir(os.path.join(ROOT, "baseline", "_ref", "tncut"))
+            or os.path.isdir("/root/reference/pkg/src/tncut")):
+        pytest.skip("reference package not present")
+    line = _run(["--impl", "reference", "--workload", "c1", "--steps", "50", "--warmup", "0",
+                 "--ref-budget-s", "0"], {}, 300)
+    assert line["steps"] == 1 and line["requested_steps"] == 50
+    assert "fit" in line["steps_note"]
