@@ -2,6 +2,7 @@
     python scripts/diag_tree.py given c4 2        # reference tree, 2 slices
     python scripts/diag_tree.py reordered c4 16   # same slices, re-ordered tree
     python scripts/diag_tree.py batched c4 4      # 2^4 slices per contraction, 1 block
+    python scripts/diag_tree.py plan c4_opt31_b200 1   # a frozen plan's own tree
 One warm-up run first (compile + graphs), then the measured run; with
 TNB_DIAG_SKIP_WARM=1 only the measured run (ncu -c counts stay small)."""
 import os
@@ -17,7 +18,7 @@ mode = sys.argv[1] if len(sys.argv) > 1 else "given"
 name = sys.argv[2] if len(sys.argv) > 2 else "c4"
 n = int(sys.argv[3]) if len(sys.argv) > 3 else 2
 w = tnb.load_workload(name)
-if mode == "given":
+if mode in ("given", "plan"):  # plan: any frozen workload's own tree, e.g. c4_opt31_b200
     prog = E.head_program(w.tn, w.tree, w.sliced, "single", device=0)
     rng = [(0, n), (n, 2 * n)]
 elif mode == "reordered":
