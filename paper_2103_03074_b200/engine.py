@@ -637,8 +637,10 @@ def _tail(tn, tree, head, space_cap, precision, stats, device):
     else:
         amps = np.empty(1 << n2, dtype=dtype)
         w = 1 << (n2 - kb)
-        for j in range(1 << kb):
-            amps[j * w:(j + 1) * w] = prog.run(entries, j, j + 1, "fixed")
+        with prog.lock:  # one upload of the leaves (the head vector), then every block
+            prog._update_leaves(entries)
+            for j in range(1 << kb):
+                amps[j * w:(j + 1) * w] = prog._run_range(j, j + 1, "fixed", None)
     return _make_table(tn, tree, head, amps.astype(dtype, copy=False), open_qubits, precision)
 
 
