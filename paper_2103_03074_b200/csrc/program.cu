@@ -137,6 +137,7 @@ struct StepRec {
   // Program::guard_bits binary orders looser it rewrites the operand scaled
   // by the exact max, else exits at once.  The decision lands in *guard,
   // which the consumer's ScaleSrc follows
+  bool dstage = false;  // fp64 wide step: operands permuted to [M][K] / [N][K] first (scratch)
   bool has_redo = false;
   unsigned int* guard = nullptr;
   TcGemmPlan tc_redo;
@@ -186,6 +187,7 @@ struct Program {
   unsigned int* d_progress = nullptr;  // GEMM soft-pacing counters (one per CTA unit)
   unsigned int* d_guard = nullptr;  // fp16 scale guard words (per tensor slot) + redo counter
   int guard_bits = 18;              // TNB_SCALE_GUARD_BITS at creation (< 0: guard off)
+  int lut_ident = -1;               // identity LUT (staged fp64 operands are canonical)
   std::vector<int> slot;            // tensor -> slot
   int inv_slot_begin = 0, inv_slot_count = 0, var_slot_begin = 0, var_slot_count = 0;
   std::vector<StageTables> stages;  // device views of the TC staging tables
@@ -405,6 +407,7 @@ void plan_memory(Program* P) {
     if (r.def_step >= 0 && r.last_use >= 0 && r.last_use < n_steps) free_after[r.last_use].push_back(t);
   }
   int64_t scratch_bytes = 0;
+  static const int dstage_env = env_int("TNB_DSTAGE", 1);
   std::vector<std::vector<int>> deferred(n_steps + 1);
   for (int i = 0; i < n_steps; ++i) {
     StepRec& s = P->steps[i];
@@ -418,6 +421,22 @@ void plan_memory(Program* P) {
     } else {
       o.pool = POOL_ARENA;
       o.off = arena.alloc(ob) / (int64_t)P->esize;
+    }
+    if (s.kind == KIND_SIMT && s.batch < 0 && P->precision == TNB_DOUBLE && dstage_env &&
+        simt_uses_wide(s.M, s.N, s.K)) {
+      // fp64 wide step: both operands permuted once into canonical row-major
+      // [M][K] / [N][K] (the tile loads are then coalesced instead of gathered
+      // N/64 resp. M/64 times); scratch for this step only, like TC staging
+      s.dstage = true;
+      const int64_t need = align_up(s.M * s.K * 16, kAlign) + s.N * s.K * 16;
+      s.scratch_bytes = need;
+      s.scratch_off = arena.alloc(need);
+      scratch_bytes = std::max(scratch_bytes, need);
+      if (P->lut_ident < 0) {
+        std::vector<int> ident(32);
+        for (int b = 0; b < 32; ++b) ident[b] = b;
+        P->lut_ident = add_lut(P, ident);
+      }
     }
     if (s.kind == KIND_TC) {
       // operand staging (+ split-K workspace) lives in the arena for the
@@ -445,7 +464,7 @@ void plan_memory(Program* P) {
       TensorRec& r = P->tensors[t];
       if (r.pool == POOL_ARENA) arena.release(r.off * (int64_t)P->esize, tensor_bytes(r, (int64_t)P->esize));
     }
-    if (s.kind == KIND_TC && s.scratch_bytes > 0) arena.release(s.scratch_off, s.scratch_bytes);
+    if ((s.kind == KIND_TC || s.dstage) && s.scratch_bytes > 0) arena.release(s.scratch_off, s.scratch_bytes);
   }
   P->persist_elems = persist_off;
   P->arena_bytes = arena.top;
@@ -1444,6 +1463,19 @@ void exec_step(Program* P, StepRec& s, int parts) {
     launch_contract_simt_batch<T>(b.d_descs, b.n, b.blocks, P->stream);
     C.close(2, e);
     C.launches++;
+    return;
+  }
+  if (s.kind == KIND_SIMT && s.dstage) {
+    cudaEvent_t e = C.mark(2);
+    T* ac = (T*)((char*)P->d_arena + s.scratch_off);
+    T* bc = (T*)((char*)P->d_arena + s.scratch_off + align_up(s.M * s.K * 16, kAlign));
+    const ByteLut* id = P->d_luts + P->lut_ident;
+    launch_permute<T>((const T*)P->tensor_ptr(s.a), ac, s.M * s.K, P->d_luts + s.lut_a, P->stream);
+    launch_permute<T>((const T*)P->tensor_ptr(s.b), bc, s.N * s.K, P->d_luts + s.lut_b, P->stream);
+    launch_contract_simt<T>(ac, bc, (T*)P->tensor_ptr(s.out), s.M, s.N, s.K, id, id, nullptr,
+                            nullptr, nullptr, P->stream);
+    C.close(2, e);
+    C.launches += 3;
     return;
   }
   if (s.kind == KIND_SIMT) {
