@@ -110,7 +110,7 @@ class ClockSampler:
 # promotion chunk) changes the executed schedule, so the bench refuses to run
 # with one set unless --allow-knobs marks the line as a diagnostic run.
 _BENCH_ENV_OK = {"TNB_SHARE_DEVICE", "TNB_DIST_BACKEND", "TNB_REF_BUDGET_S", "TNB_PLAN_THREADS",
-                 "TNB_BENCH_FAIL_LEG", "TNB_BENCH_PROFILE_E2E"}
+                 "TNB_BENCH_FAIL_LEG", "TNB_BENCH_FAIL_RANK", "TNB_BENCH_PROFILE_E2E"}
 
 
 def diagnostic_knobs():
@@ -140,9 +140,28 @@ def spawn_ranks(n: int, argv) -> int:
         env = dict(os.environ, RANK=str(r), LOCAL_RANK=str(r), WORLD_SIZE=str(n),
                    LOCAL_WORLD_SIZE=str(n), MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
         procs.append(subprocess.Popen([sys.executable, os.path.abspath(__file__), *argv], env=env))
+    # like torchrun: a rank that fails takes the others down (they would
+    # otherwise wait in their next collective forever)
     rc = 0
-    for p in procs:
-        rc = max(rc, p.wait())
+    live = list(procs)
+    while live:
+        for p in list(live):
+            code = p.poll()
+            if code is None:
+                continue
+            live.remove(p)
+            rc = max(rc, code)
+            if code != 0:
+                for q in live:
+                    q.terminate()
+                for q in live:
+                    try:
+                        q.wait(timeout=30)
+                    except subprocess.TimeoutExpired:
+                        q.kill()
+                live = []
+                break
+        time.sleep(0.2)
     return rc
 
 
@@ -272,6 +291,8 @@ def run_dry(args):
     ranks, active, comm = rank_inventory(dist, local)
     total = (args.warmup + args.steps) * args.slices
     mine = (rank * total, (rank + 1) * total)
+    if os.environ.get("TNB_BENCH_FAIL_RANK") == str(rank):  # test hook: a rank dies before the collective
+        raise SystemExit(f"rank {rank}: injected failure")
     amps = torch.full((1 << 10,), float(rank + 1), dtype=torch.float32)
     t0 = time.perf_counter()
     if dist is not None:

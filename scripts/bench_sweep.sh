@@ -10,7 +10,7 @@ for wl in c5_26 c5_28 c4 c5_32 c5_n21; do
   [ "$wl" = "c5_26" ] && S=8
   [ "$wl" = "c5_28" ] && S=4
   [ "$wl" = "c5_32" ] && S=1
-  timeout -s KILL 600 python bench.py --workload $wl --slices $S --steps 3 --warmup 3 --no-cpu --no-e2e --reuse 1 >> $OUT 2> gpurun_out/sweep_${TAG}_$wl.err
+  timeout -s KILL 600 python bench.py --workload $wl --slices $S --steps 3 --warmup 3 --no-cpu --no-e2e --reuse 1 --double 0 >> $OUT 2> gpurun_out/sweep_${TAG}_$wl.err
   echo "$wl rc=$?"
 done
 python - <<EOF

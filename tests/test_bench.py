@@ -39,6 +39,18 @@ def test_gpus_flag_spawns_ranks_dry_run():
     assert line["allreduce_sum"] == 3.0
 
 
+def test_failed_rank_takes_the_others_down():
+    """A rank that dies before a collective ends the job with a non-zero
+    exit instead of leaving the other ranks waiting forever."""
+    env = {k: v for k, v in os.environ.items() if not k.startswith("TNB_")}
+    for k in ("WORLD_SIZE", "RANK", "LOCAL_RANK", "MASTER_ADDR", "MASTER_PORT"):
+        env.pop(k, None)
+    env.update(TNB_SHARE_DEVICE="1", TNB_BENCH_FAIL_RANK="1")
+    r = subprocess.run([sys.executable, BENCH, "--gpus", "2", "--dry-run", "--steps", "1"],
+                       capture_output=True, text=True, timeout=120, env=env, cwd=ROOT)
+    assert r.returncode != 0 and "injected failure" in r.stderr
+
+
 def test_bench_refuses_executor_knobs():
     env = {k: v for k, v in os.environ.items() if not k.startswith("TNB_")}
     env["TNB_CHUNK_KB"] = "0"
