@@ -988,7 +988,7 @@ Program* program_create(const tnb_program_desc* d) {
   // tensor-core eligibility: big enough to fill 128x256 tiles and amortise
   // staging.  TNB_TC_MIN_RANK (read per program; tests lower it so small
   // random networks exercise the tensor-core and fused-staging paths)
-  const int tc_min_rank = env_int("TNB_TC_MIN_RANK", 27);
+  const int tc_min_rank = env_int("TNB_TC_MIN_RANK", 26);
   const int tc_min_k = env_int("TNB_TC_MIN_K", 3);  // log2 of the smallest shared dimension
   auto tc_eligible = [&](int na, int nb, int nab) {
     return use_tc && nab >= tc_min_k && na + nb + nab >= tc_min_rank && std::max(na, nb) >= 7 &&

@@ -48,7 +48,7 @@ def step_mults(leaf_sets: dict, steps, removed=frozenset()) -> tuple:
     return total, rank
 
 
-def _tiled_simt(na: int, nb: int, nab: int, tc_min_rank: int = 27) -> bool:
+def _tiled_simt(na: int, nb: int, nab: int, tc_min_rank: int = 26) -> bool:
     """Whether the executor runs a step on the tiled SIMT kernel (the only
     kind it batches): not tensor-core eligible (program.cu tc_eligible) and
     not the streaming small-K kernel (tnb_internal.h simt_uses_smallk)."""

@@ -31,7 +31,7 @@ elif mode == "reordered":
 else:
     prog = SB.batched_program(w.tn, w.tree, w.sliced, n, "single", 0)
     rng = [(0, 1), (1, 2)]
-prog.set_timing(2)
+prog.set_timing(int(os.environ.get("TNB_DIAG_TIMING", "2")))
 reps = int(os.environ.get("TNB_DIAG_REPS", "1"))
 rng = rng[:1] + rng[1:] * reps
 if os.environ.get("TNB_DIAG_SKIP_WARM") == "1":
