@@ -21,6 +21,10 @@
 #include <cstdlib>
 #include <mutex>
 
+#ifndef TNB_NB64_GROUPS
+#define TNB_NB64_GROUPS 2
+#endif
+
 namespace tnb {
 namespace {
 
@@ -40,7 +44,7 @@ constexpr int EPI_COLS = 64;                 // fp32 register accumulator column
 template <int NB>
 struct Epi {
   static constexpr int SPLIT = NB / EPI_COLS;     // column groups per TMEM lane quadrant
-  static constexpr int GROUPS = NB == 64 ? 2 : 1; // tile-parallel epilogue groups (<= 384
+  static constexpr int GROUPS = NB == 64 ? TNB_NB64_GROUPS : 1; // tile-parallel epilogue groups (<= 384
                                                   // threads: the 64-float accumulators stay in registers)
   static constexpr int GROUP_THREADS = 128 * SPLIT;
   static constexpr int THREADS = GROUP_THREADS * GROUPS;  // epilogue threads
