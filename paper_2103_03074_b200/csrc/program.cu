@@ -656,8 +656,10 @@ void plan_tensor_core_steps(Program* P) {
       f.lut_n = P->d_fuse_luts + 2 * e + 1;
     }
   }
-  // scale-guard re-runs of every fused producer: the same launch, gated on
-  // the guard word, scaling by the result's exact max
+  // scale-guard re-runs of every fused producer: the same launch again; its
+  // prologue decides (bound vs the result's exact max) whether to rewrite the
+  // operand scaled by the exact max, records that in the guard word the
+  // consumer's ScaleSrc reads, and otherwise exits at once
   if (P->guard_bits >= 0) {
     for (int i = 0; i < n_steps; ++i) {
       StepRec& st = P->steps[i];

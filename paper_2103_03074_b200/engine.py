@@ -270,15 +270,15 @@ class Program:
             return self._run_range(a, b, mode, out)
 
     def _run_range(self, a, b, mode, out):
-        if True:
-            if out is None:
-                res = _host_array(self.info.out_elems, self.dtype)
-                _lib.check(self.lib.tnb_program_run_range(
-                    self.handle, a, b, _MODES[mode], res.ctypes.data_as(C.c_void_p), 0))
-                return res
+        """run_range without the lock (callers hold it)."""
+        if out is None:
+            res = _host_array(self.info.out_elems, self.dtype)
             _lib.check(self.lib.tnb_program_run_range(
-                self.handle, a, b, _MODES[mode], C.c_void_p(out), 1))
-            return None
+                self.handle, a, b, _MODES[mode], res.ctypes.data_as(C.c_void_p), 0))
+            return res
+        _lib.check(self.lib.tnb_program_run_range(
+            self.handle, a, b, _MODES[mode], C.c_void_p(out), 1))
+        return None
 
     def set_timing(self, on) -> None:
         """False/0 off, True/1 every kernel class, 2 GEMM launches + total only."""
@@ -430,9 +430,9 @@ def head_vector_to_device(tn, tree, sliced_indices, s1, out, slice_range=None,
     """``compute_head_vector`` whose 2^n_c result stays in device memory: it is
     written to ``out`` (a caller-owned contiguous torch CUDA tensor of the
     precision's complex dtype on ``device``; the call returns after the device
-    finished).  The returned HeadVector carries
-    the metadata with ``data=None``.  Used by the sharded (multi-GPU) path so
-    head -> tail -> all-reduce never round-trips through the host."""
+    finished).  The returned HeadVector carries the metadata with
+    ``data=None``.  Used by the sharded (multi-GPU) path so head -> tail ->
+    all-reduce never round-trips through the host."""
     _check_out(out, precision)
     return _head(tn, tree, sliced_indices, s1, slice_range, precision, mode, stats, device,
                  out, batch_ok=False)
