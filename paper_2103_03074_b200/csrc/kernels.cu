@@ -239,13 +239,16 @@ contract_wide_kernel(const T* __restrict__ A, const T* __restrict__ B, T* __rest
 // the LUTs into planar (re | im) shared-memory tiles, 8 warps of 32x16
 // outputs, four real products per complex fragment (re += ar br - ai bi,
 // im += ar bi + ai br).  Exact IEEE fp64 products and sums, like the FMA path.
+#ifndef TNB_DMMA_BLOCKS
+#define TNB_DMMA_BLOCKS 1
+#endif
 __device__ __forceinline__ void dmma_8x8x4(double (&d)[2], double a, double b) {
   asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
                : "+d"(d[0]), "+d"(d[1])
                : "d"(a), "d"(b));
 }
 
-__global__ void __launch_bounds__(256, 1)
+__global__ void __launch_bounds__(256, TNB_DMMA_BLOCKS)
 contract_dmma_kernel(const double2* __restrict__ A, const double2* __restrict__ B,
                      double2* __restrict__ C, int64_t M, int64_t N, int64_t K,
                      const ByteLut* __restrict__ gla, const ByteLut* __restrict__ glb,
@@ -313,13 +316,21 @@ contract_dmma_kernel(const double2* __restrict__ A, const double2* __restrict__ 
         bi[j] = Bs[1][k4 + fk][wn + 8 * j + fr];
         bn[j] = -bi[j];
       }
+      // two passes over the 16 accumulators so that the two products into
+      // one accumulator are 16 DMMAs apart (back to back they stall on the
+      // DMMA latency: "wait" was 30 % of the issue gaps)
 #pragma unroll
       for (int i = 0; i < 4; ++i)
 #pragma unroll
         for (int j = 0; j < 2; ++j) {
           dmma_8x8x4(acc[i][j][0], ar[i], br[j]);
-          dmma_8x8x4(acc[i][j][0], ai[i], bn[j]);
           dmma_8x8x4(acc[i][j][1], ar[i], bi[j]);
+        }
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {
+          dmma_8x8x4(acc[i][j][0], ai[i], bn[j]);
           dmma_8x8x4(acc[i][j][1], ai[i], br[j]);
         }
     }
