@@ -814,6 +814,13 @@ void tc_plan_gemm(TcGemmPlan* p, const __half* Ahi, const __half* Alo, const __h
   static const int spin = env_int("TNB_EPI_SPIN", -1);
   p->epi_spin = spin >= 0 ? spin : 0;
   const int b_rows = p->nb / p->cta_group;
+  p->ahi = Ahi; p->alo = Alo; p->bhi = Bhi; p->blo = Blo;
+  // short-K skinny steps (one K block of <= 32 real, <= 64 real columns):
+  // per 256-row tile the tcgen05 pipeline is a latency chain (TMA -> MMA ->
+  // TMEM -> epilogue, ~1.6 us per tile at M = 2^23, N = 16, K = 8 complex);
+  // the same staged operands through the FP32 pipe stream at HBM speed
+  static const int skinny_env = env_int("TNB_SKINNY", 1);
+  p->skinny = skinny_env && Kp <= 32 && Np <= 64 && p->splits == 1 && M % 256 == 0;
   make_map(p->tmap[0], Ahi, M, Kp, BM);
   make_map(p->tmap[1], Alo, M, Kp, BM);
   make_map(p->tmap[2], Bhi, Np, Kp, b_rows);
@@ -845,7 +852,110 @@ void launch_cg(const TcGemmPlan* p, cudaStream_t s) {
                               p->pace_slack, p->fuse, p->epi_spin));
 }
 
+// Short-K skinny GEMM on the FP32 pipe (TcGemmPlan::skinny): C'[m][0..Np)
+// = alpha * sum_k (Ahi + Alo)[m][k] (Bhi + Blo)[n][k] over the SAME staged
+// operands and with the SAME epilogue (fused staged store or fp32 C, max
+// publication, scale-guard re-run prologue) as gemm_f16x3_kernel.  Kp <= 32
+// means the staged layouts are plain [rows][Kp] (one K block).  One thread
+// per row, warps on 32 consecutive rows (the fused store's lane mapping).
+template <int KP, int NP>
+__global__ void __launch_bounds__(256)
+gemm_skinny_kernel(const __half* __restrict__ ahi, const __half* __restrict__ alo,
+                   const __half* __restrict__ bhi, const __half* __restrict__ blo,
+                   float* __restrict__ C, int64_t M, const ScaleSrc scale_rows,
+                   const ScaleSrc scale_cols, unsigned int* __restrict__ max_out,
+                   const __grid_constant__ FuseOut fo) {
+  if (fo.redo && !fused_redo_fires(fo)) return;
+  __shared__ float bs[NP][KP + 1];
+  for (int i = threadIdx.x; i < NP * KP; i += blockDim.x) {
+    const int n = i / KP, k = i % KP;
+    bs[n][k] = __half2float(bhi[i]) + __half2float(blo[i]);
+  }
+  const float alpha = 1.f / (scale_from_src(scale_rows) * scale_from_src(scale_cols));
+  const float so = fo.mode != 0 ? scale_from_src(fo.scale) : 1.f;
+  __syncthreads();
+  const int lane = threadIdx.x & 31;
+  float vmax = 0.f;
+  for (int64_t row = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; row < M;
+       row += (int64_t)gridDim.x * blockDim.x) {
+    float a[KP];
+#pragma unroll
+    for (int k = 0; k < KP; k += 8) {
+      const uint4 h = *reinterpret_cast<const uint4*>(ahi + row * KP + k);
+      const uint4 l = *reinterpret_cast<const uint4*>(alo + row * KP + k);
+      const __half2* hh = reinterpret_cast<const __half2*>(&h);
+      const __half2* ll = reinterpret_cast<const __half2*>(&l);
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const float2 x = __half22float2(hh[e]), y = __half22float2(ll[e]);
+        a[k + 2 * e] = x.x + y.x;
+        a[k + 2 * e + 1] = x.y + y.y;
+      }
+    }
+    float acc[EPI_COLS];
+#pragma unroll
+    for (int n = 0; n < EPI_COLS; ++n) {
+      float v = 0.f;
+      if (n < NP) {
+#pragma unroll
+        for (int k = 0; k < KP; ++k) v = fmaf(a[k], bs[n][k], v);
+      }
+      acc[n] = v;
+    }
+    float tm = 0.f;
+#pragma unroll
+    for (int n = 0; n < NP; ++n) tm = fmaxf(tm, fabsf(acc[n]));
+    vmax = fmaxf(vmax, tm * alpha);
+    if (fo.mode != 0) {
+      const int64_t row0 = row & ~(int64_t)31;
+      // LUTs through L1 (every block staging them into shared memory measured
+      // 1.75x slower: 2368 blocks x 8 KB of setup)
+      const uint32_t tile = lut_lookup(fo.lut_m, (uint32_t)row0) | lut_lookup(fo.lut_n, 0u);
+      if (fo.mode == 1) fused_store<1>(fo, nullptr, tile, acc, alpha * so, NP / 2, lane);
+      else fused_store<2>(fo, nullptr, tile, acc, alpha * so, NP / 2, lane);
+    } else {
+      float* dst = C + row * NP;
+#pragma unroll
+      for (int n = 0; n < NP; n += 4)
+        *reinterpret_cast<float4*>(dst + n) =
+            make_float4(acc[n] * alpha, acc[n + 1] * alpha, acc[n + 2] * alpha, acc[n + 3] * alpha);
+    }
+  }
+  if (max_out != nullptr) {
+    for (int o = 16; o > 0; o >>= 1) vmax = fmaxf(vmax, __shfl_xor_sync(0xffffffffu, vmax, o));
+    if (lane == 0 && vmax > 0.f) atomicMax(max_out, __float_as_uint(vmax));
+  }
+}
+
+template <int KP, int NP>
+void launch_skinny(const TcGemmPlan* p, cudaStream_t s) {
+  int64_t blocks = (p->M + 255) / 256;
+  if (blocks > 148 * 16) blocks = 148 * 16;
+  gemm_skinny_kernel<KP, NP><<<(unsigned)blocks, 256, 0, s>>>(
+      p->ahi, p->alo, p->bhi, p->blo, p->C, p->M, p->scale_rows, p->scale_cols, p->max_out, p->fuse);
+}
+
 void tc_launch_gemm(const TcGemmPlan* p, cudaStream_t s) {
+  if (p->skinny) {
+    const int key = (int)p->Kp * 1000 + (int)p->Np;
+    switch (key) {
+      case 8008: launch_skinny<8, 8>(p, s); break;
+      case 8016: launch_skinny<8, 16>(p, s); break;
+      case 8032: launch_skinny<8, 32>(p, s); break;
+      case 8064: launch_skinny<8, 64>(p, s); break;
+      case 16008: launch_skinny<16, 8>(p, s); break;
+      case 16016: launch_skinny<16, 16>(p, s); break;
+      case 16032: launch_skinny<16, 32>(p, s); break;
+      case 16064: launch_skinny<16, 64>(p, s); break;
+      case 32008: launch_skinny<32, 8>(p, s); break;
+      case 32016: launch_skinny<32, 16>(p, s); break;
+      case 32032: launch_skinny<32, 32>(p, s); break;
+      case 32064: launch_skinny<32, 64>(p, s); break;
+      default: throw Error(TNB_ERR_ARG, "unsupported skinny GEMM shape");
+    }
+    check_launch("gemm_skinny");
+    return;
+  }
   const int key = p->cta_group * 1000 + p->nb;
   switch (key) {
     case 2256: launch_cg<2, 256>(p, s); break;

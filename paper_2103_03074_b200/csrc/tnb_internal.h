@@ -262,6 +262,11 @@ __device__ __forceinline__ bool fused_redo_fires(const FuseOut& fo) {
 // split products of Ahi/Alo[M][Kp] (fp16, K-major) x Bhi/Blo[Np][Kp].
 struct TcGemmPlan {
   int64_t M = 0, Np = 0, Kp = 0;
+  const __half* ahi = nullptr;   // staged operand planes (also in the TMA maps): the
+  const __half* alo = nullptr;   // short-K skinny path reads them directly
+  const __half* bhi = nullptr;
+  const __half* blo = nullptr;
+  int skinny = 0;                // Kp <= 32 and Np <= 64: FP32-pipe kernel instead of tcgen05
   int splits = 1;
   int chunk_kb = 8;              // promotion chunk (K blocks); see gemm_tc.cu
   int group_m = 16;              // raster band height (m-tiles)
