@@ -4,7 +4,7 @@
 
 DEBUG_LOG: stderr of a run with TNB_DEBUG_GEMM=1 (plan-time shapes, one
 line per tensor-core step, plan order, with its hoisted flag).  NCU_CSV:
-``ncu --csv -k regex:gemm_f16x3 --metrics gpu__time_duration.sum,
+``ncu --csv -k regex:"gemm_(f16x3|skinny)" --metrics gpu__time_duration.sum,
 dram__bytes_read.sum,dram__bytes_write.sum,
 sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_elapsed,
 sm__cycles_elapsed.avg.per_second`` of the same run (guard re-runs off:

@@ -15,7 +15,7 @@ M="gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum,sm__pipe_te
 timeout -s KILL 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 1500 --csv --log-file $O/${T}_launches_c4.csv python bench.py --steps 1 --warmup 1 --slices 1 --no-e2e --no-cpu --reuse 0 --batch-s1 0 --opt-plan 0 --reordered 0 --batch-slices 0 > $O/${T}_launches_c4.log 2>&1; echo "launch list rc=$?"
 for spec in "given c4 2" "reordered c4 16" "batched c4 4"; do
   set -- $spec
-  TNB_SCALE_GUARD_BITS=-1 TNB_DEBUG_GEMM=1 TNB_DIAG_SKIP_WARM=1 timeout -s KILL 900 ncu --metrics $M --clock-control none -k regex:gemm_f16x3 --csv --log-file $O/${T}_gemm_$1.csv python scripts/diag_tree.py $1 $2 $3 > $O/${T}_gemm_$1.log 2>&1; echo "gemm $1 rc=$?"
+  TNB_SCALE_GUARD_BITS=-1 TNB_DEBUG_GEMM=1 TNB_DIAG_SKIP_WARM=1 timeout -s KILL 900 ncu --metrics $M --clock-control none -k regex:"gemm_(f16x3|skinny)" --csv --log-file $O/${T}_gemm_$1.csv python scripts/diag_tree.py $1 $2 $3 > $O/${T}_gemm_$1.log 2>&1; echo "gemm $1 rc=$?"
   python scripts/gemm_roofline.py $O/${T}_gemm_$1.log $O/${T}_gemm_$1.csv > $O/${T}_gemm_$1_roofline.txt 2>&1; tail -4 $O/${T}_gemm_$1_roofline.txt
 done
 if [ -z "$SKIP_FULL" ]; then
