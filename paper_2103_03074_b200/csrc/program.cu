@@ -597,9 +597,10 @@ void plan_tensor_core_steps(Program* P) {
                  P->num_sms);
     s.tc.progress = P->d_progress;
     if (getenv("TNB_DEBUG_GEMM"))
-      fprintf(stderr, "TNB_GEMM step %d M %lld Np %lld Kp %lld cg %d nb %d splits %d fused_out %d rows_fused %d cols_fused %d hoisted %d grid %d\n",
+      fprintf(stderr, "TNB_GEMM step %d M %lld Np %lld Kp %lld cg %d nb %d splits %d fused_out %d rows_fused %d cols_fused %d hoisted %d grid %d skinny %d\n",
               i, (long long)s.M, (long long)Np, (long long)Kp, s.tc.cta_group, s.tc.nb, s.tc.splits,
-              P->tensors[s.out].fuse_role, (int)s.fuse_rows, (int)s.fuse_cols, (int)s.hoisted, s.tc.grid);
+              P->tensors[s.out].fuse_role, (int)s.fuse_rows, (int)s.fuse_cols, (int)s.hoisted, s.tc.grid,
+              s.tc.skinny);
     if (P->tensors[s.out].fuse_role == 0) continue;
     if (s.tc.splits != 1) throw Error(TNB_ERR_SHAPE, "fused staging planned for a split-K step");
     FuseOut& f = s.tc.fuse;

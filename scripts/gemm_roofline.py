@@ -38,14 +38,14 @@ def hbm_peak():
 
 def steps(log):
     pat = re.compile(r"TNB_GEMM step (\d+) M (\d+) Np (\d+) Kp (\d+) cg (\d+) nb (\d+) splits (\d+) "
-                     r"fused_out (\d+) rows_fused (\d+) cols_fused (\d+) hoisted (\d+) grid (\d+)")
+                     r"fused_out (\d+) rows_fused (\d+) cols_fused (\d+) hoisted (\d+) grid (\d+)(?: skinny (\d+))?")
     out = []
     for line in open(log):
         m = pat.search(line)
         if m:
-            v = list(map(int, m.groups()))
+            v = [int(x) if x is not None else 0 for x in m.groups()]
             out.append(dict(step=v[0], M=v[1], Np=v[2], Kp=v[3], cg=v[4], nb=v[5], splits=v[6],
-                            fused=v[7], hoisted=v[10], grid=v[11]))
+                            fused=v[7], hoisted=v[10], grid=v[11], skinny=v[12]))
     return out
 
 
@@ -98,10 +98,12 @@ def main():
         wave = tiles / (math.ceil(tiles / u) * u)
         frac = max(tens, hbm)
         bound = "tensor" if tens >= hbm else "hbm"
-        agg[bound][0] += t
-        agg[bound][1] += t * frac
+        if s.get("skinny"):
+            bound = "hbm*"  # FP32-pipe skinny kernel: judged against HBM
+        agg[bound.rstrip("*")][0] += t
+        agg[bound.rstrip("*")][1] += t * (hbm if s.get("skinny") else frac)
         tot_t += t
-        tot_w += t * frac
+        tot_w += t * (hbm if s.get("skinny") else frac)
         tot_f += fl
         print(f"{s['step']:5d} {s['M']:7d} {s['Np'] // 2:7d} {s['Kp'] // 2:7d} {s['nb']:3d} {s['splits']:2d} "
               f"{t * 1e3:8.3f} {fl / t / 1e12:6.1f} {100 * tens:6.1f} {by / 1e9:6.2f} {by / t / 1e9:6.0f} "
