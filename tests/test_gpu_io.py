@@ -110,3 +110,36 @@ def test_sharded_device_path_two_ranks_one_gpu(gpu, workloads):
         e = rel_l2(a, amps)
         print(f"rank {rank}: sharded amplitudes rel L2 {e:.2e}")
         assert e < 1e-5
+
+
+def test_device_resident_api_validates_and_matches_host_api(gpu, workloads):
+    """engine.head_vector_to_device / tail_amplitudes_to_device: same numbers
+    as the host API; wrong dtype / size / host tensors are rejected."""
+    import torch
+
+    from conftest import measured, rel_l2
+    from paper_2103_03074_b200 import engine as E
+
+    w = workloads("s8")
+    hv = tnb.compute_head_vector(w.tn, w.tree, w.sliced, None, slice_range=(0, 4),
+                                 precision="single")
+    tab = tnb.tail_amplitudes_unchecked(w.tn, w.tree, hv, precision="single")
+    dev = torch.device("cuda", 0)
+    head = torch.empty(hv.data.size, dtype=torch.complex64, device=dev)
+    meta = E.head_vector_to_device(w.tn, w.tree, w.sliced, None, head, slice_range=(0, 4),
+                                   precision="single")
+    assert meta.data is None and meta.slice_range == (0, 4) and meta.provenance == hv.provenance
+    assert np.array_equal(head.cpu().numpy(), hv.data)
+    amps = torch.empty(tab.amplitudes.size, dtype=torch.complex64, device=dev)
+    t2 = E.tail_amplitudes_to_device(w.tn, w.tree, meta, head, amps, precision="single")
+    assert t2.amplitudes is None and t2.open_qubits == tab.open_qubits
+    assert measured(rel_l2(amps.cpu().numpy(), tab.amplitudes)) < 1e-6
+    with pytest.raises(ValueError):
+        E.head_vector_to_device(w.tn, w.tree, w.sliced, None, head.to(torch.complex128),
+                                slice_range=(0, 4), precision="single")
+    with pytest.raises(ValueError):
+        E.head_vector_to_device(w.tn, w.tree, w.sliced, None, head.cpu(), slice_range=(0, 4),
+                                precision="single")
+    with pytest.raises(tnb.ShapeMismatch):
+        E.head_vector_to_device(w.tn, w.tree, w.sliced, None, head[:-1], slice_range=(0, 4),
+                                precision="single")
