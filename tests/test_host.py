@@ -152,3 +152,34 @@ def test_tree_doc_roundtrip(workloads):
                       subtask=w.doc["subtask"])
     with open(os.path.join(ROOT, "tests", "golden", "c4", "order.json")) as fh:
         assert dumps_order(doc) == fh.read()
+
+
+def test_thread_devices_round_robin(monkeypatch):
+    """set_thread_devices: each calling thread gets the next device (the
+    reference CLI's --threads workers spread over the GPUs); an explicit
+    device argument always wins; off -> the process default."""
+    import threading
+
+    from paper_2103_03074_b200 import _lib, engine as E
+
+    monkeypatch.setattr(_lib, "device_count", lambda: 4)
+    monkeypatch.setattr(E, "_thread_counter", [0])
+    E.set_thread_devices(True)
+    try:
+        seen = []
+
+        def work():
+            d1 = E._resolve_device(None)
+            d2 = E._resolve_device(None)  # sticky per thread
+            seen.append((d1, d2, E._resolve_device(7)))
+
+        th = [threading.Thread(target=work) for _ in range(6)]
+        for t in th:
+            t.start()
+        for t in th:
+            t.join()
+        assert all(a == b and c == 7 for a, b, c in seen)
+        assert sorted(a for a, _, _ in seen) == [0, 0, 1, 1, 2, 3]
+    finally:
+        E.set_thread_devices(False)
+    assert E._resolve_device(None) == E._default_device
