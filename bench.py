@@ -205,7 +205,11 @@ def rank_inventory(dist, local):
         dist.all_gather_object(ranks, me)
         comm = {"backend": dist.get_backend(), "size": dist.get_world_size()}
         if comm["backend"] == "nccl":
-            comm["nccl_version"] = ".".join(map(str, torch.cuda.nccl.version()))
+            try:
+                v = torch.cuda.nccl.version()
+                comm["nccl_version"] = ".".join(map(str, v)) if isinstance(v, tuple) else str(v)
+            except Exception:  # noqa: BLE001 - informational only
+                comm["nccl_version"] = None
     active = len({r.get("pci_bus_id", r["device"]) for r in ranks})
     return ranks, active, comm
 
