@@ -1057,6 +1057,11 @@ def main():
     else:
         args.knobs = refuse_diagnostics(args.allow_knobs)
         run_ours(args)
+        import torch.distributed as dist_
+
+        if dist_.is_available() and dist_.is_initialized():
+            dist_.barrier()  # rank 0 has printed; leave together
+            dist_.destroy_process_group()
 
 
 if __name__ == "__main__":
