@@ -187,6 +187,42 @@ def sharded_amplitudes(tn, tree, sliced_indices, s1, slice_range=None, precision
     return dataclasses.replace(tab, amplitudes=amps.astype(want, copy=False))
 
 
+def threaded_head_vector(tn, tree, sliced_indices, s1, slice_range=None, precision="single",
+                         mode="fixed", devices=None):
+    """Single-process multi-GPU ``compute_head_vector``: the aligned ranges
+    of [a, b) (one per entry of ``devices``, default every visible GPU) run
+    in one thread per device, and the partial head vectors are combined
+    with ``reduce_partials``' aligned binary tree (engine.py:428-442) on the
+    host -- in fixed mode bit-identical to one call over [a, b) when the
+    device count is a power of two dividing b - a.  No torch.distributed
+    needed (the reference's ``cli run --threads`` pattern, cli.py:367-380,
+    without the file round trip)."""
+    import concurrent.futures as cf
+
+    from . import _lib, engine
+
+    if devices is None:
+        devices = list(range(max(1, _lib.device_count())))
+    n_e = len(sliced_indices)
+    a, b = slice_range if slice_range is not None else (0, 1 << n_e)
+    spans = aligned_ranges(a, b, len(devices))
+
+    def one(i):
+        lo, hi = spans[i]
+        return engine.compute_head_vector(tn, tree, sliced_indices, s1, slice_range=(lo, hi),
+                                          precision=precision, mode=mode, device=devices[i])
+
+    with cf.ThreadPoolExecutor(max_workers=len(devices)) as pool:
+        parts = list(pool.map(one, range(len(devices))))
+    if mode == "fixed":
+        total = tree_combine([p.data for p in parts], lambda x, y: x + y)
+    else:
+        total = parts[0].data
+        for p in parts[1:]:
+            total = total + p.data
+    return dataclasses.replace(parts[0], data=total, slice_range=(a, b))
+
+
 class NcclComm:
     """The C-ABI collective (``tnb_allreduce_sum``, include/tnb.h) for callers
     that do not run torch.distributed: one communicator per process/device.

@@ -143,3 +143,23 @@ def test_device_resident_api_validates_and_matches_host_api(gpu, workloads):
     with pytest.raises(tnb.ShapeMismatch):
         E.head_vector_to_device(w.tn, w.tree, w.sliced, None, head[:-1], slice_range=(0, 4),
                                 precision="single")
+
+
+@pytest.mark.parametrize("mode", ["fixed", "free"])
+def test_threaded_multi_device_head_vector(gpu, workloads, mode):
+    """distributed.threaded_head_vector: one thread per device (here 4
+    threads sharing the box's GPU), aligned ranges, reduce_partials' tree --
+    fixed mode bit-identical to one call over the whole range."""
+    from conftest import measured, rel_l2
+    from paper_2103_03074_b200.distributed import threaded_head_vector
+
+    w = workloads("s8")
+    full = tnb.compute_head_vector(w.tn, w.tree, w.sliced, None, slice_range=(0, 16),
+                                   precision="single", mode=mode)
+    got = threaded_head_vector(w.tn, w.tree, w.sliced, None, slice_range=(0, 16),
+                               precision="single", mode=mode, devices=[0, 0, 0, 0])
+    assert got.slice_range == (0, 16) and got.provenance == full.provenance
+    if mode == "fixed":
+        assert np.array_equal(got.data, full.data)
+    else:
+        assert measured(rel_l2(got.data, full.data)) < 1e-6
