@@ -110,7 +110,8 @@ class ClockSampler:
 # promotion chunk) changes the executed schedule, so the bench refuses to run
 # with one set unless --allow-knobs marks the line as a diagnostic run.
 _BENCH_ENV_OK = {"TNB_SHARE_DEVICE", "TNB_DIST_BACKEND", "TNB_REF_BUDGET_S", "TNB_PLAN_THREADS",
-                 "TNB_BENCH_FAIL_LEG", "TNB_BENCH_FAIL_RANK", "TNB_BENCH_PROFILE_E2E"}
+                 "TNB_BENCH_FAIL_LEG", "TNB_BENCH_FAIL_LEG_RANK", "TNB_BENCH_FAIL_RANK",
+                 "TNB_BENCH_PROFILE_E2E"}
 
 
 def diagnostic_knobs():
@@ -214,19 +215,6 @@ def rank_inventory(dist, local):
     return ranks, active, comm
 
 
-def agree_min(dist, dev, v: int) -> int:
-    """The minimum of an integer choice over ranks (plan choices made by
-    time-budgeted host searches can differ between ranks; the legs' later
-    collectives need every rank on the same branch)."""
-    if dist is None:
-        return v
-    import torch
-
-    t = torch.tensor([int(v)], device=dev, dtype=torch.int64)
-    dist.all_reduce(t, op=dist.ReduceOp.MIN)
-    return int(t.item())
-
-
 def barrier(dist, local):
     import torch
 
@@ -266,22 +254,52 @@ def cpu_baseline(w, budget_s):
             "est_s_per_slice": est, "tflops": flops / est / 1e12}
 
 
-def _run_leg(name, fn):
-    """An optional bench leg: its failure (e.g. device memory on another box)
-    is reported in the JSON line instead of losing the headline."""
+def _run_leg(name, fn, dist=None, dev=None):
+    """An optional bench leg.  ``fn`` does only rank-local work (no
+    collectives) and returns ``(result, local, finalize)``: ``local`` maps
+    the leg's timings to this rank's values, ``finalize(maxed)`` fills the
+    result from their max over ranks.  The wrapper makes ONE all-reduce per
+    leg with a failure flag in it, so a leg that fails on one rank (e.g.
+    device memory on a shared box) cannot leave the other ranks waiting in a
+    collective: every rank marks it unavailable and the bench continues."""
+    keys, failed, res, local, fin = [], 0, None, {}, None
     try:
-        if os.environ.get("TNB_BENCH_FAIL_LEG") == name:  # test hook
-            raise RuntimeError("injected failure")
-        return fn()
+        if os.environ.get("TNB_BENCH_FAIL_LEG") == name and (
+                os.environ.get("TNB_BENCH_FAIL_LEG_RANK") in (None, os.environ.get("RANK", "0"))):
+            raise RuntimeError("injected failure")  # test hook
+        res, local, fin = fn()
+        keys = sorted(local)
     except Exception as exc:  # noqa: BLE001
+        failed = 1
         print(f"[bench] leg {name} failed: {exc!r}", file=sys.stderr, flush=True)
+        res = {"unavailable": f"{type(exc).__name__}: {str(exc)[:200]}"}
         try:
             from paper_2103_03074_b200 import engine as _E
 
             _E.clear_cache()
         except Exception:  # noqa: BLE001
             pass
-        return {"unavailable": f"{type(exc).__name__}: {str(exc)[:200]}"}
+    maxed = dict(local)
+    if dist is not None:
+        import torch
+
+        # the key set is the leg's own (identical on every rank that got that far);
+        # a failed rank contributes the flag and zeros
+        n = torch.tensor([len(keys)], device=dev, dtype=torch.int64)
+        dist.all_reduce(n, op=dist.ReduceOp.MAX)
+        width = int(n.item())
+        vals = [float(failed)] + [float(local[k]) for k in keys] + [0.0] * (width - len(keys))
+        t = torch.tensor(vals, device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        if t[0].item() > 0 and not failed:
+            res = {"unavailable": "failed on another rank (see its stderr)"}
+            failed = 1
+        maxed = {k: float(t[1 + i].item()) for i, k in enumerate(keys)}
+    if failed or res is None:
+        return res
+    if fin is not None:
+        fin(maxed)
+    return res
 
 
 def run_dry(args):
@@ -456,41 +474,46 @@ def run_ours(args):
     # ---- optional: batched closed-bit assignments --
     # 2^b s1 values in one head pass over the same slices; reported beside
     # the headline as assignment-slices/s (a bigger correlated batch)
+    def sync():
+        torch.cuda.synchronize(local)
+
     def _leg_batched():
-        batched = None
-        if args.batch_s1 > 0:
-            from paper_2103_03074_b200.batched import cheapest_batch_qubits, compute_head_vectors_batched
+        if args.batch_s1 <= 0:
+            return None, {}, None
+        from paper_2103_03074_b200.batched import cheapest_batch_qubits, compute_head_vectors_batched
 
-            qs, ratio = cheapest_batch_qubits(tn, tree, w.sliced, args.batch_s1)
-            closed = sorted(tn.fixed_output_bits)
-            s1_list = []
-            for v in range(1 << len(qs)):
-                s = dict(tn.fixed_output_bits)
-                for i, q in enumerate(qs):
-                    s[q] = (v >> (len(qs) - 1 - i)) & 1
-                s1_list.append("".join(str(s[q]) for q in closed))
-            a = base
+        qs, ratio = cheapest_batch_qubits(tn, tree, w.sliced, args.batch_s1)
+        closed = sorted(tn.fixed_output_bits)
+        s1_list = []
+        for v in range(1 << len(qs)):
+            s = dict(tn.fixed_output_bits)
+            for i, q in enumerate(qs):
+                s[q] = (v >> (len(qs) - 1 - i)) & 1
+            s1_list.append("".join(str(s[q]) for q in closed))
+        a = base
+        compute_head_vectors_batched(tn, tree, w.sliced, s1_list, slice_range=(a, a + S),
+                                     precision="single", device=local)  # compile + warm
+        sync()
+        b_t0 = time.perf_counter()
+        for s_ in range(args.steps):
+            a = base + s_ * S
             compute_head_vectors_batched(tn, tree, w.sliced, s1_list, slice_range=(a, a + S),
-                                         precision="single", device=local)  # compile + warm
-            barrier(dist, local)
-            b_t0 = time.perf_counter()
-            for s_ in range(args.steps):
-                a = base + s_ * S
-                compute_head_vectors_batched(tn, tree, w.sliced, s1_list, slice_range=(a, a + S),
-                                             precision="single", device=local)
-            barrier(dist, local)
-            b_ms = (time.perf_counter() - b_t0) * 1e3 / args.steps
-            batched = {"assignments": len(s1_list), "qubits": qs, "analytic_cost_ratio": ratio,
-                       "ms_per_step": b_ms,
-                       "assignment_slices_per_s": world * S * len(s1_list) / (b_ms / 1e3),
-                       "bitstrings_per_pass": len(s1_list) << len(tn.open_output_indices),
-                       "note": "head vectors of 2^b closed-bit assignments from one contraction with "
-                               "those qubits' output legs open (paper_2103_03074_b200.batched; equal to "
-                               "per-s1 runs, tests/test_batched.py); wall time incl. host copies"}
-            E.clear_cache()
-        return batched
+                                         precision="single", device=local)
+        sync()
+        b_ms = (time.perf_counter() - b_t0) * 1e3 / args.steps
+        batched = {"assignments": len(s1_list), "qubits": qs, "analytic_cost_ratio": ratio,
+                   "bitstrings_per_pass": len(s1_list) << len(tn.open_output_indices),
+                   "note": "head vectors of 2^b closed-bit assignments from one contraction with "
+                           "those qubits' output legs open (paper_2103_03074_b200.batched; equal to "
+                           "per-s1 runs, tests/test_batched.py); wall time incl. host copies"}
+        E.clear_cache()
 
-    batched = _run_leg("batched", _leg_batched)
+        def fin(m):
+            batched["ms_per_step"] = m["b_ms"]
+            batched["assignment_slices_per_s"] = world * S * len(s1_list) / (m["b_ms"] / 1e3)
+        return batched, {"b_ms": b_ms}, fin
+
+    batched = _run_leg("batched", _leg_batched, dist, dev)
 
     # ---- optional: the co-optimised plan of the same network:
     # same head leaves / cut / head vector, head tree + sliced set from
@@ -499,276 +522,265 @@ def run_ours(args):
     # Reported beside the headline: slices of a different plan are a
     # different unit; the comparable figure is the time for ALL slices.
     def _leg_opt_plan():
-        opt_plan = None
         opt_name = next((args.workload + sfx for sfx in ("_opt31_b200", "_opt_b200", "_opt")
                          if os.path.isdir(os.path.join(ROOT, "tests", "golden", args.workload + sfx))), None)
-        if args.opt_plan and opt_name is not None:
-            wo = tnb.load_workload(opt_name)
-            op = E.head_program(wo.tn, wo.tree, wo.sliced, "single", device=local)
-            op.set_timing(2)
-            So = args.opt_slices
-            ob = rank * (args.warmup + args.steps) * So
+        if not (args.opt_plan and opt_name is not None):
+            return None, {}, None
+        wo = tnb.load_workload(opt_name)
+        op = E.head_program(wo.tn, wo.tree, wo.sliced, "single", device=local)
+        op.set_timing(2)
+        So = args.opt_slices
+        ob = rank * (args.warmup + args.steps) * So
+        for s_ in range(args.warmup):
+            op.run_range(ob + s_ * So, ob + (s_ + 1) * So, "fixed", out=hvec.data_ptr())
+        sync()
+        o_ms = o_gemm_ms = o_gemm_flops = 0.0
+        o_launches = 0
+        for s_ in range(args.warmup, args.warmup + args.steps):
+            op.run_range(ob + s_ * So, ob + (s_ + 1) * So, "fixed", out=hvec.data_ptr())
+            t = op.timing()
+            o_ms += t["total_ms"]
+            o_gemm_ms += t["gemm_ms"]
+            o_gemm_flops += t["gemm_flops"]
+            o_launches += t["launches"]
+        opt_plan = {"workload": opt_name, "n_e": wo.n_e,
+                    "target_space": wo.target_space, "flops_per_slice": 8.0 * wo.tc_per_slice,
+                    "gemm_tflops": o_gemm_flops / (o_gemm_ms / 1e3) / 1e12 if o_gemm_ms else 0.0,
+                    "slices_per_step_per_gpu": So, "launches_per_step": o_launches / args.steps,
+                    "planner": wo.doc.get("planner", {}).get("tool"),
+                    "note": "device time of the co-optimised plan's head slices (same network, head "
+                            "leaves, cut and head vector as the reference plan; tests/test_gpu_treeopt.py "
+                            "pins its results to the reference engine run on that plan)"}
+        del op
+        E.clear_cache()
+        # the co-optimised plan's slices in 2^k blocks (slice_batch.py, rank <= 32);
+        # the block width comes from a time-budgeted host search, so ranks may
+        # differ: each runs its own, the line reports the range
+        from paper_2103_03074_b200 import slice_batch as SB
+
+        for ko in (3, 2, 1):
+            try:
+                SB.batched_plan(wo.tn, wo.tree, wo.sliced, ko, max_rank=32)
+                break
+            except (tnb.ShapeMismatch, tnb.TncutError, ValueError):
+                ko = 0
+        bo_ms = 0.0
+        if ko:
+            bo = SB.batched_program(wo.tn, wo.tree, wo.sliced, ko, "single", local, max_rank=32)
+            bo.set_timing(2)
+            ob2 = (1 << (wo.n_e - ko)) // 2 + rank * (args.warmup + args.steps)
             for s_ in range(args.warmup):
-                op.run_range(ob + s_ * So, ob + (s_ + 1) * So, "fixed", out=hvec.data_ptr())
-            barrier(dist, local)
-            o_ms = o_gemm_ms = o_gemm_flops = 0.0
-            o_launches = 0
+                bo.run_range(ob2 + s_, ob2 + s_ + 1, "fixed", out=hvec.data_ptr())
+            sync()
             for s_ in range(args.warmup, args.warmup + args.steps):
-                op.run_range(ob + s_ * So, ob + (s_ + 1) * So, "fixed", out=hvec.data_ptr())
-                t = op.timing()
-                o_ms += t["total_ms"]
-                o_gemm_ms += t["gemm_ms"]
-                o_gemm_flops += t["gemm_flops"]
-                o_launches += t["launches"]
-            if dist is not None:
-                tt_ = torch.tensor([o_ms], device=dev)
-                dist.all_reduce(tt_, op=dist.ReduceOp.MAX)
-                o_ms = float(tt_.item())
-            sps = world * args.steps * So / (o_ms / 1e3)
-            opt_plan = {"workload": opt_name, "n_e": wo.n_e,
-                        "target_space": wo.target_space, "flops_per_slice": 8.0 * wo.tc_per_slice,
-                        "slices_per_s": sps, "contraction_tflops": sps * 8.0 * wo.tc_per_slice / 1e12,
-                        "gemm_tflops": o_gemm_flops / (o_gemm_ms / 1e3) / 1e12 if o_gemm_ms else 0.0,
-                        "slices_per_step_per_gpu": So, "launches_per_step": o_launches / args.steps,
-                        "all_slices_head_s_log2": wo.n_e - math.log2(sps),
-                        "planner": wo.doc.get("planner", {}).get("tool"),
-                        "note": "device time of the co-optimised plan's head slices (same network, head "
-                                "leaves, cut and head vector as the reference plan; tests/test_gpu_treeopt.py "
-                                "pins its results to the reference engine run on that plan)"}
-            del op
+                bo.run_range(ob2 + s_, ob2 + s_ + 1, "fixed", out=hvec.data_ptr())
+                bo_ms += bo.timing()["total_ms"]
+            del bo
             E.clear_cache()
-            # the co-optimised plan's slices in 2^k blocks (slice_batch.py, rank <= 32)
-            from paper_2103_03074_b200 import slice_batch as SB
 
-            for ko in (3, 2, 1):
-                try:
-                    SB.batched_plan(wo.tn, wo.tree, wo.sliced, ko, max_rank=32)
-                    break
-                except (tnb.ShapeMismatch, tnb.TncutError, ValueError):
-                    ko = 0
-            ko = agree_min(dist, dev, ko)  # time-budgeted planning may differ per rank
-            if ko:
-                bo = SB.batched_program(wo.tn, wo.tree, wo.sliced, ko, "single", local, max_rank=32)
-                bo.set_timing(2)
-                ob2 = (1 << (wo.n_e - ko)) // 2 + rank * (args.warmup + args.steps)
-                for s_ in range(args.warmup):
-                    bo.run_range(ob2 + s_, ob2 + s_ + 1, "fixed", out=hvec.data_ptr())
-                barrier(dist, local)
-                bo_ms = 0.0
-                for s_ in range(args.warmup, args.warmup + args.steps):
-                    bo.run_range(ob2 + s_, ob2 + s_ + 1, "fixed", out=hvec.data_ptr())
-                    bo_ms += bo.timing()["total_ms"]
-                if dist is not None:
-                    tt_ = torch.tensor([bo_ms], device=dev)
-                    dist.all_reduce(tt_, op=dist.ReduceOp.MAX)
-                    bo_ms = float(tt_.item())
-                bsps = world * args.steps * (1 << ko) / (bo_ms / 1e3)
-                opt_plan["batched"] = {"batch_log2": ko, "slices_per_s": bsps,
+        def fin(m):
+            sps = world * args.steps * So / (m["o_ms"] / 1e3)
+            opt_plan.update(slices_per_s=sps, contraction_tflops=sps * 8.0 * wo.tc_per_slice / 1e12,
+                            all_slices_head_s_log2=wo.n_e - math.log2(sps))
+            k_lo, k_hi = int(-m["neg_ko"]), int(m["ko"])
+            if k_lo > 0 and m["bo_ms"] > 0:
+                bsps = world * args.steps * (1 << k_lo) / (m["bo_ms"] / 1e3)
+                opt_plan["batched"] = {"batch_log2": k_lo, "slices_per_s": bsps,
                                        "all_slices_head_s_log2": wo.n_e - math.log2(bsps)}
-                del bo
-                E.clear_cache()
-        return opt_plan
+                if k_hi != k_lo:
+                    opt_plan["batched"]["note"] = f"block width differed across ranks ({k_lo}..{k_hi})"
+        return opt_plan, {"o_ms": o_ms, "bo_ms": bo_ms, "ko": float(ko), "neg_ko": -float(ko)}, fin
 
-    opt_plan = _run_leg("opt_plan", _leg_opt_plan)
+    opt_plan = _run_leg("opt_plan", _leg_opt_plan, dist, dev)
 
     # ---- optional: the SAME slices (reference sliced set, same masks, same
     # partial head vectors) through a re-ordered head tree
     # (treeopt keep_slices; tests/golden/<workload>_reordered).  Reported
     # beside the headline, which executes the reference tree as given.
     def _leg_reordered():
-        reordered = None
         ro_name = args.workload + "_reordered"
-        if args.reordered and os.path.isdir(os.path.join(ROOT, "tests", "golden", ro_name)):
-            wr = tnb.load_workload(ro_name)
-            assert wr.sliced == w.sliced
-            # the re-ordered tree with its small steps clustered, as set_reorder runs it
-            from paper_2103_03074_b200.planner import cluster_small_steps
+        if not (args.reordered and os.path.isdir(os.path.join(ROOT, "tests", "golden", ro_name))):
+            return None, {}, None
+        wr = tnb.load_workload(ro_name)
+        assert wr.sliced == w.sliced
+        # the re-ordered tree with its small steps clustered, as set_reorder runs it
+        from paper_2103_03074_b200.planner import cluster_small_steps
 
-            _hl, _hs, _, _, _cut = E._split(wr.tn, wr.tree)
-            _steps = cluster_small_steps({n: wr.tn.nodes[n].indices for n in _hl}, _hs,
-                                         frozenset(wr.sliced))
-            rp = E.get_program(E._leaf_entries(wr.tn, _hl), E._steps_tuples(_steps), list(wr.sliced),
-                               sorted(_cut), "single", local)
-            rp.set_timing(2)
-            Sr = args.reordered_slices
-            rb = rank * (args.warmup + args.steps) * Sr
-            for s_ in range(args.warmup):
-                rp.run_range(rb + s_ * Sr, rb + (s_ + 1) * Sr, "fixed", out=hvec.data_ptr())
-            barrier(dist, local)
-            r_ms = r_gemm_ms = r_gemm_flops = 0.0
-            r_launches = 0
-            for s_ in range(args.warmup, args.warmup + args.steps):
-                rp.run_range(rb + s_ * Sr, rb + (s_ + 1) * Sr, "fixed", out=hvec.data_ptr())
-                t = rp.timing()
-                r_ms += t["total_ms"]
-                r_gemm_ms += t["gemm_ms"]
-                r_gemm_flops += t["gemm_flops"]
-                r_launches += t["launches"]
-            if dist is not None:
-                tt_ = torch.tensor([r_ms], device=dev)
-                dist.all_reduce(tt_, op=dist.ReduceOp.MAX)
-                r_ms = float(tt_.item())
-            rsps = world * args.steps * Sr / (r_ms / 1e3)
-            reordered = {"workload": ro_name, "slices_per_s": rsps,
-                         "executed_flops_per_slice": 8.0 * wr.tc_per_slice,
-                         "executed_tflops": rsps * 8.0 * wr.tc_per_slice / 1e12,
-                         "gemm_tflops": r_gemm_flops / (r_gemm_ms / 1e3) / 1e12 if r_gemm_ms else 0.0,
-                         "slices_per_step_per_gpu": Sr, "launches_per_step": r_launches / args.steps,
-                         "note": "the reference plan's own slices (same sliced set and masks, same partial "
-                                 "head vectors: tests/test_gpu_treeopt.py) with the head tree re-ordered by "
-                                 "treeopt (keep_slices, exact subtree DP + B200 polish); executed FLOPs "
-                                 "are the re-ordered tree's"}
-            del rp
-            E.clear_cache()
-            # the same through the public API (set_reorder; host buffers, leaves
-            # H2D and the head vector D2H every call)
-            tnb.set_reorder(True)
-            try:
-                a0 = base + total_slices  # slices beyond the headline subset
-                tnb.compute_head_vector(tn, tree, w.sliced, None, slice_range=(a0, a0 + Sr),
-                                        precision="single", device=local)  # plan + compile
-                barrier(dist, local)
-                e_t0 = time.perf_counter()
-                for s_ in range(args.steps):
-                    a = a0 + (s_ + 1) * Sr
-                    hv = tnb.compute_head_vector(tn, tree, w.sliced, None, slice_range=(a, a + Sr),
-                                                 precision="single", device=local)
-                barrier(dist, local)
-                re_ms = (time.perf_counter() - e_t0) * 1e3
-            finally:
-                tnb.set_reorder(False)
-            reordered["e2e_api_slices_per_s"] = world * args.steps * Sr / (re_ms / 1e3)
-            E.clear_cache()
-        return reordered
+        _hl, _hs, _, _, _cut = E._split(wr.tn, wr.tree)
+        _steps = cluster_small_steps({n: wr.tn.nodes[n].indices for n in _hl}, _hs,
+                                     frozenset(wr.sliced))
+        rp = E.get_program(E._leaf_entries(wr.tn, _hl), E._steps_tuples(_steps), list(wr.sliced),
+                           sorted(_cut), "single", local)
+        rp.set_timing(2)
+        Sr = args.reordered_slices
+        rb = rank * (args.warmup + args.steps) * Sr
+        for s_ in range(args.warmup):
+            rp.run_range(rb + s_ * Sr, rb + (s_ + 1) * Sr, "fixed", out=hvec.data_ptr())
+        sync()
+        r_ms = r_gemm_ms = r_gemm_flops = 0.0
+        r_launches = 0
+        for s_ in range(args.warmup, args.warmup + args.steps):
+            rp.run_range(rb + s_ * Sr, rb + (s_ + 1) * Sr, "fixed", out=hvec.data_ptr())
+            t = rp.timing()
+            r_ms += t["total_ms"]
+            r_gemm_ms += t["gemm_ms"]
+            r_gemm_flops += t["gemm_flops"]
+            r_launches += t["launches"]
+        reordered = {"workload": ro_name,
+                     "executed_flops_per_slice": 8.0 * wr.tc_per_slice,
+                     "gemm_tflops": r_gemm_flops / (r_gemm_ms / 1e3) / 1e12 if r_gemm_ms else 0.0,
+                     "slices_per_step_per_gpu": Sr, "launches_per_step": r_launches / args.steps,
+                     "note": "the reference plan's own slices (same sliced set and masks, same partial "
+                             "head vectors: tests/test_gpu_treeopt.py) with the head tree re-ordered by "
+                             "treeopt (keep_slices, exact subtree DP + B200 polish); executed FLOPs "
+                             "are the re-ordered tree's"}
+        del rp
+        E.clear_cache()
+        # the same through the public API (set_reorder; host buffers, leaves
+        # H2D and the head vector D2H every call)
+        tnb.set_reorder(True)
+        try:
+            a0 = base + total_slices  # slices beyond the headline subset
+            tnb.compute_head_vector(tn, tree, w.sliced, None, slice_range=(a0, a0 + Sr),
+                                    precision="single", device=local)  # plan + compile
+            sync()
+            e_t0 = time.perf_counter()
+            for s_ in range(args.steps):
+                a = a0 + (s_ + 1) * Sr
+                tnb.compute_head_vector(tn, tree, w.sliced, None, slice_range=(a, a + Sr),
+                                        precision="single", device=local)
+            sync()
+            re_ms = (time.perf_counter() - e_t0) * 1e3
+        finally:
+            tnb.set_reorder(False)
+        E.clear_cache()
 
-    reordered = _run_leg("reordered", _leg_reordered)
+        def fin(m):
+            rsps = world * args.steps * Sr / (m["r_ms"] / 1e3)
+            reordered.update(slices_per_s=rsps, executed_tflops=rsps * 8.0 * wr.tc_per_slice / 1e12,
+                             e2e_api_slices_per_s=world * args.steps * Sr / (m["re_ms"] / 1e3))
+        return reordered, {"r_ms": r_ms, "re_ms": re_ms}, fin
+
+    reordered = _run_leg("reordered", _leg_reordered, dist, dev)
 
     # ---- optional: batched slices (slice_batch.py): 2^k aligned slices of the
     # SAME plan per contraction (the k lowest-mask-bit sliced indices
     # un-sliced), head tree re-ordered for the reduced sliced set
     def _leg_batched_slices():
-        batched_slices = None
-        if args.batch_slices > 0:
-            from paper_2103_03074_b200 import slice_batch as SB
+        if args.batch_slices <= 0:
+            return None, {}, None
+        from paper_2103_03074_b200 import slice_batch as SB
 
-            kb = args.batch_slices
-            while True:  # the largest k <= --batch-slices whose intermediates fit rank 32
-                try:
-                    steps_b, reduced_b, sc_b = SB.batched_plan(tn, tree, w.sliced, kb)
-                    break
-                except tnb.ShapeMismatch:
-                    kb -= 1
-                    if kb == 0:
-                        raise
-            kb = agree_min(dist, dev, kb)  # every rank runs the same block width
-            bp = SB.batched_program(tn, tree, w.sliced, kb, "single", local)
-            bp.set_timing(2)
-            Bb = 4  # blocks per step
-            # blocks beyond the headline subset, disjoint per rank
-            bb = ((world * total_slices) >> kb) + 1 + rank * (args.warmup + args.steps) * Bb
-            for s_ in range(args.warmup):
-                bp.run_range(bb + s_ * Bb, bb + (s_ + 1) * Bb, "fixed", out=hvec.data_ptr())
-            barrier(dist, local)
-            b_ms = b_gemm_ms = b_gemm_flops = 0.0
-            for s_ in range(args.warmup, args.warmup + args.steps):
-                bp.run_range(bb + s_ * Bb, bb + (s_ + 1) * Bb, "fixed", out=hvec.data_ptr())
-                t = bp.timing()
-                b_ms += t["total_ms"]
-                b_gemm_ms += t["gemm_ms"]
-                b_gemm_flops += t["gemm_flops"]
-            if dist is not None:
-                tt_ = torch.tensor([b_ms], device=dev)
-                dist.all_reduce(tt_, op=dist.ReduceOp.MAX)
-                b_ms = float(tt_.item())
-            from paper_2103_03074_b200.planner import step_mults
-
-            mb, _ = step_mults({n: tn.nodes[n].indices for n in hl}, steps_b, frozenset(reduced_b))
-            sps_b = world * args.steps * Bb * (1 << kb) / (b_ms / 1e3)
-            batched_slices = {"batch_log2": kb, "slices_per_s": sps_b, "max_rank": sc_b,
-                              "executed_flops_per_slice": 8.0 * mb / (1 << kb),
-                              "executed_tflops": sps_b * 8.0 * mb / (1 << kb) / 1e12,
-                              "gemm_tflops": b_gemm_flops / (b_gemm_ms / 1e3) / 1e12 if b_gemm_ms else 0.0,
-                              "speedup_vs_headline": None,
-                              "note": "the reference plan's slices, 2^k aligned slices per contraction "
-                                      "(lowest-mask-bit sliced indices un-sliced, tree re-ordered; "
-                                      "tests/test_gpu_slice_batch.py); executed FLOPs are the batched tree's"}
-            del bp
-            E.clear_cache()
-            # the same through the public API (set_slice_batch; host buffers)
-            tnb.set_slice_batch(kb)
+        kb = args.batch_slices
+        while True:  # the largest k <= --batch-slices whose intermediates fit rank 32
             try:
-                a0 = (bb + (args.warmup + args.steps) * Bb) << kb
-                tnb.compute_head_vector(tn, tree, w.sliced, None, slice_range=(a0, a0 + (Bb << kb)),
-                                        precision="single", device=local)  # plan + compile
-                barrier(dist, local)
-                e_t0 = time.perf_counter()
-                for s_ in range(args.steps):
-                    a = a0 + ((s_ + 1) * Bb << kb)
-                    tnb.compute_head_vector(tn, tree, w.sliced, None, slice_range=(a, a + (Bb << kb)),
-                                            precision="single", device=local)
-                barrier(dist, local)
-                be_ms = (time.perf_counter() - e_t0) * 1e3
-            finally:
-                tnb.set_slice_batch(0)
-            batched_slices["e2e_api_slices_per_s"] = world * args.steps * (Bb << kb) / (be_ms / 1e3)
-            E.clear_cache()
-        return batched_slices
+                steps_b, reduced_b, sc_b = SB.batched_plan(tn, tree, w.sliced, kb)
+                break
+            except tnb.ShapeMismatch:
+                kb -= 1
+                if kb == 0:
+                    raise
+        bp = SB.batched_program(tn, tree, w.sliced, kb, "single", local)
+        bp.set_timing(2)
+        Bb = 4  # blocks per step
+        # blocks beyond the headline subset, disjoint per rank
+        bb = ((world * total_slices) >> kb) + 1 + rank * (args.warmup + args.steps) * Bb
+        for s_ in range(args.warmup):
+            bp.run_range(bb + s_ * Bb, bb + (s_ + 1) * Bb, "fixed", out=hvec.data_ptr())
+        sync()
+        b_ms = b_gemm_ms = b_gemm_flops = 0.0
+        for s_ in range(args.warmup, args.warmup + args.steps):
+            bp.run_range(bb + s_ * Bb, bb + (s_ + 1) * Bb, "fixed", out=hvec.data_ptr())
+            t = bp.timing()
+            b_ms += t["total_ms"]
+            b_gemm_ms += t["gemm_ms"]
+            b_gemm_flops += t["gemm_flops"]
+        from paper_2103_03074_b200.planner import step_mults
 
-    batched_slices = _run_leg("batched_slices", _leg_batched_slices)
+        mb, _ = step_mults({n: tn.nodes[n].indices for n in hl}, steps_b, frozenset(reduced_b))
+        batched_slices = {"batch_log2": kb, "max_rank": sc_b,
+                          "executed_flops_per_slice": 8.0 * mb / (1 << kb),
+                          "gemm_tflops": b_gemm_flops / (b_gemm_ms / 1e3) / 1e12 if b_gemm_ms else 0.0,
+                          "speedup_vs_headline": None,
+                          "note": "the reference plan's slices, 2^k aligned slices per contraction "
+                                  "(lowest-mask-bit sliced indices un-sliced, tree re-ordered; "
+                                  "tests/test_gpu_slice_batch.py); executed FLOPs are the batched tree's"}
+        del bp
+        E.clear_cache()
+        # the same through the public API (set_slice_batch; host buffers)
+        tnb.set_slice_batch(kb)
+        try:
+            a0 = (bb + (args.warmup + args.steps) * Bb) << kb
+            tnb.compute_head_vector(tn, tree, w.sliced, None, slice_range=(a0, a0 + (Bb << kb)),
+                                    precision="single", device=local)  # plan + compile
+            sync()
+            e_t0 = time.perf_counter()
+            for s_ in range(args.steps):
+                a = a0 + ((s_ + 1) * Bb << kb)
+                tnb.compute_head_vector(tn, tree, w.sliced, None, slice_range=(a, a + (Bb << kb)),
+                                        precision="single", device=local)
+            sync()
+            be_ms = (time.perf_counter() - e_t0) * 1e3
+        finally:
+            tnb.set_slice_batch(0)
+        E.clear_cache()
+
+        def fin(m):
+            sps_b = world * args.steps * Bb * (1 << kb) / (m["b_ms"] / 1e3)
+            batched_slices.update(slices_per_s=sps_b,
+                                  executed_tflops=sps_b * 8.0 * mb / (1 << kb) / 1e12,
+                                  e2e_api_slices_per_s=world * args.steps * (Bb << kb) / (m["be_ms"] / 1e3))
+            if int(-m["neg_kb"]) != int(m["kb"]):
+                batched_slices["note_ranks"] = (f"block width differed across ranks "
+                                                f"({int(-m['neg_kb'])}..{int(m['kb'])})")
+        return batched_slices, {"b_ms": b_ms, "be_ms": be_ms, "kb": float(kb), "neg_kb": -float(kb)}, fin
+
+    batched_slices = _run_leg("batched_slices", _leg_batched_slices, dist, dev)
 
     # ---- optional: double precision (the reference's default, engine.py:248):
     # the same slices on the fp64 path (DMMA / FMA; tcgen05 has no fp64 kind)
     def _leg_double():
         if not args.double:
-            return None
+            return None, {}, None
         E.clear_cache()
         dp = E.head_program(tn, tree, w.sliced, "double", device=local)
         dp.set_timing(2)
         d0 = base
         dp.run_range(d0, d0 + 1, "fixed")  # compile + warm
-        barrier(dist, local)
+        sync()
         d_ms = 0.0
         for s_ in range(args.double):
             dp.run_range(d0 + 1 + s_, d0 + 2 + s_, "fixed")
             d_ms += dp.timing()["total_ms"]
-        if dist is not None:
-            tt_ = torch.tensor([d_ms], device=dev)
-            dist.all_reduce(tt_, op=dist.ReduceOp.MAX)
-            d_ms = float(tt_.item())
-        sps = world * args.double / (d_ms / 1e3)
         del dp
         E.clear_cache()
-        return {"slices_per_s": sps, "contraction_tflops": sps * 8.0 * w.tc_per_slice / 1e12,
-                "slices_per_gpu": args.double,
-                "note": "precision='double' (complex128; the reference's default) on the fp64 path "
-                        "(DMMA mma.sync m8n8k4 for the big steps, FMA for the rest), same slices and "
-                        "tree as the headline; device time"}
+        res = {"slices_per_gpu": args.double,
+               "note": "precision='double' (complex128; the reference's default) on the fp64 path "
+                       "(DMMA mma.sync m8n8k4 for the big steps, FMA for the rest), same slices and "
+                       "tree as the headline; device time"}
 
-    double_leg = _run_leg("double", _leg_double)
+        def fin(m):
+            sps = world * args.double / (m["d_ms"] / 1e3)
+            res.update(slices_per_s=sps, contraction_tflops=sps * 8.0 * w.tc_per_slice / 1e12)
+        return res, {"d_ms": d_ms}, fin
+
+    double_leg = _run_leg("double", _leg_double, dist, dev)
 
     # ---- optional: cross-slice reuse (TNB_FLAG_REUSE_SLICES) -- reported beside the
     # headline, NOT as it: it skips re-computing results whose mask bits did not change
-    reuse = None
-    if args.reuse:
+    def _leg_reuse():
+        if not args.reuse:
+            return None, {}, None
         from paper_2103_03074_b200 import _lib as L
 
-        import gc
-
-        E.clear_cache()
-        del head, tail, step  # the closure holds the programs too
-        gc.collect()
-        try:
-            rprog = E.head_program(tn, tree, w.sliced, "single", device=local,
-                                   flags=L.TNB_FLAG_REUSE_SLICES)
-        except RuntimeError as exc:  # e.g. the dedicated cache buffers exceed HBM
-            rprog = None
-            reuse = {"unavailable": str(exc)[:200]}
-    if args.reuse and rprog is not None:
+        # e.g. the dedicated cache buffers exceeding HBM -> the leg is unavailable
+        rprog = E.head_program(tn, tree, w.sliced, "single", device=local,
+                               flags=L.TNB_FLAG_REUSE_SLICES)
         rprog.set_timing(2)
         rbase = base + total_slices  # fresh slices beyond the headline subset
         for s in range(args.warmup):
             rprog.run_range(rbase + s * S, rbase + (s + 1) * S, "fixed", out=hvec.data_ptr())
-        barrier(dist, local)
+        sync()
         r_ms = r_gemm_ms = r_gemm_flops = 0.0
         r_reused = 0
         for s in range(args.warmup, args.warmup + args.steps):
@@ -778,13 +790,27 @@ def run_ours(args):
             r_gemm_ms += t["gemm_ms"]
             r_gemm_flops += t["gemm_flops"]
             r_reused += t["steps_reused"]
-        reuse = {"value": world * args.steps * S / (r_ms / 1e3), "unit": "slices/s",
-                 "executed_gemm_tflops": r_gemm_flops / (r_gemm_ms / 1e3) / 1e12 if r_gemm_ms else 0,
-                 "executed_flop_fraction": r_gemm_flops / (args.steps * S * 8.0 * w.tc_per_slice),
-                 "steps_reused": r_reused, "cache_bytes": int(rprog.info.reuse_bytes),
-                 "note": "head slices with TNB_FLAG_REUSE_SLICES: steps whose mask bits did not "
-                         "change between consecutive slices are not recomputed (results "
-                         "bit-identical, tests/test_gpu_parity.py); tail excluded"}
+        res = {"unit": "slices/s",
+               "executed_gemm_tflops": r_gemm_flops / (r_gemm_ms / 1e3) / 1e12 if r_gemm_ms else 0,
+               "executed_flop_fraction": r_gemm_flops / (args.steps * S * 8.0 * w.tc_per_slice),
+               "steps_reused": r_reused, "cache_bytes": int(rprog.info.reuse_bytes),
+               "note": "head slices with TNB_FLAG_REUSE_SLICES: steps whose mask bits did not "
+                       "change between consecutive slices are not recomputed (results "
+                       "bit-identical, tests/test_gpu_parity.py); tail excluded"}
+        del rprog
+        E.clear_cache()
+
+        def fin(m):
+            res["value"] = world * args.steps * S / (m["r_ms"] / 1e3)
+        return res, {"r_ms": r_ms}, fin
+
+    if args.reuse:
+        import gc
+
+        E.clear_cache()
+        del head, tail, step  # the closure holds the programs too
+        gc.collect()
+    reuse = _run_leg("reuse", _leg_reuse, dist, dev)
 
     if rank != 0:
         return

@@ -77,7 +77,7 @@ def test_bench_two_ranks_share_one_gpu(gpu):
     over ranks, rank 0's line."""
     line = _run(["--gpus", "2", "--steps", "1", "--warmup", "1", "--slices", "1", "--no-cpu",
                  "--no-e2e", "--reuse", "0", "--opt-plan", "0", "--reordered", "0",
-                 "--batch-slices", "0", "--batch-s1", "0"],
+                 "--batch-slices", "0", "--batch-s1", "0", "--double", "0"],
                 {"TNB_SHARE_DEVICE": "1", "TNB_DIST_BACKEND": "gloo"}, 900)
     assert line["n_gpus"] == 2 and line["communicator"]["size"] == 2
     assert line["gpus_active"] == 1 and line["value"] > 0
@@ -131,3 +131,17 @@ def test_reference_arm_budget_caps_the_timed_slices(monkeypatch):
                  "--ref-budget-s", "0"], {}, 300)
     assert line["steps"] == 1 and line["requested_steps"] == 50
     assert "fit" in line["steps_note"]
+
+
+@pytest.mark.gpu
+def test_bench_leg_failing_on_one_rank_does_not_hang(gpu):
+    """A leg that fails on rank 1 only (injected; e.g. device memory) is
+    reported unavailable on every rank and the other legs still run: the
+    legs' timings meet in one all-reduce per leg with a failure flag."""
+    line = _run(["--gpus", "2", "--workload", "c2", "--steps", "1", "--warmup", "1", "--slices", "1",
+                 "--no-cpu", "--no-e2e", "--reuse", "0", "--opt-plan", "0", "--reordered", "0",
+                 "--batch-slices", "2", "--batch-s1", "0", "--double", "1"],
+                {"TNB_SHARE_DEVICE": "1", "TNB_DIST_BACKEND": "gloo",
+                 "TNB_BENCH_FAIL_LEG": "batched_slices", "TNB_BENCH_FAIL_LEG_RANK": "1"}, 900)
+    assert "unavailable" in line["batched_slices"]
+    assert line["double_precision"]["slices_per_s"] > 0
