@@ -13,6 +13,12 @@ vector.  Ranks own disjoint aligned slice ranges of a fixed subset
 
     python bench.py [--gpus N --steps K --warmup W]      # this executor
     python bench.py --impl reference ...                 # reference CPU path
+
+Without a launcher, ``--gpus N`` spawns N rank processes (torchrun's env);
+under torchrun it uses the launcher's ranks.  Beside the headline the line
+carries optional legs (batched s1, co-optimised plan, re-ordered tree,
+batched slices, double precision, cross-slice reuse), each reported
+separately, and the reference engine's own CPU time (``cpu_baseline``).
 """
 
 from __future__ import annotations
@@ -1048,7 +1054,7 @@ def main():
     ap.add_argument("--allow-knobs", action="store_true",
                     help="run with TNB_* executor knobs set (the line is marked diagnostic)")
     ap.add_argument("--ref-budget-s", type=float, default=float(os.environ.get("TNB_REF_BUDGET_S", "420")),
-                    help="wall budget of the reference arm's timed slices (each ~70-110 s at C4)")
+                    help="wall budget of the reference arm's timed slices (each ~62-69 s at C4 on 16 cores)")
     ap.add_argument("--workload", default=WORKLOAD)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
