@@ -1,7 +1,7 @@
 """End to end on the public API (what a user of the reference does):
 plan -> head slices -> tail amplitudes -> XEB, on the frozen C4 workload.
 
-    python examples/c4_end_to_end.py [--slices 64] [--plan given|reordered|batched]
+    python examples/c4_end_to_end.py [--slices 64] [--plan given|reordered|batched] [--tsv amps.tsv]
 
 * ``given``: the reference plan's tree as is (the bench headline path);
 * ``reordered``: same slices, re-ordered head tree (``set_reorder``);
@@ -27,6 +27,7 @@ def main() -> None:
     ap = argparse.ArgumentParser()
     ap.add_argument("--slices", type=int, default=64)
     ap.add_argument("--plan", choices=["given", "reordered", "batched"], default="batched")
+    ap.add_argument("--tsv", default=None, help="write the 2^20 rows as the reference's TSV")
     args = ap.parse_args()
     w = tnb.load_workload("c4")
     tnb.set_reorder(args.plan == "reordered")
@@ -44,6 +45,12 @@ def main() -> None:
           f"{len(tab.amplitudes)} amplitudes, first bitstring {tab.bitstring(0)}")
     print(f"linear XEB of this partial (a 2^-{w.n_e - int(np.log2(args.slices))} fraction of the "
           f"slice sum): {analytics.xeb(probs, 53).f_xeb:.6f}")
+    if args.tsv:
+        from paper_2103_03074_b200 import io
+
+        t3 = time.perf_counter()
+        io.write_amplitude_tsv(args.tsv, tab)  # byte-identical to tncut's writer
+        print(f"{len(tab.amplitudes)} TSV rows in {time.perf_counter() - t3:.2f} s -> {args.tsv}")
 
 
 if __name__ == "__main__":
