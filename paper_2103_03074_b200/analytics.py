@@ -64,12 +64,13 @@ except Exception:  # pragma: no cover - tncut absent (e.g. the GPU box)
         pt_density: float
 
 
-_device = 0
+_device = None  # None: torch's current device (the rank's GPU under torchrun)
 
 
-def set_device(device: int) -> None:
+def set_device(device) -> None:
+    """Device for host (numpy) inputs; None = torch's current device."""
     global _device
-    _device = int(device)
+    _device = None if device is None else int(device)
 
 
 class _DevProbs:
@@ -95,7 +96,7 @@ class _DevProbs:
                 self.t = t.clone() if (copy and t.data_ptr() == probs.data_ptr()) else t.contiguous()
         else:
             host = np.ascontiguousarray(np.asarray(probs, dtype=float).reshape(-1))
-            self.device = _device
+            self.device = _device if _device is not None else torch.cuda.current_device()
             self.t = torch.from_numpy(host).to(torch.device("cuda", self.device))
         torch.cuda.synchronize(self.t.device)
         self.n = int(self.t.numel())
